@@ -1,0 +1,169 @@
+/*
+ * torus.h -- C-ABI of libtorus.so, the B200-native 2D-Torus all-reduce.
+ *
+ * Method (Sec. 2.2, Mikami et al., arXiv 1811.05233): the N = X*Y GPUs are
+ * arranged in a 2D grid; "all-reduce consists of three steps: reduce-scatter, all-reduce,
+ * and all-gather ... Firstly, reduce-scatter is performed horizontally. Then, all-reduce
+ * is performed vertically. Finally, all-gather is performed horizontally."  The problem
+ * it solves is the data-parallel step that must "synchronize and average gradients
+ * across participating GPUs"; gradients are communicated in FP16
+ * (PAPER.md:121).
+ *
+ * Ranks are row-major: rank = row * X + col, X = GPUs per row ("horizontal"),
+ * Y = GPUs per column ("vertical")  (PAPER.md:70 defines X and Y; row-major is the
+ * reading R1 in DESIGN.md).
+ *
+ * All functions return a torus_result_t (0 = TORUS_OK) unless stated.  No function
+ * takes or returns a torch type; pointers are plain host or device pointers as stated.
+ * Nothing here is thread-safe per comm; distinct comms may be used from distinct threads.
+ */
+#ifndef TORUS_H
+#define TORUS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define TORUS_API __attribute__((visibility("default")))
+#else
+#define TORUS_API
+#endif
+
+#define TORUS_VERSION_MAJOR 0
+#define TORUS_VERSION_MINOR 1
+
+typedef struct torus_comm* torus_comm_t;
+typedef void* torus_stream_t; /* a cudaStream_t (CUstream); NULL = the legacy default stream */
+
+typedef enum { TORUS_F32 = 0, TORUS_F16 = 1, TORUS_BF16 = 2, TORUS_I32 = 3 } torus_dtype_t;
+typedef enum { TORUS_SUM = 0, TORUS_MEAN = 1 } torus_op_t;
+
+typedef enum {
+    TORUS_OK = 0,
+    TORUS_ERR_INVALID_ARG = 1, /* null pointer, bad enum, count overflow, misaligned buffer  */
+    TORUS_ERR_GRID = 2,        /* X*Y != world, rank outside [0, world), grid too large     */
+    TORUS_ERR_UNSUPPORTED = 3, /* e.g. wire wider than the buffer, i32 with a float wire     */
+    TORUS_ERR_CUDA = 4,        /* an underlying CUDA call failed; see torus_last_error()     */
+    TORUS_ERR_PEER = 5,        /* no P2P access to a peer, or IPC open failed                */
+    TORUS_ERR_TIMEOUT = 6,     /* async: a device spin-wait exceeded its budget (watchdog)   */
+    TORUS_ERR_MISMATCH = 7     /* peers disagree on the call (count/dtype/op/config)         */
+} torus_result_t;
+
+/* An exported workspace slab: the 64-byte cudaIpcMemHandle_t plus its size in bytes. */
+typedef struct {
+    unsigned char bytes[64];
+    unsigned long long offset; /* always 0 in this version                                 */
+    unsigned long long size;   /* slab size in bytes; must be equal on every rank          */
+} torus_ipc_handle_t;
+
+/* ---------------------------------------------------------------------------------------
+ * Setup (multi-process: one process per GPU)
+ * ------------------------------------------------------------------------------------- */
+
+/* Allocate this rank's symmetric workspace slab on `device` (cudaMalloc, zeroed) and
+ * export it for CUDA IPC.  `bytes` = 0 selects the default (env TORUS_WS_BYTES, else
+ * 320 MiB), enough to reduce the 25.6M-element fp16 ResNet-50 buffer in a single round
+ * on every grid.  The slab is owned by the library and adopted by the comm that
+ * torus_comm_init builds from it; release it with torus_workspace_release only if no
+ * comm was created.  out: host pointer, written on success. */
+TORUS_API int torus_workspace_alloc(int device, size_t bytes, torus_ipc_handle_t* out);
+TORUS_API int torus_workspace_release(const torus_ipc_handle_t* h);
+
+/* Build this rank's communicator (collective in the sense that every rank must call it
+ * with the same world, X, Y and the same handle array before any rank calls
+ * torus_allreduce).  ipc_handles: host array [world] of every rank's exported slab, in
+ * rank order (ipc_handles[rank] must be a slab this process allocated).  X = Y = 0 lets
+ * the topology layer choose the grid (torus_pick_grid).  The handles are copied.
+ * Uses the current CUDA device of the slab.  out: written on success. */
+TORUS_API int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t* ipc_handles,
+                    torus_comm_t* out);
+
+/* Single-GPU emulation of a whole X*Y grid ("virtual ranks"): all N
+ * ranks' workspaces live on `device` and one cooperative launch runs every rank's CTAs,
+ * so the cross-rank flag protocol and the peer-pointer paths of the product kernel are
+ * exercised without N GPUs.  ctas = CTAs per virtual rank (0 = auto, sized so all N*ctas
+ * CTAs are co-resident); ws_bytes per rank (0 = default). */
+TORUS_API int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_comm_t* out);
+
+/* Collective teardown: a device barrier among all ranks (so no peer still reads this
+ * rank's slab), then unmap peers, free the slab.  NULL is a no-op. */
+TORUS_API int torus_comm_destroy(torus_comm_t comm);
+
+/* ---------------------------------------------------------------------------------------
+ * The all-reduce
+ * ------------------------------------------------------------------------------------- */
+
+/* In-place all-reduce of `count` elements of `dtype` at device pointer `buf` (on the
+ * comm's device), enqueued on `stream`; returns once enqueued (asynchronous, CUDA-graph
+ * capturable: no host sync, no allocation).  Every rank must call it in the same order
+ * with the same count, dtype and op.  Result on every rank: the
+ * element-wise sum, or for TORUS_MEAN the sum times f32(1/N) rounded once (i32: the
+ * wrapped sum / N truncated toward zero).  The wire type equals dtype.
+ * count == 0: TORUS_OK, nothing enqueued.  buf must be element-aligned; 16-byte
+ * alignment selects the 128-bit vector path.  The caller keeps buf valid until the
+ * stream work completes.  Errors: INVALID_ARG / UNSUPPORTED before anything is
+ * enqueued; CUDA if a launch fails; TIMEOUT is reported asynchronously. */
+TORUS_API int torus_allreduce(torus_comm_t comm, void* buf, size_t count, torus_dtype_t dtype,
+                    torus_op_t op, torus_stream_t stream);
+
+/* As torus_allreduce with an explicit wire type ("the communication to
+ * synchronize gradients [is] conducted in half precision float (FP16)" while LARS runs
+ * in FP32).  Supported: wire == dtype, or dtype F32 with wire F16 / BF16: the f32 buffer
+ * is cast to the wire type on the first read (round-to-nearest-even) and cast back on the
+ * last write -- no separate pack/unpack kernels. */
+TORUS_API int torus_allreduce_ex(torus_comm_t comm, void* buf, size_t count, torus_dtype_t dtype,
+                       torus_dtype_t wire, torus_op_t op, torus_stream_t stream);
+
+/* Virtual-rank variant (comm from torus_vcomm_init): bufs is a HOST array [N] of device
+ * pointers, one buffer per virtual rank, all on the comm's device. */
+TORUS_API int torus_vallreduce(torus_comm_t comm, void* const* bufs, size_t count, torus_dtype_t dtype,
+                     torus_dtype_t wire, torus_op_t op, torus_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Queries, topology, host logic, errors
+ * ------------------------------------------------------------------------------------- */
+
+/* Async error word written by the device watchdog (TORUS_ERR_TIMEOUT) -- readable without
+ * synchronizing; 0 when healthy.  A comm that reported an async error must be destroyed. */
+TORUS_API int torus_comm_get_async_error(torus_comm_t comm);
+
+TORUS_API int torus_comm_grid(torus_comm_t comm, int* X, int* Y);  /* host out-pointers */
+TORUS_API int torus_comm_rank(torus_comm_t comm, int* rank, int* world);
+TORUS_API int torus_comm_ctas(torus_comm_t comm);                  /* CTAs per rank per launch, or -1 */
+
+/* Elements per round for a wire type: calls longer than this run as consecutive rounds
+ * (one kernel launch each), each partitioned independently.  0 on error. */
+TORUS_API size_t torus_comm_round_elems(torus_comm_t comm, torus_dtype_t wire);
+
+/* Kernel launches one torus_allreduce_ex call with these arguments enqueues (0 for
+ * count == 0 or a no-op N == 1 call).  Returns -1 on invalid arguments. */
+TORUS_API int torus_comm_launches(torus_comm_t comm, size_t count, torus_dtype_t dtype,
+                        torus_dtype_t wire);
+
+/* Topology layer: choose the grid for `world` GPUs.  p2p: host row-major [world*world]
+ * matrix, p2p[i*world+j] = relative link bandwidth (0 = no P2P); NULL = query the CUDA
+ * driver for the visible devices 0..world-1.  Writes X, Y.  On one NVSwitch domain
+ * every factorization moves the same 2(N-1)/N*S bytes per rank, so
+ * the alpha-beta model picks the grid with the fewest sequential sync rounds,
+ * X = world, Y = 1; GPUs that do not share a P2P domain are placed in different rows. */
+TORUS_API int torus_pick_grid(int world, const int* p2p, int* X, int* Y);
+
+/* Host logic export (tests): the nested quantum-aligned partition used by every launch
+ * (SURVEY C3): split n into `parts` ranges with quantum q.  off/len: host arrays
+ * [parts]. */
+TORUS_API int torus_partition(unsigned long long n, int parts, int q, unsigned long long* off,
+                    unsigned long long* len);
+
+/* Static string for a result code. */
+TORUS_API const char* torus_strerror(int code);
+/* Thread-local text of the last error raised in this thread (CUDA message included). */
+TORUS_API const char* torus_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TORUS_H */

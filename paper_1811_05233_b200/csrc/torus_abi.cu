@@ -1,0 +1,540 @@
+// torus_abi.cu -- host side of libtorus.so: the C-ABI declared in include/torus.h.
+//
+// Responsibilities: symmetric workspace slabs exported/opened through CUDA IPC, the
+// communicator (grid, peer table, device epochs, async error word), argument
+// validation, round splitting, the topology layer (grid choice) and kernel
+// launches.  PyTorch never appears here; the Python binding passes plain pointers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/torus.h"
+#include "torus_internal.h"
+
+using namespace torus;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char msg[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(msg, sizeof msg, fmt, ap);
+  va_end(ap);
+  g_last_error = std::string(torus_strerror(code)) + ": " + msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(TORUS_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define CU(call)                                         \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);  \
+  } while (0)
+
+size_t env_size(const char* name, size_t dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  return (size_t)strtoull(v, nullptr, 10);
+}
+
+constexpr size_t kDefaultSlab = 320ull << 20;
+
+struct Slab {
+  int device;
+  void* ptr;
+  size_t size;
+  cudaIpcMemHandle_t handle;
+};
+std::mutex g_mu;
+std::vector<Slab> g_slabs;  // exported, not yet adopted by a comm
+
+size_t wire_size(int t) { return (t == TORUS_F16 || t == TORUS_BF16) ? 2 : 4; }
+bool valid_dtype(int t) { return t >= TORUS_F32 && t <= TORUS_I32; }
+bool valid_pair(int dtype, int wire) {
+  if (!valid_dtype(dtype) || !valid_dtype(wire)) return false;
+  if (dtype == wire) return true;
+  return dtype == TORUS_F32 && (wire == TORUS_F16 || wire == TORUS_BF16);
+}
+
+}  // namespace
+
+struct torus_comm {
+  int rank = 0, world = 1, X = 1, Y = 1;
+  int device = 0;
+  int G = 0;
+  int nlocal = 1;           // > 1: virtual ranks on one device
+  bool virt = false;
+  size_t slab_size = 0;
+  SlabLayout layout{};
+  unsigned long long timeout_ns = 0;
+  std::vector<void*> own_slabs;   // slabs this process allocated (freed at destroy)
+  std::vector<void*> opened;      // IPC-opened peer bases (closed at destroy)
+  std::vector<int> local_ranks;   // ranks hosted by this process
+  RankDev* d_ranks = nullptr;     // device [nlocal]
+  uint32_t* d_epochs = nullptr;   // device [nlocal * G] + [nlocal] barrier counters
+  int* h_err = nullptr;           // host-mapped async error word
+  int* d_err = nullptr;
+  bool poisoned = false;
+};
+
+namespace {
+
+SlabLayout make_layout(size_t slab_size, int G) {
+  SlabLayout L;
+  L.flags_bytes = flags_bytes_for(G);
+  L.bar_off = L.flags_bytes;
+  L.data_off = L.bar_off + 65536;
+  L.size = slab_size;
+  return L;
+}
+
+// Round capacity for a wire type (elements): R = k * q * X * Y with
+// h_in (X>1: X slots of R/X) + v_in (Y slots of R/(XY)) + chunk (R/X) in the data region.
+unsigned long long round_elems(const torus_comm* c, int wire) {
+  const unsigned long long sw = wire_size(wire), q = kVecBytes / sw;
+  if (c->slab_size <= c->layout.data_off) return 0;
+  const unsigned long long data_elems = (c->slab_size - c->layout.data_off) / sw;
+  const unsigned long long per_k = q * (unsigned long long)c->Y * ((c->X > 1 ? c->X : 0) + 2);
+  const unsigned long long k = data_elems / per_k;
+  return k * q * (unsigned long long)c->X * (unsigned long long)c->Y;
+}
+
+int alloc_comm_common(torus_comm* c) {
+  const size_t n_ep = (size_t)c->nlocal * c->G + c->nlocal;
+  CU(cudaMalloc(&c->d_epochs, n_ep * sizeof(uint32_t)));
+  CU(cudaMemset(c->d_epochs, 0, n_ep * sizeof(uint32_t)));
+  CU(cudaHostAlloc(&c->h_err, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
+  *c->h_err = 0;
+  CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_err), c->h_err, 0));
+  CU(cudaMalloc(&c->d_ranks, sizeof(RankDev) * c->nlocal));
+  return TORUS_OK;
+}
+
+int upload_ranks(torus_comm* c, const std::vector<char*>& bases) {
+  std::vector<RankDev> rd(c->nlocal);
+  for (int l = 0; l < c->nlocal; ++l) {
+    RankDev& r = rd[l];
+    memset(&r, 0, sizeof r);
+    r.rank = c->local_ranks[l];
+    r.X = c->X;
+    r.Y = c->Y;
+    r.N = c->X * c->Y;
+    r.rho = r.rank / c->X;
+    r.c = r.rank % c->X;
+    r.G = c->G;
+    for (int p = 0; p < c->world; ++p) r.ws[p] = bases[p];
+    r.epoch = c->d_epochs + (size_t)l * c->G;
+    r.bar_epoch = c->d_epochs + (size_t)c->nlocal * c->G + l;
+    r.err = c->d_err;
+  }
+  CU(cudaMemcpy(c->d_ranks, rd.data(), sizeof(RankDev) * c->nlocal, cudaMemcpyHostToDevice));
+  return TORUS_OK;
+}
+
+int pick_ctas(int device, int nlocal) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  int per_sm = torus_kernel_max_ctas_per_sm(TORUS_F32, TORUS_F16);
+  for (int d = 0; d < 4; ++d) per_sm = std::min(per_sm, torus_kernel_max_ctas_per_sm(d, d));
+  if (per_sm < 1) per_sm = 1;
+  const int resident = sms * per_sm;
+  int want = (int)env_size("TORUS_CTAS", nlocal > 1 ? 16 : 32);
+  want = std::max(1, want);
+  // every CTA of every rank that waits on another must be co-resident
+  return std::min(want, std::max(1, resident / nlocal));
+}
+
+void destroy_resources(torus_comm* c) {
+  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  for (void* p : c->own_slabs) cudaFree(p);
+  if (c->d_ranks) cudaFree(c->d_ranks);
+  if (c->d_epochs) cudaFree(c->d_epochs);
+  if (c->h_err) cudaFreeHost(c->h_err);
+  delete c;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* torus_strerror(int code) {
+  switch (code) {
+    case TORUS_OK: return "TORUS_OK";
+    case TORUS_ERR_INVALID_ARG: return "TORUS_ERR_INVALID_ARG";
+    case TORUS_ERR_GRID: return "TORUS_ERR_GRID";
+    case TORUS_ERR_UNSUPPORTED: return "TORUS_ERR_UNSUPPORTED";
+    case TORUS_ERR_CUDA: return "TORUS_ERR_CUDA";
+    case TORUS_ERR_PEER: return "TORUS_ERR_PEER";
+    case TORUS_ERR_TIMEOUT: return "TORUS_ERR_TIMEOUT";
+    case TORUS_ERR_MISMATCH: return "TORUS_ERR_MISMATCH";
+    default: return "TORUS_ERR_UNKNOWN";
+  }
+}
+
+const char* torus_last_error(void) { return g_last_error.c_str(); }
+
+int torus_partition(unsigned long long n, int parts, int q, unsigned long long* off,
+                    unsigned long long* len) {
+  if (parts < 1 || q < 1 || !off || !len) return fail(TORUS_ERR_INVALID_ARG, "partition args");
+  for (int i = 0; i < parts; ++i) qpart(n, parts, q, i, &off[i], &len[i]);
+  return TORUS_OK;
+}
+
+int torus_workspace_alloc(int device, size_t bytes, torus_ipc_handle_t* out) {
+  if (!out) return fail(TORUS_ERR_INVALID_ARG, "out is NULL");
+  if (bytes == 0) bytes = env_size("TORUS_WS_BYTES", kDefaultSlab);
+  bytes = (bytes + 65535) & ~(size_t)65535;
+  CU(cudaSetDevice(device));
+  void* p = nullptr;
+  CU(cudaMalloc(&p, bytes));
+  cudaError_t e = cudaMemset(p, 0, bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_fail(e, "workspace export");
+  }
+  memset(out, 0, sizeof *out);
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(out->bytes, &h, 64);
+  out->offset = 0;
+  out->size = bytes;
+  std::lock_guard<std::mutex> g(g_mu);
+  g_slabs.push_back(Slab{device, p, bytes, h});
+  return TORUS_OK;
+}
+
+int torus_workspace_release(const torus_ipc_handle_t* h) {
+  if (!h) return fail(TORUS_ERR_INVALID_ARG, "handle is NULL");
+  std::lock_guard<std::mutex> g(g_mu);
+  for (size_t i = 0; i < g_slabs.size(); ++i)
+    if (memcmp(&g_slabs[i].handle, h->bytes, 64) == 0) {
+      cudaSetDevice(g_slabs[i].device);
+      cudaFree(g_slabs[i].ptr);
+      g_slabs.erase(g_slabs.begin() + i);
+      return TORUS_OK;
+    }
+  return fail(TORUS_ERR_INVALID_ARG, "no such local workspace");
+}
+
+int torus_pick_grid(int world, const int* p2p, int* X, int* Y) {
+  if (world < 1 || world > kMaxRanks || !X || !Y) return fail(TORUS_ERR_INVALID_ARG, "pick_grid args");
+  std::vector<int> m((size_t)world * world, 0);
+  if (p2p) {
+    for (size_t i = 0; i < m.size(); ++i) m[i] = p2p[i];
+  } else {
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    if (ndev < world) return fail(TORUS_ERR_GRID, "only %d visible devices for world %d", ndev, world);
+    for (int i = 0; i < world; ++i)
+      for (int j = 0; j < world; ++j) {
+        int ok = (i == j);
+        if (i != j) CU(cudaDeviceCanAccessPeer(&ok, i, j));
+        m[(size_t)i * world + j] = ok ? 1 : 0;
+      }
+  }
+  // P2P domains = connected components of the link graph.
+  std::vector<int> dom(world, -1);
+  int ndom = 0;
+  for (int s = 0; s < world; ++s) {
+    if (dom[s] >= 0) continue;
+    std::vector<int> st{s};
+    dom[s] = ndom;
+    while (!st.empty()) {
+      int u = st.back();
+      st.pop_back();
+      for (int v = 0; v < world; ++v)
+        if (dom[v] < 0 && (m[(size_t)u * world + v] > 0 || m[(size_t)v * world + u] > 0)) {
+          dom[v] = ndom;
+          st.push_back(v);
+        }
+    }
+    ++ndom;
+  }
+  if (ndom == 1) {
+    // One NVSwitch domain: every grid moves 2(N-1)/N*S bytes per rank; the alpha term
+    // counts handshakes (2 per non-degenerate dimension), so the flat grid X = N wins.
+    *X = world;
+    *Y = 1;
+    return TORUS_OK;
+  }
+  // Several domains: rows = domains (they must be equal-sized and rank-contiguous).
+  const int per = world / ndom;
+  if (per * ndom != world) return fail(TORUS_ERR_GRID, "unequal P2P domains");
+  for (int r = 0; r < world; ++r)
+    if (dom[r] != dom[(r / per) * per]) return fail(TORUS_ERR_GRID, "P2P domains not rank-contiguous");
+  *X = per;
+  *Y = ndom;
+  return TORUS_OK;
+}
+
+int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t* ipc_handles,
+                    torus_comm_t* out) {
+  if (!ipc_handles || !out) return fail(TORUS_ERR_INVALID_ARG, "null argument");
+  if (world < 1 || world > kMaxRanks) return fail(TORUS_ERR_GRID, "world %d outside [1,%d]", world, kMaxRanks);
+  if (rank < 0 || rank >= world) return fail(TORUS_ERR_GRID, "rank %d outside [0,%d)", rank, world);
+  if (X == 0 && Y == 0) {
+    int rc = torus_pick_grid(world, nullptr, &X, &Y);
+    if (rc) return rc;
+  }
+  if (X < 1 || Y < 1 || X * Y != world || X > kMaxDim || Y > kMaxDim)
+    return fail(TORUS_ERR_GRID, "grid %dx%d does not match world %d", X, Y, world);
+  for (int r = 1; r < world; ++r)
+    if (ipc_handles[r].size != ipc_handles[0].size)
+      return fail(TORUS_ERR_MISMATCH, "slab sizes differ across ranks");
+
+  Slab own{};
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    size_t i = 0;
+    for (; i < g_slabs.size(); ++i)
+      if (memcmp(&g_slabs[i].handle, ipc_handles[rank].bytes, 64) == 0) break;
+    if (i == g_slabs.size()) return fail(TORUS_ERR_INVALID_ARG, "ipc_handles[rank] is not a local slab");
+    own = g_slabs[i];
+    g_slabs.erase(g_slabs.begin() + i);
+  }
+  torus_comm* c = new torus_comm();
+  c->rank = rank;
+  c->world = world;
+  c->X = X;
+  c->Y = Y;
+  c->device = own.device;
+  c->nlocal = 1;
+  c->local_ranks = {rank};
+  c->slab_size = own.size;
+  c->own_slabs.push_back(own.ptr);
+  c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
+  int rc = TORUS_OK;
+  std::vector<char*> bases(world, nullptr);
+  if (cudaSetDevice(c->device) != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "cudaSetDevice");
+  if (!rc) {
+    c->G = pick_ctas(c->device, 1);
+    c->layout = make_layout(c->slab_size, c->G);
+    if (round_elems(c, TORUS_F32) == 0) rc = fail(TORUS_ERR_INVALID_ARG, "workspace too small");
+  }
+  for (int p = 0; !rc && p < world; ++p) {
+    if (p == rank) {
+      bases[p] = static_cast<char*>(own.ptr);
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handles[p].bytes, 64);
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      rc = fail(TORUS_ERR_PEER, "cudaIpcOpenMemHandle(rank %d): %s", p, cudaGetErrorString(e));
+      break;
+    }
+    c->opened.push_back(ptr);
+    bases[p] = static_cast<char*>(ptr);
+  }
+  if (!rc) rc = alloc_comm_common(c);
+  if (!rc) rc = upload_ranks(c, bases);
+  if (rc) {
+    destroy_resources(c);
+    return rc;
+  }
+  *out = c;
+  return TORUS_OK;
+}
+
+int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_comm_t* out) {
+  if (!out) return fail(TORUS_ERR_INVALID_ARG, "out is NULL");
+  if (X < 1 || Y < 1 || X > kMaxDim || Y > kMaxDim || X * Y > kMaxLocal)
+    return fail(TORUS_ERR_GRID, "virtual grid %dx%d (at most %d ranks)", X, Y, kMaxLocal);
+  CU(cudaSetDevice(device));
+  int coop = 0;
+  CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+  if (!coop) return fail(TORUS_ERR_UNSUPPORTED, "device lacks cooperative launch");
+  torus_comm* c = new torus_comm();
+  c->virt = true;
+  c->X = X;
+  c->Y = Y;
+  c->world = X * Y;
+  c->nlocal = X * Y;
+  c->device = device;
+  for (int r = 0; r < c->world; ++r) c->local_ranks.push_back(r);
+  if (ws_bytes == 0) ws_bytes = env_size("TORUS_WS_BYTES", kDefaultSlab);
+  c->slab_size = (ws_bytes + 65535) & ~(size_t)65535;
+  c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
+  if (ctas > 0) setenv("TORUS_CTAS", std::to_string(ctas).c_str(), 1);
+  c->G = pick_ctas(device, c->nlocal);
+  c->layout = make_layout(c->slab_size, c->G);
+  int rc = TORUS_OK;
+  if (round_elems(c, TORUS_F32) == 0) rc = fail(TORUS_ERR_INVALID_ARG, "workspace too small");
+  std::vector<char*> bases(c->world, nullptr);
+  for (int r = 0; !rc && r < c->world; ++r) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, c->slab_size);
+    if (e == cudaSuccess) e = cudaMemset(p, 0, c->slab_size);
+    if (e != cudaSuccess) {
+      rc = cuda_fail(e, "virtual slab");
+      break;
+    }
+    c->own_slabs.push_back(p);
+    bases[r] = static_cast<char*>(p);
+  }
+  if (!rc) rc = alloc_comm_common(c);
+  if (!rc) rc = upload_ranks(c, bases);
+  if (!rc && cudaDeviceSynchronize() != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "init sync");
+  if (rc) {
+    destroy_resources(c);
+    return rc;
+  }
+  *out = c;
+  return TORUS_OK;
+}
+
+int torus_comm_destroy(torus_comm_t c) {
+  if (!c) return TORUS_OK;
+  int rc = TORUS_OK;
+  cudaSetDevice(c->device);
+  if (!c->poisoned && *c->h_err == 0 && c->world > 1) {
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess) {
+      cudaError_t e = launch_barrier(c->d_ranks, c->nlocal, c->layout.bar_off, c->timeout_ns, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "destroy barrier");
+      cudaStreamDestroy(s);
+    }
+    if (*c->h_err) rc = fail(TORUS_ERR_TIMEOUT, "destroy barrier timed out");
+  } else {
+    cudaDeviceSynchronize();
+  }
+  destroy_resources(c);
+  return rc;
+}
+
+int torus_comm_get_async_error(torus_comm_t c) {
+  if (!c) return TORUS_ERR_INVALID_ARG;
+  return *reinterpret_cast<volatile int*>(c->h_err);
+}
+
+int torus_comm_grid(torus_comm_t c, int* X, int* Y) {
+  if (!c || !X || !Y) return fail(TORUS_ERR_INVALID_ARG, "null argument");
+  *X = c->X;
+  *Y = c->Y;
+  return TORUS_OK;
+}
+
+int torus_comm_rank(torus_comm_t c, int* rank, int* world) {
+  if (!c || !rank || !world) return fail(TORUS_ERR_INVALID_ARG, "null argument");
+  *rank = c->rank;
+  *world = c->world;
+  return TORUS_OK;
+}
+
+int torus_comm_ctas(torus_comm_t c) { return c ? c->G : -1; }
+
+size_t torus_comm_round_elems(torus_comm_t c, torus_dtype_t wire) {
+  if (!c || !valid_dtype(wire)) return 0;
+  return (size_t)round_elems(c, wire);
+}
+
+int torus_comm_launches(torus_comm_t c, size_t count, torus_dtype_t dtype, torus_dtype_t wire) {
+  if (!c || !valid_pair(dtype, wire)) return -1;
+  if (count == 0) return 0;
+  if (c->world == 1) return dtype == wire ? 0 : 1;
+  const unsigned long long R = round_elems(c, wire);
+  if (R == 0) return -1;
+  return (int)((count + R - 1) / R);
+}
+
+}  // extern "C"
+
+namespace {
+
+int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, int wire, int op,
+                   cudaStream_t stream) {
+  if (!c) return fail(TORUS_ERR_INVALID_ARG, "comm is NULL");
+  if (!valid_pair(dtype, wire))
+    return valid_dtype(dtype) && valid_dtype(wire)
+               ? fail(TORUS_ERR_UNSUPPORTED, "dtype %d with wire %d", dtype, wire)
+               : fail(TORUS_ERR_INVALID_ARG, "bad dtype/wire code");
+  if (op != TORUS_SUM && op != TORUS_MEAN) return fail(TORUS_ERR_INVALID_ARG, "bad op %d", op);
+  if (c->poisoned || *reinterpret_cast<volatile int*>(c->h_err)) {
+    c->poisoned = true;
+    return fail(TORUS_ERR_TIMEOUT, "communicator has an async error; destroy it");
+  }
+  const size_t esz = wire_size(dtype);
+  bool aligned = true;
+  for (int l = 0; l < c->nlocal; ++l) {
+    if (!bufs[l]) return fail(TORUS_ERR_INVALID_ARG, "buffer %d is NULL", l);
+    const uintptr_t p = reinterpret_cast<uintptr_t>(bufs[l]);
+    if (p % esz) return fail(TORUS_ERR_INVALID_ARG, "buffer %d not element-aligned", l);
+    if (p % kVecBytes) aligned = false;
+  }
+  if (count == 0) return TORUS_OK;
+  if (count > (size_t)1 << 48) return fail(TORUS_ERR_INVALID_ARG, "count overflow");
+  if (c->world == 1) {
+    if (dtype == wire) return TORUS_OK;  // sum/mean over one rank of wire values: identity
+    cudaError_t e = launch_castscale(bufs[0], count, dtype, wire, stream);
+    return e == cudaSuccess ? TORUS_OK : cuda_fail(e, "castscale launch");
+  }
+  const unsigned long long R = round_elems(c, wire);
+  const unsigned long long sw = wire_size(wire);
+  LaunchArgs a;
+  memset(&a, 0, sizeof a);
+  a.ranks = c->d_ranks;
+  for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];
+  a.nlocal = c->nlocal;
+  a.G = c->G;
+  a.q = (int)(kVecBytes / sw);
+  a.op = op;
+  a.inv_n = 1.0f / (float)(c->X * c->Y);
+  a.aligned = aligned ? 1 : 0;
+  a.timeout_ns = c->timeout_ns;
+  const unsigned long long Lc = R / c->X, Lcs = R / ((unsigned long long)c->X * c->Y);
+  a.hin_off = c->layout.data_off;
+  a.hin_stride = Lc * sw;
+  a.vin_off = a.hin_off + (c->X > 1 ? (unsigned long long)c->X * a.hin_stride : 0);
+  a.vin_stride = Lcs * sw;
+  a.chunk_off = a.vin_off + (unsigned long long)c->Y * a.vin_stride;
+  if (a.chunk_off + Lc * sw > c->slab_size) return fail(TORUS_ERR_INVALID_ARG, "layout overflow");
+  for (unsigned long long r0 = 0; r0 < count; r0 += R) {
+    a.n = std::min<unsigned long long>(R, count - r0);
+    a.buf_off = r0;
+    cudaError_t e = launch_torus(a, dtype, wire, c->virt, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "torus kernel launch");
+  }
+  return TORUS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int torus_allreduce_ex(torus_comm_t c, void* buf, size_t count, torus_dtype_t dtype,
+                       torus_dtype_t wire, torus_op_t op, torus_stream_t stream) {
+  if (c && c->virt) return fail(TORUS_ERR_INVALID_ARG, "virtual comm: use torus_vallreduce");
+  void* bufs[1] = {buf};
+  return allreduce_impl(c, bufs, count, dtype, wire, op, static_cast<cudaStream_t>(stream));
+}
+
+int torus_allreduce(torus_comm_t c, void* buf, size_t count, torus_dtype_t dtype, torus_op_t op,
+                    torus_stream_t stream) {
+  return torus_allreduce_ex(c, buf, count, dtype, dtype, op, stream);
+}
+
+int torus_vallreduce(torus_comm_t c, void* const* bufs, size_t count, torus_dtype_t dtype,
+                     torus_dtype_t wire, torus_op_t op, torus_stream_t stream) {
+  if (!c || !bufs) return fail(TORUS_ERR_INVALID_ARG, "null argument");
+  if (!c->virt) return fail(TORUS_ERR_INVALID_ARG, "not a virtual comm");
+  return allreduce_impl(c, bufs, count, dtype, wire, op, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,102 @@
+// torus_internal.h -- layout and launch structures shared by the product's host code
+// (torus_abi.cu) and kernels (torus_kernels.cu).  Not part of the public ABI.
+//
+// Notation follows PAPER.md:70: N = X * Y ranks, X per row (horizontal), Y per column
+// (vertical); rank = rho * X + c (row rho, column c).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace torus {
+
+constexpr int kMaxRanks = 64;     // N <= 64 (a single NVLink domain has at most 72 GPUs)
+constexpr int kMaxDim = 64;       // X, Y <= 64
+constexpr int kMaxLocal = 16;     // virtual ranks per launch (single-GPU emulation)
+constexpr int kThreads = 512;     // threads per CTA of the torus kernel
+constexpr int kVecBytes = 16;     // 128-bit vectors (LDG/STG.E.128)
+constexpr int kFlagPhases = 4;    // H-RS, V-RS, V-AG, H-AG handshakes
+
+// Flag kinds (PAPER.md:70 phases; one u32 epoch per (kind, source, CTA)).
+enum FlagKind : int {
+  kFlagH = 0,   // row peer pushed its share of my chunk into my h_in        (phase 1)
+  kFlagV = 1,   // column peer pushed its phase-1 result into my v_in        (phase 2 RS)
+  kFlagAG = 2,  // column peer pushed its reduced sub-chunk into my chunk     (phase 2 AG)
+  kFlagR = 3,   // row peer's chunk is complete: I may pull it                (phase 3)
+};
+
+// Workspace slab layout (identical on every rank; byte offsets from the slab base):
+//   [0, flags_bytes)          flags[kind][src < kMaxDim][cta < G]  (u32 epochs)
+//   [bar_off, +kMaxRanks*4)   barrier flags for init/destroy
+//   [data_off, size)          data region, carved per call by wire type:
+//        h_in[X][Lc]   (X > 1 only) shares of MY chunk pushed by each row peer
+//        v_in[Y][Lcs]  phase-1 results of MY sub-chunk pushed by each column peer
+//        chunk[Lc]     MY chunk, complete after phase 2 (pulled by row peers in phase 3)
+struct SlabLayout {
+  size_t flags_bytes;
+  size_t bar_off;
+  size_t data_off;
+  size_t size;
+};
+
+// Per-(rank) static description, uploaded once at init (device memory).
+struct RankDev {
+  int rank, rho, c;
+  int X, Y, N;
+  int G;                         // CTAs per rank per launch
+  char* ws[kMaxRanks];           // every rank's slab base as mapped in THIS process
+  uint32_t* epoch;               // [G] local per-CTA call counters (device memory)
+  uint32_t* bar_epoch;           // [1] barrier counter
+  int* err;                      // host-mapped async error word
+};
+
+// Per-launch (per-round) arguments, passed by value.
+struct LaunchArgs {
+  const RankDev* ranks;          // device array [nlocal]
+  void* buf[kMaxLocal];          // user buffer of each local rank
+  unsigned long long n;          // elements in this round
+  unsigned long long buf_off;    // element offset of the round inside the user buffers
+  unsigned long long hin_off, hin_stride;   // bytes (from slab base / between slots)
+  unsigned long long vin_off, vin_stride;
+  unsigned long long chunk_off;
+  unsigned long long timeout_ns;
+  int nlocal;
+  int G;
+  int q;                         // partition quantum in elements (16 B / sizeof(wire))
+  int op;                        // 0 sum, 1 mean
+  float inv_n;                   // f32(1/N)
+  int aligned;                   // all user buffers 16-byte aligned -> vector path
+};
+
+// Nested quantum-aligned partition (SPEC.md:67-75 when q == 1).  Host and
+// device use this one definition; the oracle has its own, independent one.
+__host__ __device__ inline void qpart(unsigned long long n, int parts, int q, int i,
+                                      unsigned long long* off, unsigned long long* len) {
+  const unsigned long long Q = (n + q - 1) / q;
+  const unsigned long long base = Q / parts, rem = Q % parts;
+  const unsigned long long ui = (unsigned long long)i;
+  const unsigned long long start = ui * base + (ui < rem ? ui : rem);
+  const unsigned long long cnt = base + (ui < rem ? 1 : 0);
+  unsigned long long a = start * q, b = (start + cnt) * q;
+  if (a > n) a = n;
+  if (b > n) b = n;
+  *off = a;
+  *len = b - a;
+}
+
+inline size_t flags_bytes_for(int G) {
+  size_t b = (size_t)kFlagPhases * kMaxDim * (size_t)G * sizeof(uint32_t);
+  return (b + 65535) & ~(size_t)65535;
+}
+
+// ---- launch wrappers implemented in torus_kernels.cu ----
+cudaError_t launch_torus(const LaunchArgs& a, int dtype, int wire, bool cooperative,
+                         cudaStream_t stream);
+cudaError_t launch_castscale(void* buf, unsigned long long n, int dtype, int wire,
+                             cudaStream_t stream);
+cudaError_t launch_barrier(const RankDev* ranks, int nlocal, unsigned long long bar_off,
+                           unsigned long long timeout_ns, cudaStream_t stream);
+int torus_kernel_max_ctas_per_sm(int dtype, int wire);
+
+}  // namespace torus

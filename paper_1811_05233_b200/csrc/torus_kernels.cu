@@ -1,0 +1,587 @@
+// torus_kernels.cu -- sm_100a kernels of the 2D-Torus all-reduce (Sec. 2.2).
+//
+// One fused kernel per round runs the paper's three steps for one rank (or, in the
+// single-GPU emulation, for every virtual rank of the grid in one cooperative launch):
+//
+//   phase 1  horizontal reduce-scatter  ("Firstly, reduce-scatter is performed
+//            horizontally").  PUSH: each rank casts its buffer to the wire
+//            type on the first read (FP16 communication) and stores the
+//            share of every row peer's chunk straight into that peer's h_in slot over
+//            NVLink.  The chunk owner folds the X shares in the ring's order (SURVEY C5:
+//            w[c+1] + ... + w[c], f32 accumulation) and stores the rounded result into
+//            the v_in slot of the rank that owns each sub-chunk in its column (this is
+//            the send half of phase 2, fused).
+//   phase 2  vertical all-reduce on the 1/X shard ("Then, all-reduce is performed
+//            vertically").  Reduce-scatter: the sub-chunk owner folds the Y rows' values
+//            (rows rho+1 ... rho), applies the 1/N mean scale, rounds once,
+//            and PUSHES the result into its own and every column peer's chunk slot
+//            (the all-gather half, fused).
+//   phase 3  horizontal all-gather ("Finally, all-gather is performed horizontally").
+//            PULL: each rank reads every row peer's completed chunk over NVLink and
+//            writes its user buffer with the wire->dtype cast fused.
+//
+// Every element crosses NVLink exactly once per hop the algorithm needs; the
+// per-rank NVLink volume is (X-1)/X*S + 2(Y-1)/Y*S/X + (X-1)/X*S = 2(N-1)/N*S.
+// All data movement is 128-bit (LDG/STG.E.128), coalesced, CTA-sliced so that CTA b of
+// every rank owns the same slice of every sub-chunk; cross-GPU ordering uses one
+// st.release.sys / ld.acquire.sys epoch flag per (phase, source rank, CTA).
+// No tensor cores: the path is a bandwidth-bound reduction (BASELINE.json north_star).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "torus_internal.h"
+
+namespace torus {
+namespace {
+
+enum { DT_F32 = 0, DT_F16 = 1, DT_BF16 = 2, DT_I32 = 3 };
+enum { kErrTimeout = 6 };
+
+// ------------------------------------------------------------------------------------
+// memory-model primitives
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Workspace traffic goes through L2 only (.cg): slots are written by peers over NVLink
+// during the kernel, so L1 must never hold a stale line.
+__device__ __forceinline__ uint4 ld_ws(const void* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
+__device__ __forceinline__ void st_ws(void* p, uint4 v) { __stcg(reinterpret_cast<uint4*>(p), v); }
+
+// ------------------------------------------------------------------------------------
+// wire traits: a 16-byte vector holds VE wire elements; Acc is the accumulation type
+// (f32 for float wires, u32 two's-complement for i32)
+// ------------------------------------------------------------------------------------
+template <int W> struct Wire;
+template <> struct Wire<DT_F32> { static constexpr int VE = 4; using Acc = float; };
+template <> struct Wire<DT_I32> { static constexpr int VE = 4; using Acc = uint32_t; };
+template <> struct Wire<DT_F16> { static constexpr int VE = 8; using Acc = float; };
+template <> struct Wire<DT_BF16> { static constexpr int VE = 8; using Acc = float; };
+
+template <int W>
+__device__ __forceinline__ void unpack(const uint4 v, typename Wire<W>::Acc* a) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  if constexpr (W == DT_F32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = __uint_as_float(w[i]);
+  } else if constexpr (W == DT_I32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = w[i];
+  } else if constexpr (W == DT_F16) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+      float2 f = __half22float2(h);  // exact
+      a[2 * i] = f.x;
+      a[2 * i + 1] = f.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // bf16 -> f32 is a shift (exact)
+      a[2 * i] = __uint_as_float(w[i] << 16);
+      a[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+}
+
+// round to the wire type: IEEE round-to-nearest-even, no FTZ
+template <int W>
+__device__ __forceinline__ uint4 pack(const typename Wire<W>::Acc* a) {
+  uint32_t w[4];
+  if constexpr (W == DT_F32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = __float_as_uint(a[i]);
+  } else if constexpr (W == DT_I32) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) w[i] = a[i];
+  } else if constexpr (W == DT_F16) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half2 h = __floats2half2_rn(a[2 * i], a[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int W>
+__device__ __forceinline__ void acc_add(typename Wire<W>::Acc* a, const typename Wire<W>::Acc* b) {
+#pragma unroll
+  for (int i = 0; i < Wire<W>::VE; ++i) {
+    if constexpr (W == DT_I32) a[i] = a[i] + b[i];  // wraps
+    else a[i] = __fadd_rn(a[i], b[i]);               // no contraction, no FTZ
+  }
+}
+
+// mean = f32 sum * f32(1/N), or (i32) wrapped sum / N truncated
+template <int W>
+__device__ __forceinline__ void acc_mean(typename Wire<W>::Acc* a, float inv_n, int N) {
+#pragma unroll
+  for (int i = 0; i < Wire<W>::VE; ++i) {
+    if constexpr (W == DT_I32) a[i] = (uint32_t)((int32_t)a[i] / N);
+    else a[i] = __fmul_rn(a[i], inv_n);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// user-buffer access with the dtype <-> wire cast fused
+// ------------------------------------------------------------------------------------
+template <int DT> struct Elem;
+template <> struct Elem<DT_F32> { using T = float; };
+template <> struct Elem<DT_I32> { using T = int32_t; };
+template <> struct Elem<DT_F16> { using T = __half; };
+template <> struct Elem<DT_BF16> { using T = __nv_bfloat16; };
+
+// Load `nrem` (<= VE) elements at element index e of the user buffer, converted to the
+// wire type (C1: w = to_wire(in)); missing lanes are zero.
+template <int DT, int W>
+__device__ __forceinline__ uint4 load_user(const void* buf, unsigned long long e, int nrem,
+                                           bool aligned) {
+  constexpr int VE = Wire<W>::VE;
+  using T = typename Elem<DT>::T;
+  const T* p = reinterpret_cast<const T*>(buf) + e;
+  if constexpr (DT == W) {
+    if (aligned && nrem == VE) return __ldcs(reinterpret_cast<const uint4*>(p));
+    uint16_t h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t u[4] = {0, 0, 0, 0};
+    if constexpr (sizeof(T) == 2) {
+      for (int i = 0; i < nrem; ++i) h[i] = reinterpret_cast<const uint16_t*>(p)[i];
+      return make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16),
+                        h[4] | (uint32_t(h[5]) << 16), h[6] | (uint32_t(h[7]) << 16));
+    } else {
+      for (int i = 0; i < nrem; ++i) u[i] = reinterpret_cast<const uint32_t*>(p)[i];
+      return make_uint4(u[0], u[1], u[2], u[3]);
+    }
+  } else {
+    static_assert(DT == DT_F32 && VE == 8, "only f32 buffers take a narrower wire");
+    float f[8];
+    if (aligned && nrem == 8) {
+      const float4 a0 = __ldcs(reinterpret_cast<const float4*>(p));
+      const float4 a1 = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+      f[0] = a0.x; f[1] = a0.y; f[2] = a0.z; f[3] = a0.w;
+      f[4] = a1.x; f[5] = a1.y; f[6] = a1.z; f[7] = a1.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) f[i] = (i < nrem) ? p[i] : 0.0f;
+    }
+    return pack<W>(f);
+  }
+}
+
+// Store `nrem` elements from a wire vector into the user buffer (from_wire, exact).
+template <int DT, int W>
+__device__ __forceinline__ void store_user(void* buf, unsigned long long e, int nrem, uint4 v,
+                                           bool aligned) {
+  constexpr int VE = Wire<W>::VE;
+  using T = typename Elem<DT>::T;
+  T* p = reinterpret_cast<T*>(buf) + e;
+  if constexpr (DT == W) {
+    if (aligned && nrem == VE) { __stcs(reinterpret_cast<uint4*>(p), v); return; }
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    if constexpr (sizeof(T) == 2) {
+      for (int i = 0; i < nrem; ++i)
+        reinterpret_cast<uint16_t*>(p)[i] = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
+    } else {
+      for (int i = 0; i < nrem; ++i) reinterpret_cast<uint32_t*>(p)[i] = w[i];
+    }
+  } else {
+    float f[8];
+    unpack<W>(v, f);
+    if (aligned && nrem == 8) {
+      __stcs(reinterpret_cast<float4*>(p), make_float4(f[0], f[1], f[2], f[3]));
+      __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(f[4], f[5], f[6], f[7]));
+    } else {
+      for (int i = 0; i < nrem; ++i) p[i] = f[i];
+    }
+  }
+}
+
+// CTA b's slice of a range of `len` elements, in whole vectors of VE elements.
+__device__ __forceinline__ void cta_slice(unsigned long long len, int b, int G, int VE,
+                                          unsigned long long* va, unsigned long long* vz) {
+  const unsigned long long nv = (len + VE - 1) / VE;
+  *va = nv * (unsigned long long)b / (unsigned long long)G;
+  *vz = nv * (unsigned long long)(b + 1) / (unsigned long long)G;
+}
+
+constexpr int kUnrollCopy = 4;   // 16-byte vectors in flight per thread (copy loops)
+constexpr int kUnrollFold = 2;   // vectors per thread per fold step (x X or Y operands)
+
+// ------------------------------------------------------------------------------------
+// the fused torus kernel
+// ------------------------------------------------------------------------------------
+template <int DT, int W>
+__global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) {
+  using Acc = typename Wire<W>::Acc;
+  constexpr int VE = Wire<W>::VE;
+  constexpr int SW = kVecBytes / VE;  // bytes per wire element
+
+  const int lr = blockIdx.x / a.G;
+  const int b = blockIdx.x - lr * a.G;
+  const RankDev* __restrict__ R = a.ranks + lr;
+  const int X = R->X, Y = R->Y, N = R->N, rho = R->rho, c = R->c, me = R->rank;
+  const int G = a.G, q = a.q;
+  const int tid = threadIdx.x;
+  const unsigned long long n = a.n;
+  const bool aligned = a.aligned != 0;
+  void* const buf = a.buf[lr];
+  char* const myws = R->ws[me];
+
+  __shared__ uint32_t s_e;
+  __shared__ int s_abort;
+  if (tid == 0) {
+    s_e = R->epoch[b] + 1u;
+    s_abort = 0;
+  }
+  __syncthreads();
+  const uint32_t e = s_e;
+  const unsigned long long deadline = gtimer() + a.timeout_ns;
+
+  auto flag = [&](char* ws, int kind, int src) -> uint32_t* {
+    return reinterpret_cast<uint32_t*>(ws) + ((size_t)(kind * kMaxDim + src) * G + b);
+  };
+  // Wait until `cnt` sources' flags of `kind` reach epoch e; src(t) names the t-th.
+  auto wait_flags = [&](int kind, int cnt, auto src_of) -> bool {
+    if (tid < cnt) {
+      const uint32_t* f = flag(myws, kind, src_of(tid));
+      unsigned it = 0;
+      while ((int32_t)(ld_acquire_sys(f) - e) < 0) {
+        if ((++it & 255u) == 0 && gtimer() > deadline) {
+          atomicExch_system(R->err, kErrTimeout);
+          s_abort = 1;
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    return s_abort == 0;
+  };
+  // Publish epoch e in `cnt` destination ranks' flags of `kind` under my source index.
+  auto signal = [&](int kind, int cnt, int my_src, auto dst_of) {
+    __syncthreads();  // every thread's data stores precede the release (cumulativity)
+    if (tid < cnt) st_release_sys(flag(R->ws[dst_of(tid)], kind, my_src), e);
+  };
+
+  // ---------------- phase 1a: horizontal reduce-scatter, push shares ----------------
+  if (X > 1) {
+    for (int jj = 1; jj < X; ++jj) {
+      const int j = (c + jj) % X;  // staggered so the X ranks of a row hit distinct peers
+      char* const dst = R->ws[rho * X + j] + a.hin_off + (size_t)c * a.hin_stride;
+      unsigned long long co, cl;
+      qpart(n, X, q, j, &co, &cl);
+      for (int s = 0; s < Y; ++s) {
+        unsigned long long so, sl, va, vz;
+        qpart(cl, Y, q, s, &so, &sl);
+        cta_slice(sl, b, G, VE, &va, &vz);
+        for (unsigned long long v0 = va + tid; v0 < vz; v0 += kUnrollCopy * kThreads) {
+          uint4 r[kUnrollCopy];
+#pragma unroll
+          for (int u = 0; u < kUnrollCopy; ++u) {
+            const unsigned long long v = v0 + (unsigned long long)u * kThreads;
+            if (v < vz) {
+              const unsigned long long el = so + v * VE;
+              const int nrem = (int)min((unsigned long long)VE, cl - el);
+              r[u] = load_user<DT, W>(buf, a.buf_off + co + el, nrem, aligned);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kUnrollCopy; ++u) {
+            const unsigned long long v = v0 + (unsigned long long)u * kThreads;
+            if (v < vz) st_ws(dst + (so + v * VE) * SW, r[u]);
+          }
+        }
+      }
+    }
+    signal(kFlagH, X - 1, c, [&](int t) { return rho * X + (c + 1 + t) % X; });
+    if (!wait_flags(kFlagH, X - 1, [&](int t) { return (c + 1 + t) % X; })) return;
+  }
+
+  // ---------------- phase 1b: fold my chunk, push to the column owners ----------------
+  {
+    unsigned long long co, cl;
+    qpart(n, X, q, c, &co, &cl);
+    for (int s = 0; s < Y; ++s) {
+      unsigned long long so, sl, va, vz;
+      qpart(cl, Y, q, s, &so, &sl);
+      cta_slice(sl, b, G, VE, &va, &vz);
+      // Y > 1: into v_in[rho] of rank (s, c), indexed within the sub-chunk;
+      // Y == 1: this is the last reduce phase -> my own chunk slot, indexed within chunk.
+      char* const dst = (Y > 1) ? R->ws[s * X + c] + a.vin_off + (size_t)rho * a.vin_stride
+                                : myws + a.chunk_off + so * SW;
+      for (unsigned long long v0 = va + tid; v0 < vz; v0 += kUnrollFold * kThreads) {
+        Acc acc[kUnrollFold][VE];
+#pragma unroll
+        for (int u = 0; u < kUnrollFold; ++u)
+#pragma unroll
+          for (int i = 0; i < VE; ++i) acc[u][i] = 0;
+        for (int k = 1; k <= X; ++k) {  // ring order: columns c+1, c+2, ..., c
+          const int j = (c + k) % X;
+          uint4 w[kUnrollFold];
+#pragma unroll
+          for (int u = 0; u < kUnrollFold; ++u) {
+            const unsigned long long v = v0 + (unsigned long long)u * kThreads;
+            if (v < vz) {
+              const unsigned long long el = so + v * VE;
+              if (j == c) {
+                const int nrem = (int)min((unsigned long long)VE, cl - el);
+                w[u] = load_user<DT, W>(buf, a.buf_off + co + el, nrem, aligned);
+              } else {
+                w[u] = ld_ws(myws + a.hin_off + (size_t)j * a.hin_stride + el * SW);
+              }
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kUnrollFold; ++u) {
+            Acc t[VE];
+            unpack<W>(w[u], t);
+            if (k == 1) {
+#pragma unroll
+              for (int i = 0; i < VE; ++i) acc[u][i] = t[i];
+            } else {
+              acc_add<W>(acc[u], t);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnrollFold; ++u) {
+          const unsigned long long v = v0 + (unsigned long long)u * kThreads;
+          if (v < vz) {
+            if (Y == 1 && a.op == 1) acc_mean<W>(acc[u], a.inv_n, N);
+            st_ws(dst + v * VE * SW, pack<W>(acc[u]));
+          }
+        }
+      }
+    }
+  }
+
+  // ---------------- phase 2: vertical all-reduce of my sub-chunk ----------------------
+  if (Y > 1) {
+    signal(kFlagV, Y - 1, rho, [&](int t) { return ((rho + 1 + t) % Y) * X + c; });
+    if (!wait_flags(kFlagV, Y - 1, [&](int t) { return (rho + 1 + t) % Y; })) return;
+    unsigned long long co, cl, so, sl, va, vz;
+    qpart(n, X, q, c, &co, &cl);
+    qpart(cl, Y, q, rho, &so, &sl);
+    cta_slice(sl, b, G, VE, &va, &vz);
+    for (unsigned long long v0 = va + tid; v0 < vz; v0 += kUnrollFold * kThreads) {
+      Acc acc[kUnrollFold][VE];
+#pragma unroll
+      for (int u = 0; u < kUnrollFold; ++u)
+#pragma unroll
+        for (int i = 0; i < VE; ++i) acc[u][i] = 0;
+      for (int k = 1; k <= Y; ++k) {  // rows rho+1, ..., rho
+        const int i = (rho + k) % Y;
+        uint4 w[kUnrollFold];
+#pragma unroll
+        for (int u = 0; u < kUnrollFold; ++u) {
+          const unsigned long long v = v0 + (unsigned long long)u * kThreads;
+          if (v < vz) w[u] = ld_ws(myws + a.vin_off + (size_t)i * a.vin_stride + v * VE * SW);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnrollFold; ++u) {
+          Acc t[VE];
+          unpack<W>(w[u], t);
+          if (k == 1) {
+#pragma unroll
+            for (int ii = 0; ii < VE; ++ii) acc[u][ii] = t[ii];
+          } else {
+            acc_add<W>(acc[u], t);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnrollFold; ++u) {
+        const unsigned long long v = v0 + (unsigned long long)u * kThreads;
+        if (v < vz) {
+          if (a.op == 1) acc_mean<W>(acc[u], a.inv_n, N);
+          const uint4 out = pack<W>(acc[u]);
+          const size_t off = a.chunk_off + (so + v * VE) * SW;
+          st_ws(myws + off, out);
+          for (int ii = 1; ii < Y; ++ii)  // vertical all-gather, pushed (fused)
+            st_ws(R->ws[((rho + ii) % Y) * X + c] + off, out);
+        }
+      }
+    }
+    signal(kFlagAG, Y - 1, rho, [&](int t) { return ((rho + 1 + t) % Y) * X + c; });
+    if (!wait_flags(kFlagAG, Y - 1, [&](int t) { return (rho + 1 + t) % Y; })) return;
+  }
+
+  // ---------------- phase 3: horizontal all-gather, pull + cast back -----------------
+  if (X > 1) {
+    signal(kFlagR, X - 1, c, [&](int t) { return rho * X + (c + 1 + t) % X; });
+    if (!wait_flags(kFlagR, X - 1, [&](int t) { return (c + 1 + t) % X; })) return;
+  } else {
+    __syncthreads();
+  }
+  for (int jj = 0; jj < X; ++jj) {
+    const int j = (c + jj) % X;  // own chunk first (local), then the row peers'
+    const char* const src = R->ws[rho * X + j] + a.chunk_off;
+    unsigned long long co, cl;
+    qpart(n, X, q, j, &co, &cl);
+    for (int s = 0; s < Y; ++s) {
+      unsigned long long so, sl, va, vz;
+      qpart(cl, Y, q, s, &so, &sl);
+      cta_slice(sl, b, G, VE, &va, &vz);
+      for (unsigned long long v0 = va + tid; v0 < vz; v0 += kUnrollCopy * kThreads) {
+        uint4 r[kUnrollCopy];
+#pragma unroll
+        for (int u = 0; u < kUnrollCopy; ++u) {
+          const unsigned long long v = v0 + (unsigned long long)u * kThreads;
+          if (v < vz) r[u] = ld_ws(src + (so + v * VE) * SW);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnrollCopy; ++u) {
+          const unsigned long long v = v0 + (unsigned long long)u * kThreads;
+          if (v < vz) {
+            const unsigned long long el = so + v * VE;
+            const int nrem = (int)min((unsigned long long)VE, cl - el);
+            store_user<DT, W>(buf, a.buf_off + co + el, nrem, r[u], aligned);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) R->epoch[b] = e;
+}
+
+// N = 1: buf = from_wire(to_wire(buf)); the mean scale is x * 1.0 (identity).
+template <int W>
+__global__ void __launch_bounds__(256) castscale_kernel(float* buf, unsigned long long n) {
+  const unsigned long long nv = (n + 7) / 8;
+  const bool aligned = (reinterpret_cast<uintptr_t>(buf) & 15) == 0;
+  for (unsigned long long v = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; v < nv;
+       v += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long e = v * 8;
+    const int nrem = (int)min(8ull, n - e);
+    const uint4 w = load_user<DT_F32, W>(buf, e, nrem, aligned);
+    store_user<DT_F32, W>(buf, e, nrem, w, aligned);
+  }
+}
+
+// Device barrier among all ranks (init/destroy): every rank stores its epoch into every
+// peer's barrier slot, then waits for all peers' slots.
+__global__ void barrier_kernel(const RankDev* ranks, unsigned long long bar_off,
+                               unsigned long long timeout_ns) {
+  const RankDev* R = ranks + blockIdx.x;
+  __shared__ uint32_t s_e;
+  if (threadIdx.x == 0) s_e = *R->bar_epoch + 1u;
+  __syncthreads();
+  const uint32_t e = s_e;
+  const int t = threadIdx.x;
+  if (t < R->N && t != R->rank)
+    st_release_sys(reinterpret_cast<uint32_t*>(R->ws[t] + bar_off) + R->rank, e);
+  if (t < R->N && t != R->rank) {
+    const uint32_t* f = reinterpret_cast<const uint32_t*>(R->ws[R->rank] + bar_off) + t;
+    const unsigned long long deadline = gtimer() + timeout_ns;
+    unsigned it = 0;
+    while ((int32_t)(ld_acquire_sys(f) - e) < 0) {
+      if ((++it & 255u) == 0 && gtimer() > deadline) {
+        atomicExch_system(R->err, kErrTimeout);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  if (t == 0) *R->bar_epoch = e;
+}
+
+template <int DT, int W>
+cudaError_t launch_typed(const LaunchArgs& a, bool cooperative, cudaStream_t stream) {
+  const dim3 grid(a.nlocal * a.G), block(kThreads);
+  if (cooperative) {
+    void* args[] = {const_cast<LaunchArgs*>(&a)};
+    return cudaLaunchCooperativeKernel((const void*)torus_kernel<DT, W>, grid, block, args, 0,
+                                       stream);
+  }
+  torus_kernel<DT, W><<<grid, block, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+template <int DT, int W>
+int max_ctas_typed() {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, torus_kernel<DT, W>, kThreads, 0) !=
+      cudaSuccess)
+    return 0;
+  return nb;
+}
+
+}  // namespace
+
+cudaError_t launch_torus(const LaunchArgs& a, int dtype, int wire, bool cooperative,
+                         cudaStream_t stream) {
+  if (dtype == wire) {
+    switch (dtype) {
+      case DT_F32: return launch_typed<DT_F32, DT_F32>(a, cooperative, stream);
+      case DT_F16: return launch_typed<DT_F16, DT_F16>(a, cooperative, stream);
+      case DT_BF16: return launch_typed<DT_BF16, DT_BF16>(a, cooperative, stream);
+      case DT_I32: return launch_typed<DT_I32, DT_I32>(a, cooperative, stream);
+    }
+  } else if (dtype == DT_F32 && wire == DT_F16) {
+    return launch_typed<DT_F32, DT_F16>(a, cooperative, stream);
+  } else if (dtype == DT_F32 && wire == DT_BF16) {
+    return launch_typed<DT_F32, DT_BF16>(a, cooperative, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int torus_kernel_max_ctas_per_sm(int dtype, int wire) {
+  if (dtype == wire) {
+    switch (dtype) {
+      case DT_F32: return max_ctas_typed<DT_F32, DT_F32>();
+      case DT_F16: return max_ctas_typed<DT_F16, DT_F16>();
+      case DT_BF16: return max_ctas_typed<DT_BF16, DT_BF16>();
+      case DT_I32: return max_ctas_typed<DT_I32, DT_I32>();
+    }
+  } else if (dtype == DT_F32 && wire == DT_F16) {
+    return max_ctas_typed<DT_F32, DT_F16>();
+  } else if (dtype == DT_F32 && wire == DT_BF16) {
+    return max_ctas_typed<DT_F32, DT_BF16>();
+  }
+  return 0;
+}
+
+cudaError_t launch_castscale(void* buf, unsigned long long n, int dtype, int wire,
+                             cudaStream_t stream) {
+  if (dtype != DT_F32) return cudaErrorInvalidValue;
+  const unsigned long long nv = (n + 7) / 8;
+  unsigned long long want = (nv + 255) / 256;
+  int blocks = (int)(want < 148ull * 8 ? want : 148ull * 8);
+  if (blocks < 1) blocks = 1;
+  if (wire == DT_F16)
+    castscale_kernel<DT_F16><<<blocks, 256, 0, stream>>>(reinterpret_cast<float*>(buf), n);
+  else if (wire == DT_BF16)
+    castscale_kernel<DT_BF16><<<blocks, 256, 0, stream>>>(reinterpret_cast<float*>(buf), n);
+  else
+    return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_barrier(const RankDev* ranks, int nlocal, unsigned long long bar_off,
+                           unsigned long long timeout_ns, cudaStream_t stream) {
+  if (nlocal > 1) {
+    void* args[] = {const_cast<RankDev**>(&ranks), &bar_off, &timeout_ns};
+    return cudaLaunchCooperativeKernel((const void*)barrier_kernel, dim3(nlocal), dim3(kMaxRanks),
+                                       args, 0, stream);
+  }
+  barrier_kernel<<<1, kMaxRanks, 0, stream>>>(ranks, bar_off, timeout_ns);
+  return cudaGetLastError();
+}
+
+}  // namespace torus

@@ -1,0 +1,165 @@
+"""Python binding of the 2D-Torus all-reduce.  Argument marshalling only:
+every step of the collective runs in libtorus.so's sm_100a kernels.  PyTorch supplies
+device memory, streams and the process group used once to exchange IPC handles.
+
+    comm = TorusComm.init(X=2, Y=4)          # one process per GPU, after init_process_group
+    comm.all_reduce(grad, op="mean")         # in place, async on the current stream
+    comm.all_reduce(grad32, op="mean", wire=torch.float16)   # PAPER.md:121 FP16 comm
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import torch
+
+from . import _lib
+from ._lib import check, torus_ipc_handle_t
+
+DTYPES = {torch.float32: 0, torch.float16: 1, torch.bfloat16: 2, torch.int32: 3}
+OPS = {"sum": 0, "mean": 1}
+
+
+def _dtype_code(dt) -> int:
+    try:
+        return DTYPES[dt]
+    except KeyError:
+        raise TypeError(f"unsupported dtype {dt}; supported: f32, f16, bf16, i32") from None
+
+
+def _stream_ptr(stream) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def pick_grid(world: int, p2p: Sequence[Sequence[int]] | None = None) -> tuple[int, int]:
+    """Topology layer (torus_pick_grid): choose (X, Y) for `world` GPUs."""
+    L = _lib.load()
+    X, Y = ctypes.c_int(), ctypes.c_int()
+    arr = None
+    if p2p is not None:
+        flat = [int(v) for row in p2p for v in row]
+        arr = (ctypes.c_int * len(flat))(*flat)
+    check(L.torus_pick_grid(world, arr, ctypes.byref(X), ctypes.byref(Y)), "torus_pick_grid")
+    return X.value, Y.value
+
+
+def partition(n: int, parts: int, q: int) -> tuple[list[int], list[int]]:
+    """Host partition logic of the library, exported for tests."""
+    L = _lib.load()
+    off = (ctypes.c_ulonglong * parts)()
+    ln = (ctypes.c_ulonglong * parts)()
+    check(L.torus_partition(n, parts, q, off, ln), "torus_partition")
+    return list(off), list(ln)
+
+
+class _CommBase:
+    _comm: ctypes.c_void_p
+
+    def grid(self) -> tuple[int, int]:
+        X, Y = ctypes.c_int(), ctypes.c_int()
+        check(_lib.load().torus_comm_grid(self._comm, ctypes.byref(X), ctypes.byref(Y)), "grid")
+        return X.value, Y.value
+
+    def ctas(self) -> int:
+        return _lib.load().torus_comm_ctas(self._comm)
+
+    def round_elems(self, wire: torch.dtype) -> int:
+        return _lib.load().torus_comm_round_elems(self._comm, _dtype_code(wire))
+
+    def launches(self, count: int, dtype: torch.dtype, wire: torch.dtype | None = None) -> int:
+        return _lib.load().torus_comm_launches(self._comm, count, _dtype_code(dtype),
+                                               _dtype_code(wire or dtype))
+
+    def async_error(self) -> int:
+        return _lib.load().torus_comm_get_async_error(self._comm)
+
+    def destroy(self) -> None:
+        if getattr(self, "_comm", None):
+            c, self._comm = self._comm, None
+            check(_lib.load().torus_comm_destroy(c), "torus_comm_destroy")
+
+    def __del__(self):  # best effort; destroy() is collective, call it explicitly
+        pass
+
+
+class TorusComm(_CommBase):
+    """One rank of the 2D-Torus communicator (one process per GPU)."""
+
+    def __init__(self, comm: ctypes.c_void_p, rank: int, world: int, device: int):
+        self._comm = comm
+        self.rank, self.world, self.device = rank, world, device
+
+    @classmethod
+    def init(cls, group=None, X: int = 0, Y: int = 0, ws_bytes: int = 0,
+             device: int | None = None) -> "TorusComm":
+        import torch.distributed as dist
+        L = _lib.load()
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        dev = torch.cuda.current_device() if device is None else device
+        torch.cuda.set_device(dev)
+        h = torus_ipc_handle_t()
+        check(L.torus_workspace_alloc(dev, ws_bytes, ctypes.byref(h)), "torus_workspace_alloc")
+        if world > 1:
+            blobs: list = [None] * world
+            dist.all_gather_object(blobs, bytes(h), group=group)
+        else:
+            blobs = [bytes(h)]
+        arr = (torus_ipc_handle_t * world)()
+        for r, blob in enumerate(blobs):
+            ctypes.memmove(ctypes.byref(arr[r]), blob, ctypes.sizeof(torus_ipc_handle_t))
+        comm = ctypes.c_void_p()
+        rc = L.torus_comm_init(rank, world, X, Y, arr, ctypes.byref(comm))
+        msg = "" if rc == 0 else L.torus_last_error().decode(errors="replace")
+        if world > 1:  # every rank learns whether every peer succeeded (no half-built comm)
+            status: list = [None] * world
+            dist.all_gather_object(status, (rc, msg), group=group)
+        else:
+            status = [(rc, msg)]
+        bad = [(r, s) for r, s in enumerate(status) if s[0] != 0]
+        if bad:
+            if rc == 0:
+                L.torus_comm_destroy(comm)  # peers failed: no collective barrier possible
+            elif rc != 0:
+                L.torus_workspace_release(ctypes.byref(h))
+            raise RuntimeError(f"torus_comm_init failed on ranks {bad}")
+        return cls(comm, rank, world, dev)
+
+    def all_reduce(self, t: torch.Tensor, op: str = "mean", wire: torch.dtype | None = None,
+                   stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """In-place all-reduce of a contiguous CUDA tensor (sum or mean over all ranks)."""
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("torus all_reduce needs a contiguous CUDA tensor")
+        check(_lib.load().torus_allreduce_ex(
+            self._comm, ctypes.c_void_p(t.data_ptr()), t.numel(), _dtype_code(t.dtype),
+            _dtype_code(wire or t.dtype), OPS[op], _stream_ptr(stream)), "torus_allreduce_ex")
+        return t
+
+
+class VirtualTorus(_CommBase):
+    """A whole X-by-Y grid emulated on one GPU (one cooperative launch per round); runs
+    the product kernel with every virtual rank's peer pointers aimed at local slabs."""
+
+    def __init__(self, X: int, Y: int, device: int = 0, ctas: int = 0, ws_bytes: int = 0):
+        L = _lib.load()
+        torch.cuda.set_device(device)
+        self._comm = ctypes.c_void_p()
+        check(L.torus_vcomm_init(device, X, Y, ctas, ws_bytes, ctypes.byref(self._comm)),
+              "torus_vcomm_init")
+        self.X, self.Y, self.N, self.device = X, Y, X * Y, device
+
+    def all_reduce(self, tensors: Sequence[torch.Tensor], op: str = "mean",
+                   wire: torch.dtype | None = None,
+                   stream: torch.cuda.Stream | None = None) -> Sequence[torch.Tensor]:
+        if len(tensors) != self.N:
+            raise ValueError(f"need {self.N} tensors, one per virtual rank")
+        t0 = tensors[0]
+        for t in tensors:
+            if not t.is_cuda or not t.is_contiguous() or t.dtype != t0.dtype or t.numel() != t0.numel():
+                raise ValueError("virtual ranks need equal contiguous CUDA tensors")
+        ptrs = (ctypes.c_void_p * self.N)(*[t.data_ptr() for t in tensors])
+        check(_lib.load().torus_vallreduce(
+            self._comm, ptrs, t0.numel(), _dtype_code(t0.dtype), _dtype_code(wire or t0.dtype),
+            OPS[op], _stream_ptr(stream)), "torus_vallreduce")
+        return tensors

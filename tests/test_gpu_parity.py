@@ -1,0 +1,230 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, element by element.
+
+Single GPU: whole X-by-Y grids emulated as virtual ranks (one cooperative launch of the
+product kernel, peer pointers aimed at local slabs) -- bit-exact for every dtype under
+the oracle's PHASE policy with the library's quantum and round size.
+Full size: the 25,557,032-element fp16 mean 2x4 case, sampled outputs vs the oracle's
+closed form, plus properties that hold at any size.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synthetic
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TD = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16, "i32": torch.int32}
+PAIRS = [("f32", "f32"), ("f16", "f16"), ("bf16", "bf16"), ("i32", "i32"), ("f32", "f16"),
+         ("f32", "bf16")]
+GRIDS = [(2, 1), (1, 2), (2, 2), (2, 4), (4, 2), (1, 8), (8, 1), (3, 3), (2, 3)]
+
+
+def from_dev(t, dtype):
+    if dtype == "bf16":
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def _np_to_dev(a, dtype):
+    if dtype == "bf16":
+        return torch.from_numpy(a.view(np.int16).copy()).view(torch.bfloat16).cuda()
+    return torch.from_numpy(a.copy()).cuda()
+
+
+def q_of(wire):
+    return 16 // (2 if wire in ("f16", "bf16") else 4)
+
+
+def _isnan_bits(a):
+    if a.dtype == np.uint16:  # bf16 bit patterns
+        return ((a & 0x7F80) == 0x7F80) & ((a & 0x7F) != 0)
+    if a.dtype in (np.float16, np.float32):
+        return np.isnan(a)
+    return np.zeros(a.shape, dtype=bool)
+
+
+def assert_same(got, ref, what):
+    """Bit-exact equality; NaNs compare as a class (payloads are not compared, C9)."""
+    w = {1: np.uint8, 2: np.uint16, 4: np.uint32}[got.dtype.itemsize]
+    gn, rn = _isnan_bits(got), _isnan_bits(ref)
+    eq = (got.view(w) == ref.view(w)) | (gn & rn)
+    if not eq.all():
+        i = int(np.flatnonzero(~eq)[0])
+        raise AssertionError(f"{what}: {int((~eq).sum())} mismatches, first at {i}: "
+                             f"{got[i]!r} vs {ref[i]!r}")
+
+
+def run_virtual(vt, ins, dtype, wire, op):
+    ts = [_np_to_dev(a, dtype) for a in ins]
+    vt.all_reduce(ts, op=op, wire=TD[wire])
+    torch.cuda.synchronize()
+    assert vt.async_error() == 0
+    return [from_dev(t, dtype) for t in ts]
+
+
+@pytest.fixture(scope="module")
+def vgrids():
+    from paper_1811_05233_b200 import VirtualTorus
+    made = {}
+
+    def get(X, Y, ws=0):
+        key = (X, Y, ws)
+        if key not in made:
+            made[key] = VirtualTorus(X, Y, device=0, ws_bytes=ws)
+        return made[key]
+    yield get
+    for vt in made.values():
+        vt.destroy()
+
+
+@pytest.mark.parametrize("X,Y", GRIDS)
+@pytest.mark.parametrize("dtype,wire", PAIRS)
+@pytest.mark.parametrize("op", ["sum", "mean"])
+def test_virtual_grid_bit_exact(vgrids, X, Y, dtype, wire, op):
+    vt = vgrids(X, Y)
+    N = X * Y
+    R = vt.round_elems(TD[wire])
+    for D in (1, 7, 1000, 4099, 200_003):
+        dist = "full" if dtype == "i32" else ("wide" if D < 5000 else "normal")
+        ins = synthetic.make_all(dist, D, N, dtype, salt=D % 97)
+        got = run_virtual(vt, ins, dtype, wire, op)
+        ref = oracle.torus_allreduce(ins, X, Y, dtype, wire=wire, op=op, q=q_of(wire),
+                                     round_elems=R)
+        for r in range(N):
+            assert_same(got[r], ref[r], f"{X}x{Y} {dtype}/{wire} {op} D={D} rank {r}")
+
+
+@pytest.mark.parametrize("X,Y", [(2, 2), (2, 4), (1, 4)])
+@pytest.mark.parametrize("dtype,wire", [("f16", "f16"), ("f32", "bf16"), ("i32", "i32")])
+def test_multi_round(vgrids, X, Y, dtype, wire):
+    """A slab far smaller than the message forces several rounds."""
+    vt = vgrids(X, Y, ws=1 << 20)  # 1 MiB slab
+    R = vt.round_elems(TD[wire])
+    assert 0 < R < 300_000
+    D = 3 * R + 12345
+    N = X * Y
+    ins = synthetic.make_all("full" if dtype == "i32" else "normal", D, N, dtype)
+    got = run_virtual(vt, ins, dtype, wire, "mean")
+    ref = oracle.torus_allreduce(ins, X, Y, dtype, wire=wire, op="mean", q=q_of(wire), round_elems=R)
+    for r in range(N):
+        assert_same(got[r], ref[r], f"rounds {X}x{Y} {dtype}/{wire} rank {r}")
+    assert vt.launches(D, TD[dtype], TD[wire]) == 4
+
+
+def test_unaligned_buffers(vgrids):
+    """Buffers offset by one element take the scalar (non-vector) user-buffer path."""
+    X, Y, D = 2, 2, 5001
+    vt = vgrids(X, Y)
+    ins = synthetic.make_all("normal", D, 4, "f32")
+    ts = []
+    for a in ins:
+        base = torch.zeros(D + 1, dtype=torch.float32, device="cuda")
+        base[1:] = torch.from_numpy(a)
+        ts.append(base[1:])
+    vt.all_reduce(ts, op="sum", wire=torch.float16)
+    torch.cuda.synchronize()
+    ref = oracle.torus_allreduce(ins, X, Y, "f32", wire="f16", op="sum", q=8,
+                                 round_elems=vt.round_elems(torch.float16))
+    for r in range(4):
+        assert_same(ts[r].cpu().numpy(), ref[r], f"unaligned rank {r}")
+
+
+def test_repeated_calls_and_zero_count(vgrids):
+    """Back-to-back calls (epoch flags advance, slots are reused) with varying counts."""
+    X, Y = 2, 4
+    vt = vgrids(X, Y)
+    R = vt.round_elems(torch.float16)
+    for it, D in enumerate((0, 33, 100_000, 8, 77_777, 1)):
+        ins = synthetic.make_all("normal", D, 8, "f16", salt=it)
+        got = run_virtual(vt, ins, "f16", "f16", "mean")
+        if D == 0:
+            continue
+        ref = oracle.torus_allreduce(ins, X, Y, "f16", op="mean", q=8, round_elems=R)
+        for r in range(8):
+            assert_same(got[r], ref[r], f"call {it} D={D} rank {r}")
+
+
+def test_special_values(vgrids):
+    """inf / nan / subnormal / signed zero go through the same rounding as the oracle."""
+    X, Y, D = 2, 2, 64
+    vt = vgrids(X, Y)
+    specials = np.array([np.inf, -np.inf, np.nan, 0.0, -0.0, 1e-45, -1e-45, 6e-8, 65504.0,
+                         65520.0, -65536.0, 3.4e38, 1e-38, 5.9e-8, 2.98e-8], dtype=np.float32)
+    g = np.random.Generator(np.random.PCG64(5))
+    ins = [g.choice(specials, D).astype(np.float32) for _ in range(4)]
+    for wire in ("f32", "f16", "bf16"):
+        got = run_virtual(vt, ins, "f32", wire, "mean")
+        ref = oracle.torus_allreduce(ins, X, Y, "f32", wire=wire, op="mean", q=q_of(wire),
+                                     round_elems=vt.round_elems(TD[wire]))
+        for r in range(4):
+            assert_same(got[r], ref[r], f"specials {wire} rank {r}")
+
+
+def test_single_rank_cast_scale():
+    """N = 1 (a7): f32 buffer with f16/bf16 wire -> fused cast round trip; same-type no-op."""
+    from paper_1811_05233_b200 import VirtualTorus
+    vt = VirtualTorus(1, 1, device=0)
+    try:
+        for wire in ("f16", "bf16", "f32"):
+            for D in (1, 13, 1 << 20):
+                x = synthetic.make("wide", D, 0, "f32")
+                got = run_virtual(vt, [x], "f32", wire, "mean")[0]
+                ref = oracle.torus_allreduce([x], 1, 1, "f32", wire=wire, op="mean")[0]
+                assert_same(got, ref, f"N=1 {wire} D={D}")
+        assert vt.launches(1000, torch.float32, torch.float32) == 0
+        assert vt.launches(1000, torch.float32, torch.float16) == 1
+    finally:
+        vt.destroy()
+
+
+def test_full_size_resnet50_sampled():
+    """BASELINE config 2 at full size, in the bench's launch configuration (2x4 grid,
+    fp16, mean, default slab -> one round): sampled outputs vs the oracle's closed form,
+    plus all-ranks-identical and the f64 error bound on the sample."""
+    from paper_1811_05233_b200 import VirtualTorus
+    X, Y, D = 2, 4, synthetic.RESNET50_NUMEL
+    vt = VirtualTorus(X, Y, device=0)
+    try:
+        R = vt.round_elems(torch.float16)
+        assert R >= D, "north-star message must be a single round"
+        ins = synthetic.make_all("grad", D, 8, "f16")
+        ts = [_np_to_dev(a, "f16") for a in ins]
+        vt.all_reduce(ts, op="mean")
+        torch.cuda.synchronize()
+        assert vt.async_error() == 0
+        for t in ts[1:]:
+            assert torch.equal(t, ts[0])
+        g = np.random.Generator(np.random.PCG64(1))
+        off, ln = oracle.qpart(D, X, 8)
+        idx = set(g.integers(0, D, 4000).tolist()) | {0, 1, D - 1, D - 2, D - 9}
+        for o, l in zip(off, ln):  # chunk and sub-chunk boundaries
+            so, sl = oracle.qpart(l, Y, 8)
+            for a, b in zip(so, sl):
+                idx |= {o + a, o + a + b - 1}
+        idx = np.array(sorted(i for i in idx if 0 <= i < D))
+        got = ts[3].cpu().numpy()[idx]
+        ref = oracle.torus_elements(ins, X, Y, idx, "f16", op="mean", q=8, round_elems=R)
+        assert_same(got, ref, "full-size sample")
+        exact = sum(a[idx].astype(np.float64) for a in ins) / 8
+        mag = sum(np.abs(a[idx].astype(np.float64)) for a in ins) / 8
+        assert (np.abs(got.astype(np.float64) - exact) <= 1e-2 * mag + 1e-7).all()
+    finally:
+        vt.destroy()
+
+
+def test_errors_are_reported():
+    from paper_1811_05233_b200 import TorusError, VirtualTorus
+    vt = VirtualTorus(2, 2, device=0)
+    try:
+        t = [torch.zeros(10, dtype=torch.int32, device="cuda") for _ in range(4)]
+        with pytest.raises(TorusError, match="UNSUPPORTED"):
+            vt.all_reduce(t, wire=torch.float16)       # i32 buffer with a float wire
+        t16 = [torch.zeros(10, dtype=torch.float16, device="cuda") for _ in range(4)]
+        with pytest.raises(TorusError, match="UNSUPPORTED"):
+            vt.all_reduce(t16, wire=torch.float32)     # wire wider than the buffer
+    finally:
+        vt.destroy()
+    with pytest.raises(TorusError, match="GRID"):
+        VirtualTorus(5, 5, device=0)                   # > 16 virtual ranks
