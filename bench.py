@@ -1,0 +1,455 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for the B200 2D-Torus all-reduce.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl torus|reference] ...
+  (N > 1: launched by torch.distributed.run, one rank per GPU, NCCL process group)
+
+A "step" is one 2D-Torus all-reduce (all SURVEY Sec. 8(a) rows) of the ResNet-50
+gradient buffer (25,557,032 elements, synthetic N(0,1)*2^-7 values, per-rank seed
+20181113 + rank).  Workloads:
+  N >= 2 : fp16 buffer, fp16 wire, mean, grid 2x4 (8), 2x2 (4), 1x2 (2)  -> BASELINE metric
+  N == 1 : f32 buffer, fp16 wire, mean: the fused cast/scale-only degenerate case
+value = busbw (GB/s) = S * 2(N-1)/N / t, t = max over ranks of the per-call device time
+(CUDA events on the launching stream); at N == 1 busbw is 0 by definition and value is
+the algbw S/t of the degenerate pass (S = fp16 message bytes).  L2 is flushed (256 MiB
+write) before every timed call, outside the events.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synthetic  # noqa: E402  (seeded inputs only; no method arithmetic)
+
+METRIC = ("2D-torus allreduce busbw GB/s (fp16 25.6M elems, 8×B200, max over ranks) "
+          "vs NVLink peak")
+NVLINK_NOMINAL = 900.0      # GB/s per direction per GPU (18 x 50)
+NVLINK_MEASURED = 770.0     # GB/s per direction, B200_PROFILING.md "peer copy" measurement
+DEFAULT_GRID = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
+DT_BYTES = {"f32": 4, "f16": 2, "bf16": 2, "i32": 4}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="torus", choices=["torus", "reference"])
+    p.add_argument("--grid", default=None, help="XxY (default: 2x4 / 2x2 / 1x2 / 1x1)")
+    p.add_argument("--count", type=int, default=synthetic.RESNET50_NUMEL)
+    p.add_argument("--dtype", default=None, help="buffer dtype (default f16; f32 at N=1)")
+    p.add_argument("--wire", default="f16")
+    p.add_argument("--op", default="mean", choices=["sum", "mean"])
+    p.add_argument("--no-nccl", action="store_true", help="skip the NCCL comparison")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
+    p.add_argument("--out", default=None, help="also append the JSON line to this file")
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------------------
+# distributed plumbing
+# ----------------------------------------------------------------------------------------
+def dist_setup(n_gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def gather_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------------------
+# clocks (B200_PROFILING.md "clocks DURING the timed region")
+# ----------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, enabled):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+        if enabled:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            try:
+                self.fh = open(self.path, "w")
+                self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}",
+                                              "--format=csv,noheader,nounits", "-lms", "100"],
+                                             stdout=self.fh, stderr=subprocess.DEVNULL)
+            except OSError:
+                self.proc = None
+
+    def stop(self, n_gpus):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or not f[0].isdigit() or int(f[0]) >= n_gpus:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        top = sorted(sm)[len(sm) // 2:]  # samples under load: upper half
+        return {"sm_mhz": statistics.median(top), "sm_max_mhz": max(mx),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------------------
+# the torus arm
+# ----------------------------------------------------------------------------------------
+def make_input(args, rank, dtype_s):
+    dist_name = "grad"
+    a = synthetic.make(dist_name, args.count, rank, dtype_s if dtype_s != "bf16" else "bf16")
+    return a
+
+
+def to_tensor(a, dtype_s, device):
+    import torch
+    if dtype_s == "bf16":
+        return torch.from_numpy(a.view(np.int16).copy()).view(torch.bfloat16).to(device)
+    return torch.from_numpy(a).to(device)
+
+
+def run_torus(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1811_05233_b200 import TorusComm
+
+    rank, world, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    X, Y = (tuple(int(v) for v in args.grid.lower().split("x")) if args.grid
+            else DEFAULT_GRID.get(world, (world, 1)))
+    dtype_s = args.dtype or ("f32" if world == 1 else "f16")
+    wire_s = args.wire if dtype_s == "f32" else dtype_s
+    TD = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16, "i32": torch.int32}
+    D = args.count
+    S = D * DT_BYTES[wire_s]                    # message bytes on the wire (BASELINE: fp16)
+    bus = 2.0 * (world - 1) / world
+
+    comm = TorusComm.init(X=X, Y=Y)
+    host = make_input(args, rank, dtype_s)
+    x0 = to_tensor(host, dtype_s, dev)
+    buf = x0.clone()
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def call():
+        comm.all_reduce(buf, op=args.op, wire=TD[wire_s], stream=stream)
+
+    # sanity (not the parity gate -- that is tests/): all ranks agree, and the result is
+    # within the north-star tolerance of an f64 all-reduce done with NCCL in f64.
+    buf.copy_(x0)
+    call()
+    torch.cuda.synchronize()
+    sanity = {}
+    if world > 1:
+        ref = x0.double()
+        dist.all_reduce(ref)
+        if args.op == "mean":
+            ref /= world
+        mag = x0.double().abs()
+        dist.all_reduce(mag)
+        if args.op == "mean":
+            mag /= world
+        err = float(((buf.double() - ref).abs() / (mag + 1e-30)).max())
+        cs = buf.view(torch.uint8).to(torch.int64).sum()
+        cs_all = [torch.zeros_like(cs) for _ in range(world)]
+        dist.all_gather(cs_all, cs)
+        sanity = {"ranks_identical": all(int(c) == int(cs_all[0]) for c in cs_all),
+                  "max_err_over_sum_abs_vs_f64": err}
+    else:
+        ref = x0.to(TD[wire_s]).to(x0.dtype)
+        sanity = {"ranks_identical": True, "equals_cast_roundtrip": bool(torch.equal(buf, ref))}
+    if comm.async_error():
+        raise SystemExit("device watchdog fired")
+
+    # ---- device-timed region ----
+    for _ in range(max(args.warmup, 3)):
+        call()
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = Clocks(rank == 0)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    barrier(world)
+    for s in range(args.steps):
+        flush.fill_(s & 0xFF)                   # evict L2 (256 MiB > 126 MB), untimed
+        ev[s][0].record(stream)
+        call()
+        ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop(args.gpus) if rank == 0 else None
+    times = [a.elapsed_time(b) * 1e-3 for a, b in ev]   # seconds
+    t_local = sum(times) / len(times)
+    t = gather_max(t_local, world)
+    t_min = gather_max(min(times), world)
+    algbw = S / t / 1e9
+    busbw = algbw * bus
+    if comm.async_error():
+        raise SystemExit("device watchdog fired during timing")
+
+    # ---- NCCL comparator on the same tensor (like for like: AVG for mean) ----
+    nccl = None
+    if world > 1 and not args.no_nccl:
+        op = dist.ReduceOp.AVG if args.op == "mean" else dist.ReduceOp.SUM
+        for _ in range(max(args.warmup, 3)):
+            dist.all_reduce(buf, op=op)
+        torch.cuda.synchronize()
+        barrier(world)
+        evn = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        ns = torch.cuda.current_stream()
+        for s in range(args.steps):
+            flush.fill_(s & 0xFF)
+            evn[s][0].record(ns)
+            dist.all_reduce(buf, op=op)
+            evn[s][1].record(ns)
+        torch.cuda.synchronize()
+        tn = gather_max(sum(a.elapsed_time(b) for a, b in evn) * 1e-3 / args.steps, world)
+        nccl = {"busbw": S / tn / 1e9 * bus, "algbw": S / tn / 1e9, "us": tn * 1e6,
+                "version": ".".join(map(str, torch.cuda.nccl.version())),
+                "nvls_env": os.environ.get("NCCL_NVLS_ENABLE", "default")}
+        buf.copy_(x0)
+
+    # ---- e2e through the public API with HOST buffers: H2D, all-reduce, D2H ----
+    e2e = None
+    if not args.no_e2e:
+        hin = torch.from_numpy(host.view(np.int16) if dtype_s == "bf16" else host).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        view = buf.view(torch.int16) if dtype_s == "bf16" else buf
+        for _ in range(2):
+            view.copy_(hin, non_blocking=True)
+            call()
+            hout.copy_(view, non_blocking=True)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(args.steps):
+            view.copy_(hin, non_blocking=True)
+            call()
+            hout.copy_(view, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = gather_max(e0.elapsed_time(e1) * 1e-3 / args.steps, world)
+        nb = host.nbytes
+        e2e = {"value": (S / te / 1e9) * (bus if world > 1 else 1.0),
+               "unit": "GB/s", "us_per_step": te * 1e6,
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb}
+
+    launches = comm.launches(D, TD[dtype_s], TD[wire_s])
+    # ---- roofline of the dominant (only) kernel ----
+    if world > 1:
+        alg_bytes = bus * S                        # NVLink bytes per rank per launch
+        achieved = alg_bytes / (t / launches) / 1e9
+        roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_MEASURED,
+                "unit": "GB/s", "frac": achieved / NVLINK_MEASURED,
+                "frac_of_nominal_900": achieved / NVLINK_NOMINAL,
+                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction "
+                               "(MEASURED_PEAKS.json has no NVLink entry)",
+                "traffic": None, "kernel": "torus_kernel",
+                "algorithmic_bytes_per_launch": alg_bytes}
+    else:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+            os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+        hbm = peaks.get("hbm_gbs", 6650.0)
+        alg_bytes = 2.0 * D * DT_BYTES[dtype_s] if dtype_s != wire_s else 0.0
+        achieved = alg_bytes / t / 1e9 if launches else 0.0
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
+                "traffic": load_traffic("castscale"), "kernel": "castscale_kernel",
+                "algorithmic_bytes_per_launch": alg_bytes}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args, X, Y, dtype_s, wire_s, world)
+
+    comm.destroy()
+    if rank != 0:
+        return
+    value = busbw if world > 1 else algbw
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": wire_s, "data": "synthetic",
+        "config": {"workload": ("resnet50-grad-allreduce" if world > 1 else
+                                "resnet50-grad-castscale-degenerate (N=1)"),
+                   "count": D, "buffer_dtype": dtype_s, "wire_dtype": wire_s, "op": args.op,
+                   "grid": f"{X}x{Y}", "parallelism": f"torus{X}x{Y}", "ctas_per_rank": comm_ctas(),
+                   "message_bytes": S, "l2": "flushed (256 MiB write) before every timed call",
+                   "value_is": "busbw" if world > 1 else "algbw (busbw is 0 at N=1)"},
+        "algbw": algbw, "busbw": busbw, "us_per_call": t * 1e6, "us_per_call_min": t_min * 1e6,
+        "frac_nvlink_900": busbw / NVLINK_NOMINAL if world > 1 else None,
+        "gpu_launches": launches * args.steps,
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "nccl": nccl, "clocks": clk,
+        "sanity": sanity,
+    }
+    emit(line, args)
+
+
+_CTAS = [None]
+
+
+def comm_ctas():
+    return _CTAS[0]
+
+
+def load_traffic(kernel):
+    """dram bytes per launch from a committed ncu --set full capture, if present."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def emit(line, args):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if args.out:
+        with open(args.out, "a") as f:
+            f.write(s + "\n")
+
+
+# ----------------------------------------------------------------------------------------
+# the oracle (CPU) legs: cpu_baseline and --impl reference
+# ----------------------------------------------------------------------------------------
+def oracle_sample_size(X, Y):
+    # ~ a few seconds of single-threaded oracle work per call
+    return 1 << 22 if X * Y == 1 else (1 << 20)
+
+
+def time_oracle(X, Y, dtype_s, wire_s, op, D):
+    import oracle
+    N = X * Y
+    ins = synthetic.make_all("grad", D, N, dtype_s)
+    oracle.lib()
+    t0 = time.perf_counter()
+    oracle.torus_allreduce(ins, X, Y, dtype_s, wire=wire_s, op=op, q=16 // DT_BYTES[wire_s])
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(args, X, Y, dtype_s, wire_s, world):
+    D = min(args.count, oracle_sample_size(X, Y))
+    reps, tot = 0, 0.0
+    while tot < 10.0 and reps < 50:
+        tot += time_oracle(X, Y, dtype_s, wire_s, args.op, D)
+        reps += 1
+    t = tot / reps
+    S = D * DT_BYTES[wire_s]
+    bus = 2.0 * (world - 1) / world
+    v = S / t / 1e9 * (bus if world > 1 else 1.0)
+    return {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{X}x{Y} grid, {D} of {args.count} elements, {dtype_s} buffer / "
+                      f"{wire_s} wire, {args.op}; {reps} reps, {t:.3f} s each, "
+                      "single-threaded C (oracle/torus_oracle.c)",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    X, Y = (tuple(int(v) for v in args.grid.lower().split("x")) if args.grid
+            else DEFAULT_GRID.get(world, (world, 1)))
+    dtype_s = args.dtype or ("f32" if world == 1 else "f16")
+    wire_s = args.wire if dtype_s == "f32" else dtype_s
+    D = min(args.count, oracle_sample_size(X, Y))
+    for _ in range(max(args.warmup, 1) if D < (1 << 21) else 1):
+        time_oracle(X, Y, dtype_s, wire_s, args.op, D)
+    ts = [time_oracle(X, Y, dtype_s, wire_s, args.op, D) for _ in range(args.steps)]
+    t = sum(ts) / len(ts)
+    S = D * DT_BYTES[wire_s]
+    bus = 2.0 * (world - 1) / world
+    v = S / t / 1e9 * (bus if world > 1 else 1.0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": wire_s,
+        "data": "synthetic",
+        "config": {"workload": ("resnet50-grad-allreduce" if world > 1 else
+                                "resnet50-grad-castscale-degenerate (N=1)"),
+                   "count": args.count, "buffer_dtype": dtype_s, "wire_dtype": wire_s,
+                   "op": args.op, "grid": f"{X}x{Y}", "parallelism": f"torus{X}x{Y}"},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{D} of {args.count} elements per rank per step, "
+                                   f"{X}x{Y} simulated ranks, single-threaded C oracle"},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    emit(line, args)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import paper_1811_05233_b200.torus as T
+    orig_init = T.TorusComm.init
+
+    def init_and_record(*a, **k):
+        c = orig_init(*a, **k)
+        _CTAS[0] = c.ctas()
+        return c
+    T.TorusComm.init = init_and_record
+    run_torus(args)
+    try:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:
+        pass
+
+
+if __name__ == "__main__":
+    main()

@@ -470,6 +470,7 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
     c->poisoned = true;
     return fail(TORUS_ERR_TIMEOUT, "communicator has an async error; destroy it");
   }
+  if (count == 0) return TORUS_OK;  // nothing enqueued; empty buffers may be NULL
   const size_t esz = wire_size(dtype);
   bool aligned = true;
   for (int l = 0; l < c->nlocal; ++l) {
@@ -478,7 +479,6 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
     if (p % esz) return fail(TORUS_ERR_INVALID_ARG, "buffer %d not element-aligned", l);
     if (p % kVecBytes) aligned = false;
   }
-  if (count == 0) return TORUS_OK;
   if (count > (size_t)1 << 48) return fail(TORUS_ERR_INVALID_ARG, "count overflow");
   if (c->world == 1) {
     if (dtype == wire) return TORUS_OK;  // sum/mean over one rank of wire values: identity

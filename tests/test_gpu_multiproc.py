@@ -1,0 +1,138 @@
+"""Multi-process parity on real GPUs: one process per GPU, CUDA IPC + P2P over NVLink,
+the product kernel vs the oracle, bit-exact.  Needs >= 2 GPUs
+(run with `gpurun --gpus 2` / `--gpus 4`); skipped on a 1-GPU box.
+
+Every rank generates every rank's seeded inputs (so it can run the oracle itself),
+then the ranks barrier, launch together, synchronize, and only then compare -- so no
+kernel ever spin-waits on a peer that is busy in the CPU oracle.
+"""
+import os
+import socket
+import traceback
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+TD = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16, "i32": torch.int32}
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _to_dev(a, dtype, dev):
+    if dtype == "bf16":
+        return torch.from_numpy(a.view(np.int16).copy()).view(torch.bfloat16).to(dev)
+    return torch.from_numpy(a.copy()).to(dev)
+
+
+def _from_dev(t, dtype):
+    if dtype == "bf16":
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+    return t.cpu().numpy()
+
+
+def _same(got, ref):
+    w = {2: np.uint16, 4: np.uint32}[got.dtype.itemsize]
+    if got.dtype == np.uint16:
+        gn = ((got & 0x7F80) == 0x7F80) & ((got & 0x7F) != 0)
+        rn = ((ref & 0x7F80) == 0x7F80) & ((ref & 0x7F) != 0)
+    elif got.dtype in (np.float16, np.float32):
+        gn, rn = np.isnan(got), np.isnan(ref)
+    else:
+        gn = rn = np.zeros(got.shape, bool)
+    eq = (got.view(w) == ref.view(w)) | (gn & rn)
+    return bool(eq.all()), int((~eq).sum())
+
+
+def _worker(rank, world, port, cases, errfile):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    try:
+        import torch.distributed as dist
+
+        import oracle
+        import synthetic
+        from paper_1811_05233_b200 import TorusComm
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        comms = {}
+        for (X, Y, dtype, wire, op, D, dist_name) in cases:
+            if (X, Y) not in comms:
+                comms[(X, Y)] = TorusComm.init(X=X, Y=Y)
+            comm = comms[(X, Y)]
+            ins = synthetic.make_all(dist_name, D, world, dtype, salt=D % 89)
+            t = _to_dev(ins[rank], dtype, f"cuda:{rank}")
+            torch.cuda.synchronize()
+            dist.barrier()
+            comm.all_reduce(t, op=op, wire=TD[wire])
+            torch.cuda.synchronize()
+            assert comm.async_error() == 0, "watchdog"
+            got = _from_dev(t, dtype)
+            q = 16 // (2 if wire in ("f16", "bf16") else 4)
+            R = comm.round_elems(TD[wire])
+            if D <= 300_000:
+                ref = oracle.torus_allreduce(ins, X, Y, dtype, wire=wire, op=op, q=q,
+                                             round_elems=R)[rank]
+                ok, nbad = _same(got, ref)
+            else:  # full size: sampled outputs vs the oracle's closed form
+                g = np.random.Generator(np.random.PCG64(rank))
+                idx = np.unique(np.concatenate([g.integers(0, D, 3000), [0, D - 1]]))
+                ref = oracle.torus_elements(ins, X, Y, idx, dtype, wire=wire, op=op, q=q,
+                                            round_elems=R)
+                ok, nbad = _same(got[idx], ref)
+            assert ok, f"rank {rank} {X}x{Y} {dtype}/{wire} {op} D={D}: {nbad} mismatches"
+            dist.barrier()
+        for c in comms.values():
+            dist.barrier()
+            c.destroy()
+        dist.destroy_process_group()
+    except Exception:
+        with open(errfile, "a") as f:
+            f.write(f"rank {rank}:\n{traceback.format_exc()}\n")
+        raise
+
+
+def _run(world, cases, tmp_path):
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    errfile = str(tmp_path / "errors.txt")
+    try:
+        mp.spawn(_worker, args=(world, _free_port(), cases, errfile), nprocs=world, join=True)
+    except Exception as e:
+        msg = open(errfile).read() if os.path.exists(errfile) else str(e)
+        raise AssertionError(msg) from None
+
+
+PAIRS = [("f32", "f32"), ("f16", "f16"), ("bf16", "bf16"), ("i32", "i32"), ("f32", "f16"),
+         ("f32", "bf16")]
+
+
+def _cases(grids, sizes=(1, 4099, 200_003), ops=("sum", "mean")):
+    out = []
+    for (X, Y) in grids:
+        for dtype, wire in PAIRS:
+            for op in ops:
+                for D in sizes:
+                    dn = "full" if dtype == "i32" else ("wide" if D < 5000 else "normal")
+                    out.append((X, Y, dtype, wire, op, D, dn))
+    return out
+
+
+def test_two_gpus(tmp_path):
+    _run(2, _cases([(2, 1), (1, 2)]), tmp_path)
+
+
+def test_four_gpus(tmp_path):
+    cases = _cases([(2, 2), (4, 1), (1, 4)], ops=("mean",))
+    cases += [(2, 2, "f16", "f16", "mean", 25_557_032, "grad")]  # config 2 shape on 2x2
+    _run(4, cases, tmp_path)
