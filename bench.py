@@ -42,8 +42,9 @@ DT_BYTES = {"f32": 4, "f16": 2, "bf16": 2, "i32": 4}
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=400)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--ctas", type=int, default=0, help="CTAs per rank (env TORUS_CTAS)")
     p.add_argument("--impl", default="torus", choices=["torus", "reference"])
     p.add_argument("--grid", default=None, help="XxY (default: 2x4 / 2x2 / 1x2 / 1x1)")
     p.add_argument("--count", type=int, default=synthetic.RESNET50_NUMEL)
@@ -106,7 +107,7 @@ class Clocks:
             try:
                 self.fh = open(self.path, "w")
                 self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}",
-                                              "--format=csv,noheader,nounits", "-lms", "100"],
+                                              "--format=csv,noheader,nounits", "-lms", "50"],
                                              stdout=self.fh, stderr=subprocess.DEVNULL)
             except OSError:
                 self.proc = None
@@ -207,12 +208,16 @@ def run_torus(args):
     if comm.async_error():
         raise SystemExit("device watchdog fired")
 
-    # ---- device-timed region ----
-    for _ in range(max(args.warmup, 3)):
-        call()
-    torch.cuda.synchronize()
-    barrier(world)
+    # ---- device-timed region (the clock sampler starts before the warm-up) ----
     clocks = Clocks(rank == 0)
+    t_w = time.perf_counter()
+    while True:  # warm-up: >= W calls and >= 0.3 s so the sampler has seen load
+        for _ in range(max(args.warmup, 3)):
+            call()
+        torch.cuda.synchronize()
+        if gather_max(time.perf_counter() - t_w, world) > 0.3:
+            break
+    barrier(world)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     torch.cuda.synchronize()
@@ -431,6 +436,8 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.ctas:
+        os.environ["TORUS_CTAS"] = str(args.ctas)
     if args.impl == "reference":
         run_reference(args)
         return

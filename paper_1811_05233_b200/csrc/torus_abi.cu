@@ -75,6 +75,7 @@ struct torus_comm {
   int rank = 0, world = 1, X = 1, Y = 1;
   int device = 0;
   int G = 0;
+  int tile_vecs = 960;      // 16-byte vectors per tile piece (env TORUS_TILE)
   int nlocal = 1;           // > 1: virtual ranks on one device
   bool virt = false;
   size_t slab_size = 0;
@@ -151,7 +152,7 @@ int pick_ctas(int device, int nlocal) {
   for (int d = 0; d < 4; ++d) per_sm = std::min(per_sm, torus_kernel_max_ctas_per_sm(d, d));
   if (per_sm < 1) per_sm = 1;
   const int resident = sms * per_sm;
-  int want = (int)env_size("TORUS_CTAS", nlocal > 1 ? 16 : 32);
+  int want = (int)env_size("TORUS_CTAS", nlocal > 1 ? 16 : sms);
   want = std::max(1, want);
   // every CTA of every rank that waits on another must be co-resident
   return std::min(want, std::max(1, resident / nlocal));
@@ -318,6 +319,7 @@ int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t*
   c->slab_size = own.size;
   c->own_slabs.push_back(own.ptr);
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
+  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", 960));
   int rc = TORUS_OK;
   std::vector<char*> bases(world, nullptr);
   if (cudaSetDevice(c->device) != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "cudaSetDevice");
@@ -371,6 +373,7 @@ int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_
   if (ws_bytes == 0) ws_bytes = env_size("TORUS_WS_BYTES", kDefaultSlab);
   c->slab_size = (ws_bytes + 65535) & ~(size_t)65535;
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
+  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", 960));
   if (ctas > 0) setenv("TORUS_CTAS", std::to_string(ctas).c_str(), 1);
   c->G = pick_ctas(device, c->nlocal);
   c->layout = make_layout(c->slab_size, c->G);
@@ -498,6 +501,7 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   a.inv_n = 1.0f / (float)(c->X * c->Y);
   a.aligned = aligned ? 1 : 0;
   a.timeout_ns = c->timeout_ns;
+  a.tile_vecs = c->tile_vecs;
   const unsigned long long Lc = R / c->X, Lcs = R / ((unsigned long long)c->X * c->Y);
   a.hin_off = c->layout.data_off;
   a.hin_stride = Lc * sw;
@@ -508,6 +512,7 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   for (unsigned long long r0 = 0; r0 < count; r0 += R) {
     a.n = std::min<unsigned long long>(R, count - r0);
     a.buf_off = r0;
+    tile_geometry(a.n, c->X, c->Y, a.q, a.G, a.tile_vecs, &a.T);
     cudaError_t e = launch_torus(a, dtype, wire, c->virt, stream);
     if (e != cudaSuccess) return cuda_fail(e, "torus kernel launch");
   }

@@ -67,7 +67,10 @@ struct LaunchArgs {
   int op;                        // 0 sum, 1 mean
   float inv_n;                   // f32(1/N)
   int aligned;                   // all user buffers 16-byte aligned -> vector path
+  int T;                         // pipeline tiles per CTA slice (same on every rank)
+  int tile_vecs;                 // vectors per tile piece
 };
+
 
 // Nested quantum-aligned partition (SPEC.md:67-75 when q == 1).  Host and
 // device use this one definition; the oracle has its own, independent one.
@@ -83,6 +86,21 @@ __host__ __device__ inline void qpart(unsigned long long n, int parts, int q, in
   if (b > n) b = n;
   *off = a;
   *len = b - a;
+}
+
+// Pipeline geometry for a round of n elements (host and device agree by construction):
+// CTA b owns slice b of every sub-chunk; each slice is cut into T tiles of tile_vecs
+// 16-byte vectors.  T is sized from the largest sub-chunk (qpart puts it first).
+__host__ __device__ inline void tile_geometry(unsigned long long n, int X, int Y, int q, int G,
+                                              int tile_vecs, int* T) {
+  unsigned long long o, l0, s0;
+  const int VE = q;  // the quantum is one 16-byte vector
+  qpart(n, X, q, 0, &o, &l0);
+  qpart(l0, Y, q, 0, &o, &s0);
+  const unsigned long long nv = (s0 + VE - 1) / VE;
+  const unsigned long long slice = (nv + G - 1) / G;
+  unsigned long long t = (slice + tile_vecs - 1) / tile_vecs;
+  *T = (int)(t < 1 ? 1 : t);
 }
 
 inline size_t flags_bytes_for(int G) {

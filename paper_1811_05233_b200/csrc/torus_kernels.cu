@@ -212,20 +212,63 @@ __device__ __forceinline__ void store_user(void* buf, unsigned long long e, int 
   }
 }
 
-// CTA b's slice of a range of `len` elements, in whole vectors of VE elements.
-__device__ __forceinline__ void cta_slice(unsigned long long len, int b, int G, int VE,
-                                          unsigned long long* va, unsigned long long* vz) {
-  const unsigned long long nv = (len + VE - 1) / VE;
-  *va = nv * (unsigned long long)b / (unsigned long long)G;
-  *vz = nv * (unsigned long long)(b + 1) / (unsigned long long)G;
+// ------------------------------------------------------------------------------------
+// pipeline geometry: CTA b owns slice b of every sub-chunk; tile t of that slice is the
+// vector range [p0, p1) below.  Host and every rank compute the same T (tile_geometry).
+// ------------------------------------------------------------------------------------
+struct Piece {
+  unsigned long long co, cl;  // chunk j: offset / length in the round (elements)
+  unsigned long long so;      // sub-chunk s: offset inside chunk j (elements)
+  unsigned long long p0, p1;  // vectors of the sub-chunk handled in this tile
+};
+
+__device__ __forceinline__ Piece make_piece(unsigned long long n, int X, int Y, int q, int G,
+                                            int b, int TV, int j, int s, int t) {
+  Piece p;
+  unsigned long long sl;
+  qpart(n, X, q, j, &p.co, &p.cl);
+  qpart(p.cl, Y, q, s, &p.so, &sl);
+  const unsigned long long nv = (sl + q - 1) / q;
+  const unsigned long long va = nv * (unsigned long long)b / (unsigned long long)G;
+  const unsigned long long vz = nv * (unsigned long long)(b + 1) / (unsigned long long)G;
+  const unsigned long long a0 = va + (unsigned long long)t * (unsigned long long)TV;
+  p.p0 = a0 < vz ? a0 : vz;
+  p.p1 = (a0 + TV) < vz ? (a0 + TV) : vz;
+  return p;
 }
 
-constexpr int kUnrollCopy = 4;   // 16-byte vectors in flight per thread (copy loops)
-constexpr int kUnrollFold = 2;   // vectors per thread per fold step (x X or Y operands)
+constexpr int kCtrlThreads = 32;                     // warp 0: flags, fences, signals
+constexpr int kWorkers = kThreads - kCtrlThreads;    // warps 1..15: data movement
+constexpr int kUnroll = 2;                           // vectors per worker per pass
+
+// Stages of the wavefront (iteration `it` runs A on tile it, B on it-1, ... E on it-4).
+enum Stage { kA = 0, kB = 1, kC = 2, kD = 3, kE = 4, kStages = 5 };
+// named barriers: READY_k = 1 + k (control -> workers), DONE_k = 6 + k (workers -> control)
+__device__ __forceinline__ void bar_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kThreads) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kThreads) : "memory");
+}
 
 // ------------------------------------------------------------------------------------
-// the fused torus kernel
+// the fused, tile-pipelined torus kernel
 // ------------------------------------------------------------------------------------
+//   stage A (tile t)   phase 1 push: cast my buffer's share of every row peer's chunk
+//                      and store it into that peer's h_in[c]                -> flag H
+//   stage B (t-1)      phase 1 fold: wait H; fold the X shares of my chunk in ring order;
+//                      Y > 1: push the rounded P1 into v_in[rho] of the column owner
+//                      of each sub-chunk (-> flag V); Y == 1: mean, round, write my chunk
+//                      slot and my buffer
+//   stage C (t-2)      phase 2 reduce-scatter: wait V; fold the Y rows' P1 in ring order,
+//                      mean, round once; write my chunk slot + my buffer      -> flag AG
+//   stage D (t-3)      phase 2 all-gather: wait AG; pull the column peers' reduced
+//                      sub-chunks into my buffer (+ my chunk slot when X > 1) -> flag R
+//   stage E (t-4)      phase 3 all-gather: wait R; pull the row peers' completed chunks
+//                      into my buffer (wire -> dtype cast fused)
+// Every wait is on flags peers raise one iteration earlier, so in steady state no stage
+// stalls on a cross-GPU round trip; the control warp polls the next stage's flags and
+// fences/raises the previous stage's flags while the workers move data.
 template <int DT, int W>
 __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) {
   using Acc = typename Wire<W>::Acc;
@@ -236,228 +279,295 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
   const int b = blockIdx.x - lr * a.G;
   const RankDev* __restrict__ R = a.ranks + lr;
   const int X = R->X, Y = R->Y, N = R->N, rho = R->rho, c = R->c, me = R->rank;
-  const int G = a.G, q = a.q;
+  const int G = a.G, q = a.q, T = a.T, TV = a.tile_vecs;
   const int tid = threadIdx.x;
   const unsigned long long n = a.n;
   const bool aligned = a.aligned != 0;
   void* const buf = a.buf[lr];
   char* const myws = R->ws[me];
+  char* const hin = myws + a.hin_off;
+  char* const vin = myws + a.vin_off;
+  char* const chunk = myws + a.chunk_off;
 
-  __shared__ uint32_t s_e;
+  __shared__ uint32_t s_seq;
   __shared__ int s_abort;
   if (tid == 0) {
-    s_e = R->epoch[b] + 1u;
+    s_seq = R->epoch[b];
     s_abort = 0;
   }
   __syncthreads();
-  const uint32_t e = s_e;
-  const unsigned long long deadline = gtimer() + a.timeout_ns;
+  const uint32_t seq = s_seq;
 
-  auto flag = [&](char* ws, int kind, int src) -> uint32_t* {
-    return reinterpret_cast<uint32_t*>(ws) + ((size_t)(kind * kMaxDim + src) * G + b);
-  };
-  // Wait until `cnt` sources' flags of `kind` reach epoch e; src(t) names the t-th.
-  auto wait_flags = [&](int kind, int cnt, auto src_of) -> bool {
-    if (tid < cnt) {
-      const uint32_t* f = flag(myws, kind, src_of(tid));
-      unsigned it = 0;
-      while ((int32_t)(ld_acquire_sys(f) - e) < 0) {
-        if ((++it & 255u) == 0 && gtimer() > deadline) {
-          atomicExch_system(R->err, kErrTimeout);
-          s_abort = 1;
-          break;
-        }
-      }
+  // which stages run in iteration `it`, on which tile
+  auto tile_of = [&](int k, int it) -> int {
+    const int t = it - k;
+    if (t < 0 || t >= T) return -1;
+    switch (k) {
+      case kA: return X > 1 ? t : -1;
+      case kB: return t;
+      case kC: return Y > 1 ? t : -1;
+      case kD: return t;
+      default: return X > 1 ? t : -1;
     }
-    __syncthreads();
-    return s_abort == 0;
   };
-  // Publish epoch e in `cnt` destination ranks' flags of `kind` under my source index.
-  auto signal = [&](int kind, int cnt, int my_src, auto dst_of) {
-    __syncthreads();  // every thread's data stores precede the release (cumulativity)
-    if (tid < cnt) st_release_sys(flag(R->ws[dst_of(tid)], kind, my_src), e);
-  };
+  const bool has_out[kStages] = {true, Y > 1, true, X > 1, false};
+  const int iters = T + 4;
 
-  // ---------------- phase 1a: horizontal reduce-scatter, push shares ----------------
-  if (X > 1) {
-    for (int jj = 1; jj < X; ++jj) {
-      const int j = (c + jj) % X;  // staggered so the X ranks of a row hit distinct peers
-      char* const dst = R->ws[rho * X + j] + a.hin_off + (size_t)c * a.hin_stride;
-      unsigned long long co, cl;
-      qpart(n, X, q, j, &co, &cl);
-      for (int s = 0; s < Y; ++s) {
-        unsigned long long so, sl, va, vz;
-        qpart(cl, Y, q, s, &so, &sl);
-        cta_slice(sl, b, G, VE, &va, &vz);
-        for (unsigned long long v0 = va + tid; v0 < vz; v0 += kUnrollCopy * kThreads) {
-          uint4 r[kUnrollCopy];
-#pragma unroll
-          for (int u = 0; u < kUnrollCopy; ++u) {
-            const unsigned long long v = v0 + (unsigned long long)u * kThreads;
-            if (v < vz) {
-              const unsigned long long el = so + v * VE;
-              const int nrem = (int)min((unsigned long long)VE, cl - el);
-              r[u] = load_user<DT, W>(buf, a.buf_off + co + el, nrem, aligned);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < kUnrollCopy; ++u) {
-            const unsigned long long v = v0 + (unsigned long long)u * kThreads;
-            if (v < vz) st_ws(dst + (so + v * VE) * SW, r[u]);
+  if (tid < kCtrlThreads) {
+    // =============================== control warp ===============================
+    const int lane = tid;
+    const unsigned long long deadline = gtimer() + a.timeout_ns;
+    auto flag = [&](char* ws, int kind, int src) -> uint32_t* {
+      return reinterpret_cast<uint32_t*>(ws) + ((size_t)(kind * kMaxDim + src) * G + b);
+    };
+    // poll: lane l < cnt waits for flag (kind, src_of(l)) >= value
+    auto poll = [&](int kind, int cnt, auto src_of, uint32_t value) -> bool {
+      bool ok = true;
+      if (lane < cnt) {
+        const uint32_t* f = flag(myws, kind, src_of(lane));
+        unsigned it = 0;
+        while ((int32_t)(ld_acquire_sys(f) - value) < 0) {
+          if ((++it & 255u) == 0 && gtimer() > deadline) {
+            ok = false;
+            break;
           }
         }
       }
+      return __all_sync(0xffffffffu, ok);
+    };
+    auto raise = [&](int kind, int cnt, int my_src, auto dst_of, uint32_t value) {
+      if (lane < cnt) st_release_sys(flag(R->ws[dst_of(lane)], kind, my_src), value);
+    };
+    auto signal_stage = [&](int k, int t) {
+      const uint32_t v = seq + (uint32_t)t + 1u;
+      switch (k) {
+        case kA: raise(kFlagH, X - 1, c, [&](int l) { return rho * X + (c + 1 + l) % X; }, v); break;
+        case kB: raise(kFlagV, Y - 1, rho, [&](int l) { return ((rho + 1 + l) % Y) * X + c; }, v); break;
+        case kC: raise(kFlagAG, Y - 1, rho, [&](int l) { return ((rho + 1 + l) % Y) * X + c; }, v); break;
+        case kD: raise(kFlagR, X - 1, c, [&](int l) { return rho * X + (c + 1 + l) % X; }, v); break;
+        default: break;
+      }
+    };
+    auto wait_stage = [&](int k, int t) -> bool {
+      const uint32_t v = seq + (uint32_t)t + 1u;
+      switch (k) {
+        case kB: return X > 1 ? poll(kFlagH, X - 1, [&](int l) { return (c + 1 + l) % X; }, v) : true;
+        case kC: return poll(kFlagV, Y - 1, [&](int l) { return (rho + 1 + l) % Y; }, v);
+        case kD: return Y > 1 ? poll(kFlagAG, Y - 1, [&](int l) { return (rho + 1 + l) % Y; }, v) : true;
+        case kE: return poll(kFlagR, X - 1, [&](int l) { return (c + 1 + l) % X; }, v);
+        default: return true;
+      }
+    };
+    int pend_k = -1, pend_t = -1;
+    for (int it = 0; it < iters; ++it) {
+      for (int k = 0; k < kStages; ++k) {
+        const int t = tile_of(k, it);
+        if (t < 0) continue;
+        const bool ok = wait_stage(k, t);       // inputs of stage k (peers, iteration it-1)
+        if (pend_k >= 0) bar_sync(6 + pend_k);  // workers finished the pending stage
+        if (!ok) {
+          if (lane == 0) {
+            atomicExch_system(R->err, kErrTimeout);
+            s_abort = 1;
+          }
+          __syncwarp();
+          bar_arrive(1 + k);
+          return;
+        }
+        bar_arrive(1 + k);                      // release the workers into stage k
+        if (pend_k >= 0) signal_stage(pend_k, pend_t);  // fence + flags, overlapped
+        pend_k = has_out[k] ? k : -1;
+        pend_t = t;
+        if (!has_out[k]) pend_k = -1;
+      }
     }
-    signal(kFlagH, X - 1, c, [&](int t) { return rho * X + (c + 1 + t) % X; });
-    if (!wait_flags(kFlagH, X - 1, [&](int t) { return (c + 1 + t) % X; })) return;
-  }
-
-  // ---------------- phase 1b: fold my chunk, push to the column owners ----------------
-  {
-    unsigned long long co, cl;
-    qpart(n, X, q, c, &co, &cl);
-    for (int s = 0; s < Y; ++s) {
-      unsigned long long so, sl, va, vz;
-      qpart(cl, Y, q, s, &so, &sl);
-      cta_slice(sl, b, G, VE, &va, &vz);
-      // Y > 1: into v_in[rho] of rank (s, c), indexed within the sub-chunk;
-      // Y == 1: this is the last reduce phase -> my own chunk slot, indexed within chunk.
-      char* const dst = (Y > 1) ? R->ws[s * X + c] + a.vin_off + (size_t)rho * a.vin_stride
-                                : myws + a.chunk_off + so * SW;
-      for (unsigned long long v0 = va + tid; v0 < vz; v0 += kUnrollFold * kThreads) {
-        Acc acc[kUnrollFold][VE];
+    if (pend_k >= 0) {
+      bar_sync(6 + pend_k);
+      signal_stage(pend_k, pend_t);
+    }
+  } else {
+    // =============================== worker warps ===============================
+    const int w = tid - kCtrlThreads;
+    for (int it = 0; it < iters; ++it) {
+      for (int k = 0; k < kStages; ++k) {
+        const int t = tile_of(k, it);
+        if (t < 0) continue;
+        bar_sync(1 + k);
+        if (*(volatile int*)&s_abort) return;
+        if (k == kA) {
+          // ---- phase 1 push ----
+          for (int jj = 1; jj < X; ++jj) {
+            const int j = (c + jj) % X;
+            char* const dst = R->ws[rho * X + j] + a.hin_off + (size_t)c * a.hin_stride;
+            for (int s = 0; s < Y; ++s) {
+              const Piece p = make_piece(n, X, Y, q, G, b, TV, j, s, t);
+              for (unsigned long long v0 = p.p0 + w; v0 < p.p1; v0 += kUnroll * kWorkers) {
+                uint4 r[kUnroll];
 #pragma unroll
-        for (int u = 0; u < kUnrollFold; ++u)
+                for (int u = 0; u < kUnroll; ++u) {
+                  const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
+                  if (v < p.p1) {
+                    const unsigned long long el = p.so + v * VE;
+                    const int nrem = (int)min((unsigned long long)VE, p.cl - el);
+                    r[u] = load_user<DT, W>(buf, a.buf_off + p.co + el, nrem, aligned);
+                  }
+                }
 #pragma unroll
-          for (int i = 0; i < VE; ++i) acc[u][i] = 0;
-        for (int k = 1; k <= X; ++k) {  // ring order: columns c+1, c+2, ..., c
-          const int j = (c + k) % X;
-          uint4 w[kUnrollFold];
-#pragma unroll
-          for (int u = 0; u < kUnrollFold; ++u) {
-            const unsigned long long v = v0 + (unsigned long long)u * kThreads;
-            if (v < vz) {
-              const unsigned long long el = so + v * VE;
-              if (j == c) {
-                const int nrem = (int)min((unsigned long long)VE, cl - el);
-                w[u] = load_user<DT, W>(buf, a.buf_off + co + el, nrem, aligned);
-              } else {
-                w[u] = ld_ws(myws + a.hin_off + (size_t)j * a.hin_stride + el * SW);
+                for (int u = 0; u < kUnroll; ++u) {
+                  const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
+                  if (v < p.p1) st_ws(dst + (p.so + v * VE) * SW, r[u]);
+                }
               }
             }
           }
+        } else if (k == kB) {
+          // ---- phase 1 fold: columns c+1, ..., c ----
+          for (int s = 0; s < Y; ++s) {
+            const Piece p = make_piece(n, X, Y, q, G, b, TV, c, s, t);
+            char* const dst = R->ws[s * X + c] + a.vin_off + (size_t)rho * a.vin_stride;
+            for (unsigned long long v0 = p.p0 + w; v0 < p.p1; v0 += kUnroll * kWorkers) {
+              Acc acc[kUnroll][VE];
+              for (int kk = 1; kk <= X; ++kk) {
+                const int j = (c + kk) % X;
+                uint4 r[kUnroll];
 #pragma unroll
-          for (int u = 0; u < kUnrollFold; ++u) {
-            Acc t[VE];
-            unpack<W>(w[u], t);
-            if (k == 1) {
+                for (int u = 0; u < kUnroll; ++u) {
+                  const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
+                  if (v < p.p1) {
+                    const unsigned long long el = p.so + v * VE;
+                    if (j == c) {
+                      const int nrem = (int)min((unsigned long long)VE, p.cl - el);
+                      r[u] = load_user<DT, W>(buf, a.buf_off + p.co + el, nrem, aligned);
+                    } else {
+                      r[u] = ld_ws(hin + (size_t)j * a.hin_stride + el * SW);
+                    }
+                  } else {
+                    r[u] = make_uint4(0, 0, 0, 0);
+                  }
+                }
 #pragma unroll
-              for (int i = 0; i < VE; ++i) acc[u][i] = t[i];
-            } else {
-              acc_add<W>(acc[u], t);
+                for (int u = 0; u < kUnroll; ++u) {
+                  Acc tmp[VE];
+                  unpack<W>(r[u], tmp);
+                  if (kk == 1) {
+#pragma unroll
+                    for (int i = 0; i < VE; ++i) acc[u][i] = tmp[i];
+                  } else {
+                    acc_add<W>(acc[u], tmp);
+                  }
+                }
+              }
+#pragma unroll
+              for (int u = 0; u < kUnroll; ++u) {
+                const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
+                if (v >= p.p1) continue;
+                const unsigned long long el = p.so + v * VE;
+                if (Y > 1) {
+                  st_ws(dst + v * VE * SW, pack<W>(acc[u]));
+                } else {  // last reduce phase: mean, round once, final
+                  if (a.op == 1) acc_mean<W>(acc[u], a.inv_n, N);
+                  const uint4 out = pack<W>(acc[u]);
+                  if (X > 1) st_ws(chunk + el * SW, out);
+                  const int nrem = (int)min((unsigned long long)VE, p.cl - el);
+                  store_user<DT, W>(buf, a.buf_off + p.co + el, nrem, out, aligned);
+                }
+              }
+            }
+          }
+        } else if (k == kC) {
+          // ---- phase 2 reduce-scatter: rows rho+1, ..., rho, mean, round ----
+          const Piece p = make_piece(n, X, Y, q, G, b, TV, c, rho, t);
+          for (unsigned long long v0 = p.p0 + w; v0 < p.p1; v0 += kUnroll * kWorkers) {
+            Acc acc[kUnroll][VE];
+            for (int kk = 1; kk <= Y; ++kk) {
+              const int i = (rho + kk) % Y;
+              uint4 r[kUnroll];
+#pragma unroll
+              for (int u = 0; u < kUnroll; ++u) {
+                const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
+                r[u] = (v < p.p1) ? ld_ws(vin + (size_t)i * a.vin_stride + v * VE * SW)
+                                  : make_uint4(0, 0, 0, 0);
+              }
+#pragma unroll
+              for (int u = 0; u < kUnroll; ++u) {
+                Acc tmp[VE];
+                unpack<W>(r[u], tmp);
+                if (kk == 1) {
+#pragma unroll
+                  for (int i2 = 0; i2 < VE; ++i2) acc[u][i2] = tmp[i2];
+                } else {
+                  acc_add<W>(acc[u], tmp);
+                }
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+              const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
+              if (v >= p.p1) continue;
+              if (a.op == 1) acc_mean<W>(acc[u], a.inv_n, N);
+              const uint4 out = pack<W>(acc[u]);
+              const unsigned long long el = p.so + v * VE;
+              st_ws(chunk + el * SW, out);
+              const int nrem = (int)min((unsigned long long)VE, p.cl - el);
+              store_user<DT, W>(buf, a.buf_off + p.co + el, nrem, out, aligned);
+            }
+          }
+        } else if (k == kD) {
+          // ---- phase 2 all-gather: pull the column peers' reduced sub-chunks ----
+          for (int ii = 1; ii < Y; ++ii) {
+            const int i = (rho + ii) % Y;
+            const char* const src = R->ws[i * X + c] + a.chunk_off;
+            const Piece p = make_piece(n, X, Y, q, G, b, TV, c, i, t);
+            for (unsigned long long v0 = p.p0 + w; v0 < p.p1; v0 += kUnroll * kWorkers) {
+              uint4 r[kUnroll];
+#pragma unroll
+              for (int u = 0; u < kUnroll; ++u) {
+                const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
+                if (v < p.p1) r[u] = ld_ws(src + (p.so + v * VE) * SW);
+              }
+#pragma unroll
+              for (int u = 0; u < kUnroll; ++u) {
+                const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
+                if (v >= p.p1) continue;
+                const unsigned long long el = p.so + v * VE;
+                if (X > 1) st_ws(chunk + el * SW, r[u]);
+                const int nrem = (int)min((unsigned long long)VE, p.cl - el);
+                store_user<DT, W>(buf, a.buf_off + p.co + el, nrem, r[u], aligned);
+              }
+            }
+          }
+        } else {
+          // ---- phase 3 all-gather: pull the row peers' completed chunks ----
+          for (int jj = 1; jj < X; ++jj) {
+            const int j = (c + jj) % X;
+            const char* const src = R->ws[rho * X + j] + a.chunk_off;
+            for (int s = 0; s < Y; ++s) {
+              const Piece p = make_piece(n, X, Y, q, G, b, TV, j, s, t);
+              for (unsigned long long v0 = p.p0 + w; v0 < p.p1; v0 += kUnroll * kWorkers) {
+                uint4 r[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                  const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
+                  if (v < p.p1) r[u] = ld_ws(src + (p.so + v * VE) * SW);
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                  const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
+                  if (v >= p.p1) continue;
+                  const unsigned long long el = p.so + v * VE;
+                  const int nrem = (int)min((unsigned long long)VE, p.cl - el);
+                  store_user<DT, W>(buf, a.buf_off + p.co + el, nrem, r[u], aligned);
+                }
+              }
             }
           }
         }
-#pragma unroll
-        for (int u = 0; u < kUnrollFold; ++u) {
-          const unsigned long long v = v0 + (unsigned long long)u * kThreads;
-          if (v < vz) {
-            if (Y == 1 && a.op == 1) acc_mean<W>(acc[u], a.inv_n, N);
-            st_ws(dst + v * VE * SW, pack<W>(acc[u]));
-          }
-        }
-      }
-    }
-  }
-
-  // ---------------- phase 2: vertical all-reduce of my sub-chunk ----------------------
-  if (Y > 1) {
-    signal(kFlagV, Y - 1, rho, [&](int t) { return ((rho + 1 + t) % Y) * X + c; });
-    if (!wait_flags(kFlagV, Y - 1, [&](int t) { return (rho + 1 + t) % Y; })) return;
-    unsigned long long co, cl, so, sl, va, vz;
-    qpart(n, X, q, c, &co, &cl);
-    qpart(cl, Y, q, rho, &so, &sl);
-    cta_slice(sl, b, G, VE, &va, &vz);
-    for (unsigned long long v0 = va + tid; v0 < vz; v0 += kUnrollFold * kThreads) {
-      Acc acc[kUnrollFold][VE];
-#pragma unroll
-      for (int u = 0; u < kUnrollFold; ++u)
-#pragma unroll
-        for (int i = 0; i < VE; ++i) acc[u][i] = 0;
-      for (int k = 1; k <= Y; ++k) {  // rows rho+1, ..., rho
-        const int i = (rho + k) % Y;
-        uint4 w[kUnrollFold];
-#pragma unroll
-        for (int u = 0; u < kUnrollFold; ++u) {
-          const unsigned long long v = v0 + (unsigned long long)u * kThreads;
-          if (v < vz) w[u] = ld_ws(myws + a.vin_off + (size_t)i * a.vin_stride + v * VE * SW);
-        }
-#pragma unroll
-        for (int u = 0; u < kUnrollFold; ++u) {
-          Acc t[VE];
-          unpack<W>(w[u], t);
-          if (k == 1) {
-#pragma unroll
-            for (int ii = 0; ii < VE; ++ii) acc[u][ii] = t[ii];
-          } else {
-            acc_add<W>(acc[u], t);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kUnrollFold; ++u) {
-        const unsigned long long v = v0 + (unsigned long long)u * kThreads;
-        if (v < vz) {
-          if (a.op == 1) acc_mean<W>(acc[u], a.inv_n, N);
-          const uint4 out = pack<W>(acc[u]);
-          const size_t off = a.chunk_off + (so + v * VE) * SW;
-          st_ws(myws + off, out);
-          for (int ii = 1; ii < Y; ++ii)  // vertical all-gather, pushed (fused)
-            st_ws(R->ws[((rho + ii) % Y) * X + c] + off, out);
-        }
-      }
-    }
-    signal(kFlagAG, Y - 1, rho, [&](int t) { return ((rho + 1 + t) % Y) * X + c; });
-    if (!wait_flags(kFlagAG, Y - 1, [&](int t) { return (rho + 1 + t) % Y; })) return;
-  }
-
-  // ---------------- phase 3: horizontal all-gather, pull + cast back -----------------
-  if (X > 1) {
-    signal(kFlagR, X - 1, c, [&](int t) { return rho * X + (c + 1 + t) % X; });
-    if (!wait_flags(kFlagR, X - 1, [&](int t) { return (c + 1 + t) % X; })) return;
-  } else {
-    __syncthreads();
-  }
-  for (int jj = 0; jj < X; ++jj) {
-    const int j = (c + jj) % X;  // own chunk first (local), then the row peers'
-    const char* const src = R->ws[rho * X + j] + a.chunk_off;
-    unsigned long long co, cl;
-    qpart(n, X, q, j, &co, &cl);
-    for (int s = 0; s < Y; ++s) {
-      unsigned long long so, sl, va, vz;
-      qpart(cl, Y, q, s, &so, &sl);
-      cta_slice(sl, b, G, VE, &va, &vz);
-      for (unsigned long long v0 = va + tid; v0 < vz; v0 += kUnrollCopy * kThreads) {
-        uint4 r[kUnrollCopy];
-#pragma unroll
-        for (int u = 0; u < kUnrollCopy; ++u) {
-          const unsigned long long v = v0 + (unsigned long long)u * kThreads;
-          if (v < vz) r[u] = ld_ws(src + (so + v * VE) * SW);
-        }
-#pragma unroll
-        for (int u = 0; u < kUnrollCopy; ++u) {
-          const unsigned long long v = v0 + (unsigned long long)u * kThreads;
-          if (v < vz) {
-            const unsigned long long el = so + v * VE;
-            const int nrem = (int)min((unsigned long long)VE, cl - el);
-            store_user<DT, W>(buf, a.buf_off + co + el, nrem, r[u], aligned);
-          }
-        }
+        if (has_out[k]) bar_arrive(6 + k);
       }
     }
   }
   __syncthreads();
-  if (tid == 0) R->epoch[b] = e;
+  if (tid == 0 && !s_abort) R->epoch[b] = seq + (uint32_t)T;
 }
 
 // N = 1: buf = from_wire(to_wire(buf)); the mean scale is x * 1.0 (identity).
