@@ -158,6 +158,15 @@ TORUS_API int torus_pick_grid(int world, const int* p2p, int* X, int* Y);
 TORUS_API int torus_partition(unsigned long long n, int parts, int q, unsigned long long* off,
                     unsigned long long* len);
 
+/* Calibration probes (not part of the all-reduce; SURVEY.md 8(d) "Calibration"), enqueued
+ * on `stream` with `ctas` CTAs (0 = the comm's count).  mode 0: push `bytes` split over
+ * the N-1 peers' slabs; 1: pull the same; 2: flag ping-pong between ranks 0 and 1,
+ * `iters` round trips, elapsed ns written to *ns_out (host; the call then synchronizes);
+ * 3: local slab-to-slab copy of `bytes`.  Overwrites the data region of the slabs: never
+ * run concurrently with an all-reduce on the same comm. */
+TORUS_API int torus_probe(torus_comm_t comm, int mode, size_t bytes, int iters, int ctas,
+                          unsigned long long* ns_out, torus_stream_t stream);
+
 /* Static string for a result code. */
 TORUS_API const char* torus_strerror(int code);
 /* Thread-local text of the last error raised in this thread (CUDA message included). */

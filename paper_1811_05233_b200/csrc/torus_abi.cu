@@ -443,6 +443,24 @@ int torus_comm_rank(torus_comm_t c, int* rank, int* world) {
 
 int torus_comm_ctas(torus_comm_t c) { return c ? c->G : -1; }
 
+int torus_probe(torus_comm_t c, int mode, size_t bytes, int iters, int ctas, unsigned long long* ns_out,
+                torus_stream_t stream) {
+  if (!c || c->virt || mode < 0 || mode > 3) return fail(TORUS_ERR_INVALID_ARG, "probe args");
+  const size_t room = c->slab_size - c->layout.data_off;
+  if (mode != 2 && (bytes == 0 || (bytes / 16) * 16 * (size_t)(c->world + 1) > room))
+    return fail(TORUS_ERR_INVALID_ARG, "probe bytes %zu exceed the slab", bytes);
+  if (mode == 2 && c->world < 2) return fail(TORUS_ERR_INVALID_ARG, "ping-pong needs 2 ranks");
+  unsigned long long* d_out = nullptr;
+  if (ns_out) CU(cudaMalloc(&d_out, sizeof(unsigned long long)));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_probe(c->d_ranks, c->layout.data_off, bytes, mode, iters,
+                               ctas > 0 ? ctas : c->G, d_out, s);
+  if (e == cudaSuccess && ns_out) e = cudaMemcpyAsync(ns_out, d_out, 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && ns_out) e = cudaStreamSynchronize(s);
+  if (d_out) cudaFree(d_out);
+  return e == cudaSuccess ? TORUS_OK : cuda_fail(e, "probe");
+}
+
 size_t torus_comm_round_elems(torus_comm_t c, torus_dtype_t wire) {
   if (!c || !valid_dtype(wire)) return 0;
   return (size_t)round_elems(c, wire);

@@ -320,14 +320,16 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
     auto flag = [&](char* ws, int kind, int src) -> uint32_t* {
       return reinterpret_cast<uint32_t*>(ws) + ((size_t)(kind * kMaxDim + src) * G + b);
     };
-    // poll: lane l < cnt waits for flag (kind, src_of(l)) >= value
+    // poll: lane l < cnt waits for flag (kind, src_of(l)) >= value; spin == false probes
+    // once (returns whether all were already there).
+    bool spin = true;
     auto poll = [&](int kind, int cnt, auto src_of, uint32_t value) -> bool {
       bool ok = true;
       if (lane < cnt) {
         const uint32_t* f = flag(myws, kind, src_of(lane));
         unsigned it = 0;
         while ((int32_t)(ld_acquire_sys(f) - value) < 0) {
-          if ((++it & 255u) == 0 && gtimer() > deadline) {
+          if (!spin || ((++it & 255u) == 0 && gtimer() > deadline)) {
             ok = false;
             break;
           }
@@ -363,7 +365,21 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
       for (int k = 0; k < kStages; ++k) {
         const int t = tile_of(k, it);
         if (t < 0) continue;
-        const bool ok = wait_stage(k, t);       // inputs of stage k (peers, iteration it-1)
+        // Inputs of stage k were raised by peers in their iteration it-1.  Probe first; if
+        // they are not all there yet, publish my own pending outputs BEFORE blocking (a
+        // peer may be waiting for them: no circular wait), else overlap the publish with
+        // the workers' stage k.
+        spin = false;
+        bool ok = wait_stage(k, t);
+        spin = true;
+        if (!ok) {
+          if (pend_k >= 0) {
+            bar_sync(6 + pend_k);
+            signal_stage(pend_k, pend_t);
+            pend_k = -1;
+          }
+          ok = wait_stage(k, t);
+        }
         if (pend_k >= 0) bar_sync(6 + pend_k);  // workers finished the pending stage
         if (!ok) {
           if (lane == 0) {
@@ -378,7 +394,6 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
         if (pend_k >= 0) signal_stage(pend_k, pend_t);  // fence + flags, overlapped
         pend_k = has_out[k] ? k : -1;
         pend_t = t;
-        if (!has_out[k]) pend_k = -1;
       }
     }
     if (pend_k >= 0) {
@@ -691,6 +706,90 @@ cudaError_t launch_barrier(const RankDev* ranks, int nlocal, unsigned long long 
                                        args, 0, stream);
   }
   barrier_kernel<<<1, kMaxRanks, 0, stream>>>(ranks, bar_off, timeout_ns);
+  return cudaGetLastError();
+}
+
+}  // namespace torus
+
+// ------------------------------------------------------------------------------------
+// Calibration probes (SURVEY.md 8(d) "Calibration"; not on the all-reduce path):
+//   mode 0  push: each rank stores `bytes` split evenly over its N-1 peers' data regions
+//   mode 1  pull: each rank loads `bytes` split evenly from its N-1 peers' data regions
+//   mode 2  ping-pong: rank 0 and rank 1 bounce a flag `iters` times (alpha)
+//   mode 3  local copy: bytes from the slab's first half to its second half (HBM)
+// ------------------------------------------------------------------------------------
+namespace torus {
+namespace {
+
+__global__ void __launch_bounds__(512) probe_kernel(const RankDev* ranks, unsigned long long data_off,
+                                                    unsigned long long bytes, int mode, int iters,
+                                                    unsigned long long* out) {
+  const RankDev* R = ranks;
+  const int N = R->N, me = R->rank, tid = threadIdx.x, G = gridDim.x, b = blockIdx.x;
+  if (mode == 2) {
+    if (b != 0 || tid != 0 || me > 1 || N < 2) return;
+    uint32_t* mine = reinterpret_cast<uint32_t*>(R->ws[me] + data_off);
+    uint32_t* theirs = reinterpret_cast<uint32_t*>(R->ws[1 - me] + data_off);
+    const uint32_t base = ld_acquire_sys(mine);
+    const unsigned long long t0 = gtimer();
+    for (int i = 1; i <= iters; ++i) {
+      if (me == 0) {
+        st_release_sys(theirs, base + i);
+        while ((int32_t)(ld_acquire_sys(mine) - (base + i)) < 0) {
+        }
+      } else {
+        while ((int32_t)(ld_acquire_sys(mine) - (base + i)) < 0) {
+        }
+        st_release_sys(theirs, base + i);
+      }
+    }
+    if (out) out[0] = gtimer() - t0;
+    return;
+  }
+  const unsigned long long nvec = bytes / 16;
+  if (mode == 3) {
+    const uint4* src = reinterpret_cast<const uint4*>(R->ws[me] + data_off);
+    uint4* dst = reinterpret_cast<uint4*>(R->ws[me] + data_off + nvec * 16);
+    for (unsigned long long v = (unsigned long long)b * blockDim.x + tid; v < nvec;
+         v += (unsigned long long)G * blockDim.x)
+      st_ws(dst + v, ld_ws(src + v));
+    return;
+  }
+  const unsigned long long per = nvec / (N - 1);
+  for (int pp = 1; pp < N; ++pp) {
+    const int p = (me + pp) % N;
+    if (mode == 0) {
+      uint4* dst = reinterpret_cast<uint4*>(R->ws[p] + data_off) + (unsigned long long)me * per;
+      const uint4* src = reinterpret_cast<const uint4*>(R->ws[me] + data_off) + (unsigned long long)(N + pp) * per;
+      for (unsigned long long v = (unsigned long long)b * blockDim.x + tid; v < per;
+           v += (unsigned long long)G * blockDim.x)
+        st_ws(dst + v, ld_ws(src + v));
+    } else {
+      const uint4* src = reinterpret_cast<const uint4*>(R->ws[p] + data_off) + (unsigned long long)p * per;
+      uint4* dst = reinterpret_cast<uint4*>(R->ws[me] + data_off) + (unsigned long long)(N + pp) * per;
+      for (unsigned long long v0 = (unsigned long long)b * blockDim.x + tid; v0 < per;
+           v0 += 4ull * G * blockDim.x) {
+        uint4 r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const unsigned long long v = v0 + (unsigned long long)u * G * blockDim.x;
+          if (v < per) r[u] = ld_ws(src + v);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const unsigned long long v = v0 + (unsigned long long)u * G * blockDim.x;
+          if (v < per) st_ws(dst + v, r[u]);
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_probe(const RankDev* ranks, unsigned long long data_off, unsigned long long bytes,
+                         int mode, int iters, int ctas, unsigned long long* out, cudaStream_t stream) {
+  probe_kernel<<<mode == 2 ? 1 : ctas, 512, 0, stream>>>(ranks, data_off, bytes, mode, iters, out);
   return cudaGetLastError();
 }
 

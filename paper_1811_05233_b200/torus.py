@@ -71,6 +71,15 @@ class _CommBase:
         return _lib.load().torus_comm_launches(self._comm, count, _dtype_code(dtype),
                                                _dtype_code(wire or dtype))
 
+    def probe(self, mode: int, nbytes: int = 0, iters: int = 0, ctas: int = 0,
+              stream: torch.cuda.Stream | None = None) -> int:
+        """Calibration probe (torus_probe); returns ns for mode 2, else 0 (time it yourself)."""
+        ns = ctypes.c_ulonglong(0)
+        check(_lib.load().torus_probe(self._comm, mode, nbytes, iters, ctas,
+                                      ctypes.byref(ns) if mode == 2 else None,
+                                      _stream_ptr(stream)), "torus_probe")
+        return ns.value
+
     def async_error(self) -> int:
         return _lib.load().torus_comm_get_async_error(self._comm)
 
