@@ -453,7 +453,8 @@ int torus_probe(torus_comm_t c, int mode, size_t bytes, int iters, int ctas, uns
   unsigned long long* d_out = nullptr;
   if (ns_out) CU(cudaMalloc(&d_out, sizeof(unsigned long long)));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = launch_probe(c->d_ranks, c->layout.data_off, bytes, mode, iters,
+  const unsigned long long off = mode == 2 ? c->layout.bar_off + 4096 : c->layout.data_off;
+  cudaError_t e = launch_probe(c->d_ranks, off, bytes, mode, iters,
                                ctas > 0 ? ctas : c->G, d_out, s);
   if (e == cudaSuccess && ns_out) e = cudaMemcpyAsync(ns_out, d_out, 8, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && ns_out) e = cudaStreamSynchronize(s);

@@ -727,23 +727,24 @@ __global__ void __launch_bounds__(512) probe_kernel(const RankDev* ranks, unsign
   const RankDev* R = ranks;
   const int N = R->N, me = R->rank, tid = threadIdx.x, G = gridDim.x, b = blockIdx.x;
   if (mode == 2) {
+    // flag words live in the barrier area (bar region + 4 KiB), never touched by data
     if (b != 0 || tid != 0 || me > 1 || N < 2) return;
     uint32_t* mine = reinterpret_cast<uint32_t*>(R->ws[me] + data_off);
     uint32_t* theirs = reinterpret_cast<uint32_t*>(R->ws[1 - me] + data_off);
     const uint32_t base = ld_acquire_sys(mine);
     const unsigned long long t0 = gtimer();
-    for (int i = 1; i <= iters; ++i) {
-      if (me == 0) {
-        st_release_sys(theirs, base + i);
-        while ((int32_t)(ld_acquire_sys(mine) - (base + i)) < 0) {
-        }
-      } else {
-        while ((int32_t)(ld_acquire_sys(mine) - (base + i)) < 0) {
-        }
-        st_release_sys(theirs, base + i);
+    const unsigned long long deadline = t0 + 5000000000ull;
+    bool ok = true;
+    for (int i = 1; i <= iters && ok; ++i) {
+      if (me == 0) st_release_sys(theirs, base + i);
+      unsigned spin = 0;
+      while ((int32_t)(ld_acquire_sys(mine) - (base + i)) < 0) {
+        if ((++spin & 1023u) == 0 && gtimer() > deadline) { ok = false; break; }
       }
+      if (me == 1 && ok) st_release_sys(theirs, base + i);
     }
-    if (out) out[0] = gtimer() - t0;
+    if (!ok) atomicExch_system(R->err, kErrTimeout);
+    if (out) out[0] = ok ? gtimer() - t0 : 0;
     return;
   }
   const unsigned long long nvec = bytes / 16;

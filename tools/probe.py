@@ -39,15 +39,18 @@ def main():
             t = torch.tensor([e0.elapsed_time(e1) / 1e3 / it], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             gbs = nbytes / t.item() / 1e9
-            out.append({"probe": name, "ctas": ctas, "bytes": nbytes, "us": t.item() * 1e6,
-                        "GBps_per_rank": gbs * (2 if mode == 3 else 1), "n": world})
+            rec = {"probe": name, "ctas": ctas, "bytes": nbytes, "us": t.item() * 1e6,
+                   "GBps_per_rank": gbs * (2 if mode == 3 else 1), "n": world}
+            if rank == 0:
+                print(json.dumps(rec), flush=True)
             dist.barrier()
     if world >= 2:
         torch.cuda.synchronize()
         dist.barrier()
         ns = comm.probe(2, 0, iters=2000)
         if rank == 0:
-            out.append({"probe": "pingpong", "iters": 2000, "one_way_us": ns / 2000 / 2 / 1e3})
+            print(json.dumps({"probe": "pingpong", "iters": 2000, "one_way_us": ns / 2000 / 2 / 1e3,
+                              "async_error": comm.async_error()}), flush=True)
         torch.cuda.synchronize()
     dist.barrier()
     comm.destroy()
