@@ -48,6 +48,9 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -239,11 +242,14 @@ __device__ __forceinline__ Piece make_piece(unsigned long long n, int X, int Y, 
 
 constexpr int kCtrlThreads = 32;                     // warp 0: flags, fences, signals
 constexpr int kWorkers = kThreads - kCtrlThreads;    // warps 1..15: data movement
-constexpr int kUnroll = 2;                           // vectors per worker per pass
+constexpr int kUnroll = 4;                           // vectors per worker per pass (copies)
+constexpr int kUnrollFold = 2;                       // vectors per worker per pass (folds)
 
 // Stages of the wavefront (iteration `it` runs A on tile it, B on it-1, ... E on it-4).
 enum Stage { kA = 0, kB = 1, kC = 2, kD = 3, kE = 4, kStages = 5 };
-// named barriers: READY_k = 1 + k (control -> workers), DONE_k = 6 + k (workers -> control)
+// named barriers between the control warp and the workers (0 is __syncthreads)
+constexpr int kBarReady = 1;  // control -> workers: inputs of iteration it are visible
+constexpr int kBarDone = 2;   // workers -> control: iteration it's data is written
 __device__ __forceinline__ void bar_sync(int id) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kThreads) : "memory");
 }
@@ -298,117 +304,121 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
   __syncthreads();
   const uint32_t seq = s_seq;
 
-  // which stages run in iteration `it`, on which tile
-  auto tile_of = [&](int k, int it) -> int {
-    const int t = it - k;
-    if (t < 0 || t >= T) return -1;
-    switch (k) {
-      case kA: return X > 1 ? t : -1;
-      case kB: return t;
-      case kC: return Y > 1 ? t : -1;
-      case kD: return t;
-      default: return X > 1 ? t : -1;
-    }
-  };
-  const bool has_out[kStages] = {true, Y > 1, true, X > 1, false};
-  const int iters = T + 4;
+  // Active stages of this grid in pipeline order.  Stage p works on tile it - 2p in
+  // iteration it, so every flag it consumes was raised by its peers one full iteration
+  // earlier: the ~3 us cross-GPU flag latency hides behind an iteration of data movement.
+  int kinds[kStages];
+  int P = 0;
+  if (X > 1) kinds[P++] = kA;
+  kinds[P++] = kB;
+  if (Y > 1) {
+    kinds[P++] = kC;
+    kinds[P++] = kD;
+  }
+  if (X > 1) kinds[P++] = kE;
+  const int iters = T + 2 * (P - 1);
 
   if (tid < kCtrlThreads) {
     // =============================== control warp ===============================
     const int lane = tid;
     const unsigned long long deadline = gtimer() + a.timeout_ns;
-    auto flag = [&](char* ws, int kind, int src) -> uint32_t* {
+    auto flagp = [&](char* ws, int kind, int src) -> uint32_t* {
       return reinterpret_cast<uint32_t*>(ws) + ((size_t)(kind * kMaxDim + src) * G + b);
     };
-    // poll: lane l < cnt waits for flag (kind, src_of(l)) >= value; spin == false probes
-    // once (returns whether all were already there).
-    bool spin = true;
-    auto poll = [&](int kind, int cnt, auto src_of, uint32_t value) -> bool {
-      bool ok = true;
-      if (lane < cnt) {
-        const uint32_t* f = flag(myws, kind, src_of(lane));
-        unsigned it = 0;
-        while ((int32_t)(ld_acquire_sys(f) - value) < 0) {
-          if (!spin || ((++it & 255u) == 0 && gtimer() > deadline)) {
-            ok = false;
-            break;
+    // Visit the flags stage k at tile t consumes (in) or produces (!in).
+    auto for_flags = [&](int k, int t, bool in, auto visit) {
+      int kind = -1, cnt = 0;
+      bool row = true;
+      switch (k) {
+        case kA:
+          if (!in) { kind = kFlagH; cnt = X - 1; row = true; }
+          break;
+        case kB:
+          if (in) {
+            if (X > 1) { kind = kFlagH; cnt = X - 1; row = true; }
+          } else if (Y > 1) {
+            kind = kFlagV; cnt = Y - 1; row = false;
+          } else if (X > 1) {
+            kind = kFlagR; cnt = X - 1; row = true;  // Y == 1: B wrote the final chunk
           }
-        }
+          break;
+        case kC:
+          kind = in ? kFlagV : kFlagAG; cnt = Y - 1; row = false;
+          break;
+        case kD:
+          if (in) { kind = kFlagAG; cnt = Y - 1; row = false; }
+          else if (X > 1) { kind = kFlagR; cnt = X - 1; row = true; }
+          break;
+        default:
+          if (in) { kind = kFlagR; cnt = X - 1; row = true; }
+          break;
+      }
+      const uint32_t v = seq + (uint32_t)t + 1u;
+      for (int l = 0; l < cnt; ++l) {
+        const int other = row ? (c + 1 + l) % X : (rho + 1 + l) % Y;
+        const int peer = row ? rho * X + other : other * X + c;
+        visit(in ? flagp(myws, kind, other) : flagp(R->ws[peer], kind, row ? c : rho), v);
+      }
+    };
+    auto poll_iter = [&](int it) -> bool {
+      bool ok = true;
+      int e = 0;
+      for (int p = 0; p < P; ++p) {
+        const int t = it - 2 * p;
+        if (t < 0 || t >= T) continue;
+        for_flags(kinds[p], t, true, [&](uint32_t* f, uint32_t v) {
+          if ((e++ & 31) == lane && ok) {
+            unsigned spin = 0;
+            while ((int32_t)(ld_acquire_sys(f) - v) < 0) {
+              if ((++spin & 255u) == 0 && gtimer() > deadline) {
+                ok = false;
+                break;
+              }
+            }
+          }
+        });
       }
       return __all_sync(0xffffffffu, ok);
     };
-    auto raise = [&](int kind, int cnt, int my_src, auto dst_of, uint32_t value) {
-      if (lane < cnt) st_release_sys(flag(R->ws[dst_of(lane)], kind, my_src), value);
-    };
-    auto signal_stage = [&](int k, int t) {
-      const uint32_t v = seq + (uint32_t)t + 1u;
-      switch (k) {
-        case kA: raise(kFlagH, X - 1, c, [&](int l) { return rho * X + (c + 1 + l) % X; }, v); break;
-        case kB: raise(kFlagV, Y - 1, rho, [&](int l) { return ((rho + 1 + l) % Y) * X + c; }, v); break;
-        case kC: raise(kFlagAG, Y - 1, rho, [&](int l) { return ((rho + 1 + l) % Y) * X + c; }, v); break;
-        case kD: raise(kFlagR, X - 1, c, [&](int l) { return rho * X + (c + 1 + l) % X; }, v); break;
-        default: break;
+    // one system-scope fence for all the flags an iteration raises
+    auto raise_iter = [&](int it) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      int e = 0;
+      for (int p = 0; p < P; ++p) {
+        const int t = it - 2 * p;
+        if (t < 0 || t >= T) continue;
+        for_flags(kinds[p], t, false, [&](uint32_t* f, uint32_t v) {
+          if ((e++ & 31) == lane) st_relaxed_sys(f, v);
+        });
       }
     };
-    auto wait_stage = [&](int k, int t) -> bool {
-      const uint32_t v = seq + (uint32_t)t + 1u;
-      switch (k) {
-        case kB: return X > 1 ? poll(kFlagH, X - 1, [&](int l) { return (c + 1 + l) % X; }, v) : true;
-        case kC: return poll(kFlagV, Y - 1, [&](int l) { return (rho + 1 + l) % Y; }, v);
-        case kD: return Y > 1 ? poll(kFlagAG, Y - 1, [&](int l) { return (rho + 1 + l) % Y; }, v) : true;
-        case kE: return poll(kFlagR, X - 1, [&](int l) { return (c + 1 + l) % X; }, v);
-        default: return true;
-      }
-    };
-    int pend_k = -1, pend_t = -1;
     for (int it = 0; it < iters; ++it) {
-      for (int k = 0; k < kStages; ++k) {
-        const int t = tile_of(k, it);
-        if (t < 0) continue;
-        // Inputs of stage k were raised by peers in their iteration it-1.  Probe first; if
-        // they are not all there yet, publish my own pending outputs BEFORE blocking (a
-        // peer may be waiting for them: no circular wait), else overlap the publish with
-        // the workers' stage k.
-        spin = false;
-        bool ok = wait_stage(k, t);
-        spin = true;
-        if (!ok) {
-          if (pend_k >= 0) {
-            bar_sync(6 + pend_k);
-            signal_stage(pend_k, pend_t);
-            pend_k = -1;
-          }
-          ok = wait_stage(k, t);
+      const bool ok = poll_iter(it);      // inputs: raised by peers in iteration <= it-1
+      if (it > 0) bar_sync(kBarDone);     // workers finished iteration it-1
+      if (!ok) {
+        if (lane == 0) {
+          atomicExch_system(R->err, kErrTimeout);
+          s_abort = 1;
         }
-        if (pend_k >= 0) bar_sync(6 + pend_k);  // workers finished the pending stage
-        if (!ok) {
-          if (lane == 0) {
-            atomicExch_system(R->err, kErrTimeout);
-            s_abort = 1;
-          }
-          __syncwarp();
-          bar_arrive(1 + k);
-          return;
-        }
-        bar_arrive(1 + k);                      // release the workers into stage k
-        if (pend_k >= 0) signal_stage(pend_k, pend_t);  // fence + flags, overlapped
-        pend_k = has_out[k] ? k : -1;
-        pend_t = t;
+        __syncwarp();
+        bar_arrive(kBarReady);
+        return;
       }
+      bar_arrive(kBarReady);              // workers start iteration it ...
+      if (it > 0) raise_iter(it - 1);     // ... while the fence for it-1 drains
     }
-    if (pend_k >= 0) {
-      bar_sync(6 + pend_k);
-      signal_stage(pend_k, pend_t);
-    }
+    bar_sync(kBarDone);
+    raise_iter(iters - 1);
   } else {
     // =============================== worker warps ===============================
     const int w = tid - kCtrlThreads;
     for (int it = 0; it < iters; ++it) {
-      for (int k = 0; k < kStages; ++k) {
-        const int t = tile_of(k, it);
-        if (t < 0) continue;
-        bar_sync(1 + k);
-        if (*(volatile int*)&s_abort) return;
+      bar_sync(kBarReady);
+      if (*(volatile int*)&s_abort) return;
+      for (int p = 0; p < P; ++p) {
+        const int t = it - 2 * p;
+        if (t < 0 || t >= T) continue;
+        const int k = kinds[p];
         if (k == kA) {
           // ---- phase 1 push ----
           for (int jj = 1; jj < X; ++jj) {
@@ -440,13 +450,13 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
           for (int s = 0; s < Y; ++s) {
             const Piece p = make_piece(n, X, Y, q, G, b, TV, c, s, t);
             char* const dst = R->ws[s * X + c] + a.vin_off + (size_t)rho * a.vin_stride;
-            for (unsigned long long v0 = p.p0 + w; v0 < p.p1; v0 += kUnroll * kWorkers) {
-              Acc acc[kUnroll][VE];
+            for (unsigned long long v0 = p.p0 + w; v0 < p.p1; v0 += kUnrollFold * kWorkers) {
+              Acc acc[kUnrollFold][VE];
               for (int kk = 1; kk <= X; ++kk) {
                 const int j = (c + kk) % X;
-                uint4 r[kUnroll];
+                uint4 r[kUnrollFold];
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
+                for (int u = 0; u < kUnrollFold; ++u) {
                   const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
                   if (v < p.p1) {
                     const unsigned long long el = p.so + v * VE;
@@ -461,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
                   }
                 }
 #pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
+                for (int u = 0; u < kUnrollFold; ++u) {
                   Acc tmp[VE];
                   unpack<W>(r[u], tmp);
                   if (kk == 1) {
@@ -473,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
                 }
               }
 #pragma unroll
-              for (int u = 0; u < kUnroll; ++u) {
+              for (int u = 0; u < kUnrollFold; ++u) {
                 const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
                 if (v >= p.p1) continue;
                 const unsigned long long el = p.so + v * VE;
@@ -492,19 +502,19 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
         } else if (k == kC) {
           // ---- phase 2 reduce-scatter: rows rho+1, ..., rho, mean, round ----
           const Piece p = make_piece(n, X, Y, q, G, b, TV, c, rho, t);
-          for (unsigned long long v0 = p.p0 + w; v0 < p.p1; v0 += kUnroll * kWorkers) {
-            Acc acc[kUnroll][VE];
+          for (unsigned long long v0 = p.p0 + w; v0 < p.p1; v0 += kUnrollFold * kWorkers) {
+            Acc acc[kUnrollFold][VE];
             for (int kk = 1; kk <= Y; ++kk) {
               const int i = (rho + kk) % Y;
-              uint4 r[kUnroll];
+              uint4 r[kUnrollFold];
 #pragma unroll
-              for (int u = 0; u < kUnroll; ++u) {
+              for (int u = 0; u < kUnrollFold; ++u) {
                 const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
                 r[u] = (v < p.p1) ? ld_ws(vin + (size_t)i * a.vin_stride + v * VE * SW)
                                   : make_uint4(0, 0, 0, 0);
               }
 #pragma unroll
-              for (int u = 0; u < kUnroll; ++u) {
+              for (int u = 0; u < kUnrollFold; ++u) {
                 Acc tmp[VE];
                 unpack<W>(r[u], tmp);
                 if (kk == 1) {
@@ -516,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
               }
             }
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
+            for (int u = 0; u < kUnrollFold; ++u) {
               const unsigned long long v = v0 + (unsigned long long)u * kWorkers;
               if (v >= p.p1) continue;
               if (a.op == 1) acc_mean<W>(acc[u], a.inv_n, N);
@@ -577,8 +587,8 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
             }
           }
         }
-        if (has_out[k]) bar_arrive(6 + k);
       }
+      bar_arrive(kBarDone);
     }
   }
   __syncthreads();
