@@ -158,6 +158,13 @@ TORUS_API int torus_pick_grid(int world, const int* p2p, int* X, int* Y);
 TORUS_API int torus_partition(unsigned long long n, int parts, int q, unsigned long long* off,
                     unsigned long long* len);
 
+/* Device trace (tracing subsystem): with env TORUS_TRACE=1 at init, every launch records
+ * globaltimer stamps per CTA and pipeline iteration -- host array [ctas][64][8] u64
+ * (events: 0 poll start, 1 poll done, 2 DONE synced, 3 READY arrived, 4 flags raised,
+ * 5 worker READY passed, 6 worker data done).  Synchronizes the device.  UNSUPPORTED if
+ * tracing is off. */
+TORUS_API int torus_comm_trace(torus_comm_t comm, unsigned long long* host, size_t bytes);
+
 /* Calibration probes (not part of the all-reduce; SURVEY.md 8(d) "Calibration"), enqueued
  * on `stream` with `ctas` CTAs (0 = the comm's count).  mode 0: push `bytes` split over
  * the N-1 peers' slabs; 1: pull the same; 2: flag ping-pong between ranks 0 and 1,

@@ -89,6 +89,7 @@ struct torus_comm {
   int* h_err = nullptr;           // host-mapped async error word
   int* d_err = nullptr;
   bool poisoned = false;
+  unsigned long long* d_trace = nullptr;  // TORUS_TRACE=1: [G][kTraceIters][kTraceEvents]
 };
 
 namespace {
@@ -121,6 +122,11 @@ int alloc_comm_common(torus_comm* c) {
   *c->h_err = 0;
   CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_err), c->h_err, 0));
   CU(cudaMalloc(&c->d_ranks, sizeof(RankDev) * c->nlocal));
+  if (env_size("TORUS_TRACE", 0)) {
+    const size_t tb = (size_t)c->G * kTraceIters * kTraceEvents * sizeof(unsigned long long);
+    CU(cudaMalloc(&c->d_trace, tb));
+    CU(cudaMemset(c->d_trace, 0, tb));
+  }
   return TORUS_OK;
 }
 
@@ -163,6 +169,7 @@ void destroy_resources(torus_comm* c) {
   for (void* p : c->own_slabs) cudaFree(p);
   if (c->d_ranks) cudaFree(c->d_ranks);
   if (c->d_epochs) cudaFree(c->d_epochs);
+  if (c->d_trace) cudaFree(c->d_trace);
   if (c->h_err) cudaFreeHost(c->h_err);
   delete c;
 }
@@ -443,6 +450,15 @@ int torus_comm_rank(torus_comm_t c, int* rank, int* world) {
 
 int torus_comm_ctas(torus_comm_t c) { return c ? c->G : -1; }
 
+int torus_comm_trace(torus_comm_t c, unsigned long long* host, size_t bytes) {
+  if (!c || !host) return fail(TORUS_ERR_INVALID_ARG, "null argument");
+  if (!c->d_trace) return fail(TORUS_ERR_UNSUPPORTED, "tracing is off (set TORUS_TRACE=1 before init)");
+  const size_t tb = (size_t)c->G * kTraceIters * kTraceEvents * sizeof(unsigned long long);
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(host, c->d_trace, std::min(bytes, tb), cudaMemcpyDeviceToHost));
+  return TORUS_OK;
+}
+
 int torus_probe(torus_comm_t c, int mode, size_t bytes, int iters, int ctas, unsigned long long* ns_out,
                 torus_stream_t stream) {
   if (!c || c->virt || mode < 0 || mode > 3) return fail(TORUS_ERR_INVALID_ARG, "probe args");
@@ -521,6 +537,7 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   a.aligned = aligned ? 1 : 0;
   a.timeout_ns = c->timeout_ns;
   a.tile_vecs = c->tile_vecs;
+  a.trace = c->d_trace;
   const unsigned long long Lc = R / c->X, Lcs = R / ((unsigned long long)c->X * c->Y);
   a.hin_off = c->layout.data_off;
   a.hin_stride = Lc * sw;

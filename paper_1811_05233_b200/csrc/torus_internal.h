@@ -17,6 +17,8 @@ constexpr int kMaxLocal = 16;     // virtual ranks per launch (single-GPU emulat
 constexpr int kThreads = 512;     // threads per CTA of the torus kernel
 constexpr int kVecBytes = 16;     // 128-bit vectors (LDG/STG.E.128)
 constexpr int kFlagPhases = 4;    // H-RS, V-RS, V-AG, H-AG handshakes
+constexpr int kTraceIters = 64;   // trace: iterations recorded per CTA
+constexpr int kTraceEvents = 8;   // trace: events per iteration (see torus_kernels.cu)
 
 // Flag kinds (PAPER.md:70 phases; one u32 epoch per (kind, source, CTA)).
 enum FlagKind : int {
@@ -67,6 +69,7 @@ struct LaunchArgs {
   int op;                        // 0 sum, 1 mean
   float inv_n;                   // f32(1/N)
   int aligned;                   // all user buffers 16-byte aligned -> vector path
+  unsigned long long* trace;     // optional [G][kTraceIters][kTraceEvents] globaltimer stamps
   int T;                         // pipeline tiles per CTA slice (same on every rank)
   int tile_vecs;                 // vectors per tile piece
 };

@@ -247,6 +247,13 @@ constexpr int kUnrollFold = 2;                       // vectors per worker per p
 
 // Stages of the wavefront (iteration `it` runs A on tile it, B on it-1, ... E on it-4).
 enum Stage { kA = 0, kB = 1, kC = 2, kD = 3, kE = 4, kStages = 5 };
+// Trace events per iteration (TORUS_TRACE=1): control lane 0 stamps 0 poll start,
+// 1 poll done, 2 DONE(it-1) synced, 3 READY(it) arrived, 4 raise(it-1) done; worker
+// warp 1 lane 0 stamps 5 READY passed, 6 work done.
+__device__ __forceinline__ void stamp(unsigned long long* tr, int b, int it, int ev) {
+  if (tr && it < kTraceIters) tr[((size_t)b * kTraceIters + it) * kTraceEvents + ev] = gtimer();
+}
+
 // named barriers between the control warp and the workers (0 is __syncthreads)
 constexpr int kBarReady = 1;  // control -> workers: inputs of iteration it are visible
 constexpr int kBarDone = 2;   // workers -> control: iteration it's data is written
@@ -392,9 +399,13 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
         });
       }
     };
+    unsigned long long* const tr = (lane == 0 && lr == 0) ? a.trace : nullptr;
     for (int it = 0; it < iters; ++it) {
+      stamp(tr, b, it, 0);
       const bool ok = poll_iter(it);      // inputs: raised by peers in iteration <= it-1
+      stamp(tr, b, it, 1);
       if (it > 0) bar_sync(kBarDone);     // workers finished iteration it-1
+      stamp(tr, b, it, 2);
       if (!ok) {
         if (lane == 0) {
           atomicExch_system(R->err, kErrTimeout);
@@ -405,15 +416,19 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
         return;
       }
       bar_arrive(kBarReady);              // workers start iteration it ...
+      stamp(tr, b, it, 3);
       if (it > 0) raise_iter(it - 1);     // ... while the fence for it-1 drains
+      stamp(tr, b, it, 4);
     }
     bar_sync(kBarDone);
     raise_iter(iters - 1);
   } else {
     // =============================== worker warps ===============================
     const int w = tid - kCtrlThreads;
+    unsigned long long* const tr = (w == 0 && lr == 0) ? a.trace : nullptr;
     for (int it = 0; it < iters; ++it) {
       bar_sync(kBarReady);
+      stamp(tr, b, it, 5);
       if (*(volatile int*)&s_abort) return;
       for (int p = 0; p < P; ++p) {
         const int t = it - 2 * p;
@@ -588,6 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
           }
         }
       }
+      stamp(tr, b, it, 6);
       bar_arrive(kBarDone);
     }
   }

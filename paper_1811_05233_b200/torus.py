@@ -80,6 +80,15 @@ class _CommBase:
                                       _stream_ptr(stream)), "torus_probe")
         return ns.value
 
+    def trace(self):
+        """Device trace of the last launch (TORUS_TRACE=1): numpy [ctas, 64, 8] of ns."""
+        import numpy as np
+        out = np.zeros((self.ctas(), 64, 8), dtype=np.uint64)
+        check(_lib.load().torus_comm_trace(
+            self._comm, out.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), out.nbytes),
+            "torus_comm_trace")
+        return out
+
     def async_error(self) -> int:
         return _lib.load().torus_comm_get_async_error(self._comm)
 
