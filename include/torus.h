@@ -169,7 +169,8 @@ TORUS_API int torus_comm_trace(torus_comm_t comm, unsigned long long* host, size
  * on `stream` with `ctas` CTAs (0 = the comm's count).  mode 0: push `bytes` split over
  * the N-1 peers' slabs; 1: pull the same; 2: flag ping-pong between ranks 0 and 1,
  * `iters` round trips, elapsed ns written to *ns_out (host; the call then synchronizes);
- * 3: local slab-to-slab copy of `bytes`.  Overwrites the data region of the slabs: never
+ * 3: local slab-to-slab copy of `bytes`; 4 / 5: push / pull as 0 / 1 but with TMA bulk
+ * copies (cp.async.bulk, 16 KiB, 8-deep shared-memory ring, one thread per CTA).  Overwrites the data region of the slabs: never
  * run concurrently with an all-reduce on the same comm. */
 TORUS_API int torus_probe(torus_comm_t comm, int mode, size_t bytes, int iters, int ctas,
                           unsigned long long* ns_out, torus_stream_t stream);

@@ -61,6 +61,58 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ uint4 ld_ws(const void* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
 __device__ __forceinline__ void st_ws(void* p, uint4 v) { __stcg(reinterpret_cast<uint4*>(p), v); }
 
+
+// ------------------------------------------------------------------------------------
+// TMA bulk-copy primitives (cp.async.bulk, 1-D; sm_90+/sm_100a) and mbarriers
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+}
+// global (local or NVLink peer) -> shared, completion counted on `bar`
+__device__ __forceinline__ void tma_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// shared -> global (local or NVLink peer), tracked by bulk async-groups
+__device__ __forceinline__ void tma_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void tma_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tma_wait_all() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async;" ::: "memory");
+}
+
 // ------------------------------------------------------------------------------------
 // wire traits: a 16-byte vector holds VE wire elements; Acc is the accumulation type
 // (f32 for float wires, u32 two's-complement for i32)
@@ -812,10 +864,73 @@ __global__ void __launch_bounds__(512) probe_kernel(const RankDev* ranks, unsign
   }
 }
 
+
+// TMA probe (modes 4 push / 5 pull): one elected thread per CTA streams 16 KiB bulk
+// copies through a ring of kTmaStages shared-memory buffers.
+constexpr int kTmaChunk = 16384;
+constexpr int kTmaStages = 8;
+
+__global__ void __launch_bounds__(32) tma_probe_kernel(const RankDev* ranks, unsigned long long data_off,
+                                                      unsigned long long bytes, int mode) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTmaStages * kTmaChunk);
+  const RankDev* R = ranks;
+  const int N = R->N, me = R->rank, G = gridDim.x, b = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
+  fence_mbar_init();
+  const unsigned long long per = (bytes / (N - 1)) / kTmaChunk * kTmaChunk;
+  int issued = 0, done = 0;
+  for (int pp = 1; pp < N; ++pp) {
+    const int p = (me + pp) % N;
+    const char* src;
+    char* dst;
+    if (mode == 4) {  // push: my slab -> peer's slab
+      src = R->ws[me] + data_off + (unsigned long long)(N + pp) * per;
+      dst = R->ws[p] + data_off + (unsigned long long)me * per;
+    } else {          // pull: peer's slab -> my slab
+      src = R->ws[p] + data_off + (unsigned long long)p * per;
+      dst = R->ws[me] + data_off + (unsigned long long)(N + pp) * per;
+    }
+    const unsigned long long nchunks = per / kTmaChunk;
+    const unsigned long long c0 = nchunks * b / G, c1 = nchunks * (b + 1) / G;
+    // software pipeline: keep up to kTmaStages-1 loads ahead of the stores
+    unsigned long long next = c0;
+    for (; next < c1 && next - c0 < kTmaStages - 1; ++next, ++issued) {
+      const int s = issued % kTmaStages;
+      mbar_expect_tx(&bars[s], kTmaChunk);
+      tma_load(smem + s * kTmaChunk, src + next * kTmaChunk, kTmaChunk, &bars[s]);
+    }
+    for (unsigned long long ci = c0; ci < c1; ++ci, ++done) {
+      const int s = done % kTmaStages;
+      mbar_wait(&bars[s], (done / kTmaStages) & 1);
+      tma_store(dst + ci * kTmaChunk, smem + s * kTmaChunk, kTmaChunk);
+      tma_commit();
+      if (next < c1) {
+        tma_wait_read<1>();  // the buffer reloaded next was read by the store before this one
+        const int s2 = issued % kTmaStages;
+        mbar_expect_tx(&bars[s2], kTmaChunk);
+        tma_load(smem + s2 * kTmaChunk, src + next * kTmaChunk, kTmaChunk, &bars[s2]);
+        ++next;
+        ++issued;
+      }
+    }
+    tma_wait_read<0>();
+  }
+  tma_wait_all<0>();
+}
+
 }  // namespace
 
 cudaError_t launch_probe(const RankDev* ranks, unsigned long long data_off, unsigned long long bytes,
                          int mode, int iters, int ctas, unsigned long long* out, cudaStream_t stream) {
+  if (mode == 4 || mode == 5) {
+    const int smem = kTmaStages * kTmaChunk + kTmaStages * 8;
+    cudaError_t e = cudaFuncSetAttribute(tma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    tma_probe_kernel<<<ctas, 32, smem, stream>>>(ranks, data_off, bytes, mode);
+    return cudaGetLastError();
+  }
   probe_kernel<<<mode == 2 ? 1 : ctas, 512, 0, stream>>>(ranks, data_off, bytes, mode, iters, out);
   return cudaGetLastError();
 }

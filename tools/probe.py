@@ -23,8 +23,8 @@ def main():
     s = torch.cuda.current_stream()
     nbytes = 51_114_064 * 2 * (world - 1) // world // 16 * 16  # 2(N-1)/N * S
     out = []
-    for mode, name in ((0, "push"), (1, "pull"), (3, "local_copy")):
-        for ctas in (16, 32, 64, 96, 128, 148, 296):
+    for mode, name in ((0, "push"), (1, "pull"), (4, "tma_push"), (5, "tma_pull"), (3, "local_copy")):
+        for ctas in ((16, 32, 64, 148, 296) if mode < 4 else (16, 32, 64, 148)):
             for _ in range(3):
                 comm.probe(mode, nbytes, ctas=ctas)
             torch.cuda.synchronize()
