@@ -75,7 +75,8 @@ struct torus_comm {
   int rank = 0, world = 1, X = 1, Y = 1;
   int device = 0;
   int G = 0;
-  int tile_vecs = 960;      // 16-byte vectors per tile piece (env TORUS_TILE)
+  int tile_vecs = 512;      // 16-byte vectors per tile piece (env TORUS_TILE)
+  bool tma = true;          // TMA-staged kernel (env TORUS_KERNEL=ldg selects the LDG/STG one)
   int nlocal = 1;           // > 1: virtual ranks on one device
   bool virt = false;
   size_t slab_size = 0;
@@ -326,7 +327,8 @@ int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t*
   c->slab_size = own.size;
   c->own_slabs.push_back(own.ptr);
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
-  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", 960));
+  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", 512));
+  { const char* k = getenv("TORUS_KERNEL"); c->tma = !(k && strcmp(k, "ldg") == 0); }
   int rc = TORUS_OK;
   std::vector<char*> bases(world, nullptr);
   if (cudaSetDevice(c->device) != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "cudaSetDevice");
@@ -380,7 +382,8 @@ int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_
   if (ws_bytes == 0) ws_bytes = env_size("TORUS_WS_BYTES", kDefaultSlab);
   c->slab_size = (ws_bytes + 65535) & ~(size_t)65535;
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
-  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", 960));
+  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", 512));
+  { const char* k = getenv("TORUS_KERNEL"); c->tma = !(k && strcmp(k, "ldg") == 0); }
   if (ctas > 0) setenv("TORUS_CTAS", std::to_string(ctas).c_str(), 1);
   c->G = pick_ctas(device, c->nlocal);
   c->layout = make_layout(c->slab_size, c->G);
@@ -538,6 +541,17 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   a.timeout_ns = c->timeout_ns;
   a.tile_vecs = c->tile_vecs;
   a.trace = c->d_trace;
+  a.nbufs = 0;
+  if (c->tma) {
+    // ring buffers of one piece each; every fold job needs max(X,Y)+1 of them at once plus
+    // the storer's in-flight stores, so shrink the piece until enough fit
+    const int need = std::max(c->X, c->Y) + 1 + 4 + 4;
+    int tv = a.tile_vecs;
+    while (tv > 32 && (kTmaSmemMax - 1024) / (tv * 16 + 16) < need) tv /= 2;
+    a.tile_vecs = tv;
+    a.nbufs = std::min(48, (kTmaSmemMax - 1024) / (tv * 16 + 16));
+    if (a.nbufs < need) return fail(TORUS_ERR_UNSUPPORTED, "grid %dx%d too large for the TMA ring", c->X, c->Y);
+  }
   const unsigned long long Lc = R / c->X, Lcs = R / ((unsigned long long)c->X * c->Y);
   a.hin_off = c->layout.data_off;
   a.hin_stride = Lc * sw;

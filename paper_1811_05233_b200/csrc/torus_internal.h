@@ -72,7 +72,12 @@ struct LaunchArgs {
   unsigned long long* trace;     // optional [G][kTraceIters][kTraceEvents] globaltimer stamps
   int T;                         // pipeline tiles per CTA slice (same on every rank)
   int tile_vecs;                 // vectors per tile piece
+  int nbufs;                     // > 0: TMA-staged kernel with this many ring buffers
 };
+
+// TMA kernel shared memory: nbufs ring buffers of tile_vecs * 16 bytes + 2 mbarriers each
+constexpr int kTmaSmemMax = 227 * 1024;
+inline int tma_smem_bytes(int nbufs, int tile_vecs) { return nbufs * tile_vecs * 16 + nbufs * 16; }
 
 
 // Nested quantum-aligned partition (SPEC.md:67-75 when q == 1).  Host and

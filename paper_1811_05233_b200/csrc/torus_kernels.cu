@@ -663,6 +663,453 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
   if (tid == 0 && !s_abort) R->epoch[b] = seq + (uint32_t)T;
 }
 
+// ------------------------------------------------------------------------------------
+// the TMA-staged torus kernel (product path)
+// ------------------------------------------------------------------------------------
+// Same wavefront and flag protocol as torus_kernel, but every transfer that touches a
+// workspace slot -- local or an NVLink peer's -- is a TMA bulk copy (cp.async.bulk):
+//   warp 0      control: polls the iteration's input flags, releases the producer
+//               (READY), and after the storer reports the iteration's stores complete
+//               (DONE) raises the output flags behind one fence.acq_rel.sys
+//   warp 1      producer: lane 0 streams the operands of every job (h_in / v_in slots,
+//               peers' chunk slots) into a ring of shared-memory buffers, one mbarrier
+//               per buffer (full: complete_tx bytes; empty: released by the storer)
+//   warps 2-15  consumers: fold operands out of shared memory (ring order, f32), read and
+//               write the user buffer through registers with the dtype<->wire cast fused,
+//               stage results in shared memory; consumer lane 0 of warp 2 ("storer")
+//               issues the TMA stores (pushes into peers' h_in / v_in, my chunk slot) and
+//               tracks them with bulk async-groups
+// Jobs per tile (X-by-Y grid): A (X-1)*Y pushes, B Y folds of X operands, C one fold of Y
+// operands, D Y-1 pulls, E (X-1)*Y pulls.
+constexpr int kCons = kThreads - 2 * 32;   // consumer threads (warps 2..15)
+constexpr int kBarCons = 3;                // named barrier among the consumers
+constexpr int kTmaMaxBufs = 48;
+constexpr int kStoreLag = 4;               // bulk groups left in flight before a release
+
+enum JobKind { kJobA = 0, kJobB = 1, kJobC = 2, kJobD = 3, kJobE = 4 };
+
+struct Job {
+  int kind;
+  int j, s;            // chunk (column) and sub-chunk (row) of the piece
+  Piece p;
+};
+
+__device__ __forceinline__ void bar_sync_n(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_n(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// wait until at most n bulk groups are pending (n only known at run time)
+__device__ __forceinline__ void tma_wait_all_dyn(int n) {
+  switch (n) {
+    case 0: tma_wait_all<0>(); break;
+    case 1: tma_wait_all<1>(); break;
+    case 2: tma_wait_all<2>(); break;
+    case 3: tma_wait_all<3>(); break;
+    default: tma_wait_all<4>(); break;
+  }
+}
+
+template <int DT, int W>
+__global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs a) {
+  using Acc = typename Wire<W>::Acc;
+  constexpr int VE = Wire<W>::VE;
+  constexpr int SW = kVecBytes / VE;
+
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const int NB = a.nbufs;
+  const int TV = a.tile_vecs;
+  const unsigned PB = (unsigned)TV * kVecBytes;  // bytes per ring buffer (one piece)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NB * PB);
+  uint64_t* empty = full + NB;
+
+  const int lr = blockIdx.x / a.G;
+  const int b = blockIdx.x - lr * a.G;
+  const RankDev* __restrict__ R = a.ranks + lr;
+  const int X = R->X, Y = R->Y, N = R->N, rho = R->rho, c = R->c, me = R->rank;
+  const int G = a.G, q = a.q, T = a.T;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned long long n = a.n;
+  const bool aligned = a.aligned != 0;
+  void* const buf = a.buf[lr];
+  char* const myws = R->ws[me];
+
+  __shared__ uint32_t s_seq;
+  __shared__ int s_abort;
+  if (tid == 0) {
+    s_seq = R->epoch[b];
+    s_abort = 0;
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint32_t seq = s_seq;
+
+  int kinds[kStages];
+  int P = 0;
+  if (X > 1) kinds[P++] = kA;
+  kinds[P++] = kB;
+  if (Y > 1) {
+    kinds[P++] = kC;
+    kinds[P++] = kD;
+  }
+  if (X > 1) kinds[P++] = kE;
+  const int iters = T + 2 * (P - 1);
+
+  // Enumerate the jobs of iteration `it` in a fixed order (identical in every role).
+  auto for_jobs = [&](int it, auto visit) {
+    for (int pp = 0; pp < P; ++pp) {
+      const int t = it - 2 * pp;
+      if (t < 0 || t >= T) continue;
+      Job jb;
+      jb.kind = kinds[pp];
+      switch (jb.kind) {
+        case kA:
+          for (int jj = 1; jj < X; ++jj)
+            for (int s = 0; s < Y; ++s) {
+              jb.j = (c + jj) % X;
+              jb.s = s;
+              jb.p = make_piece(n, X, Y, q, G, b, TV, jb.j, s, t);
+              if (jb.p.p1 > jb.p.p0) visit(jb);
+            }
+          break;
+        case kB:
+          for (int s = 0; s < Y; ++s) {
+            jb.j = c;
+            jb.s = s;
+            jb.p = make_piece(n, X, Y, q, G, b, TV, c, s, t);
+            if (jb.p.p1 > jb.p.p0) visit(jb);
+          }
+          break;
+        case kC:
+          jb.j = c;
+          jb.s = rho;
+          jb.p = make_piece(n, X, Y, q, G, b, TV, c, rho, t);
+          if (jb.p.p1 > jb.p.p0) visit(jb);
+          break;
+        case kD:
+          for (int ii = 1; ii < Y; ++ii) {
+            jb.j = c;
+            jb.s = (rho + ii) % Y;
+            jb.p = make_piece(n, X, Y, q, G, b, TV, c, jb.s, t);
+            if (jb.p.p1 > jb.p.p0) visit(jb);
+          }
+          break;
+        default:
+          for (int jj = 1; jj < X; ++jj)
+            for (int s = 0; s < Y; ++s) {
+              jb.j = (c + jj) % X;
+              jb.s = s;
+              jb.p = make_piece(n, X, Y, q, G, b, TV, jb.j, s, t);
+              if (jb.p.p1 > jb.p.p0) visit(jb);
+            }
+          break;
+      }
+    }
+  };
+  // ring buffers a job uses: TMA-loaded operands first, then (optionally) one scratch
+  auto job_loads = [&](const Job& jb) -> int {
+    switch (jb.kind) {
+      case kA: return 0;
+      case kB: return X - 1;
+      case kC: return Y;
+      default: return 1;
+    }
+  };
+  auto job_scratch = [&](const Job& jb) -> int {
+    return (jb.kind == kA || jb.kind == kB || jb.kind == kC) ? 1 : 0;
+  };
+
+  if (warp == 0) {
+    // =============================== control warp ===============================
+    const unsigned long long deadline = gtimer() + a.timeout_ns;
+    auto flagp = [&](char* ws, int kind, int src) -> uint32_t* {
+      return reinterpret_cast<uint32_t*>(ws) + ((size_t)(kind * kMaxDim + src) * G + b);
+    };
+    auto for_flags = [&](int k, int t, bool in, auto visit) {
+      int kind = -1, cnt = 0;
+      bool row = true;
+      switch (k) {
+        case kA:
+          if (!in) { kind = kFlagH; cnt = X - 1; row = true; }
+          break;
+        case kB:
+          if (in) {
+            if (X > 1) { kind = kFlagH; cnt = X - 1; row = true; }
+          } else if (Y > 1) {
+            kind = kFlagV; cnt = Y - 1; row = false;
+          } else if (X > 1) {
+            kind = kFlagR; cnt = X - 1; row = true;
+          }
+          break;
+        case kC:
+          kind = in ? kFlagV : kFlagAG; cnt = Y - 1; row = false;
+          break;
+        case kD:
+          if (in) { kind = kFlagAG; cnt = Y - 1; row = false; }
+          else if (X > 1) { kind = kFlagR; cnt = X - 1; row = true; }
+          break;
+        default:
+          if (in) { kind = kFlagR; cnt = X - 1; row = true; }
+          break;
+      }
+      const uint32_t v = seq + (uint32_t)t + 1u;
+      for (int l = 0; l < cnt; ++l) {
+        const int other = row ? (c + 1 + l) % X : (rho + 1 + l) % Y;
+        const int peer = row ? rho * X + other : other * X + c;
+        visit(in ? flagp(myws, kind, other) : flagp(R->ws[peer], kind, row ? c : rho), v);
+      }
+    };
+    auto poll_iter = [&](int it) -> bool {
+      bool ok = true;
+      int e = 0;
+      for (int pp = 0; pp < P; ++pp) {
+        const int t = it - 2 * pp;
+        if (t < 0 || t >= T) continue;
+        for_flags(kinds[pp], t, true, [&](uint32_t* f, uint32_t v) {
+          if ((e++ & 31) == lane && ok) {
+            unsigned spin = 0;
+            while ((int32_t)(ld_acquire_sys(f) - v) < 0) {
+              if ((++spin & 255u) == 0 && gtimer() > deadline) {
+                ok = false;
+                break;
+              }
+            }
+          }
+        });
+      }
+      return __all_sync(0xffffffffu, ok);
+    };
+    auto raise_iter = [&](int it) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      int e = 0;
+      for (int pp = 0; pp < P; ++pp) {
+        const int t = it - 2 * pp;
+        if (t < 0 || t >= T) continue;
+        for_flags(kinds[pp], t, false, [&](uint32_t* f, uint32_t v) {
+          if ((e++ & 31) == lane) st_relaxed_sys(f, v);
+        });
+      }
+    };
+    unsigned long long* const tr = (lane == 0 && lr == 0) ? a.trace : nullptr;
+    for (int it = 0; it < iters; ++it) {
+      stamp(tr, b, it, 0);
+      const bool ok = poll_iter(it);
+      stamp(tr, b, it, 1);
+      if (!ok) {  // watchdog: poison the call; the producer walks the rest without loads
+        if (lane == 0) {
+          atomicExch_system(R->err, kErrTimeout);
+          s_abort = 1;
+        }
+        __syncwarp();
+        bar_arrive_n(kBarReady, 64);
+        break;
+      }
+      bar_arrive_n(kBarReady, 64);       // producer may load iteration it
+      stamp(tr, b, it, 3);
+      if (it > 0) {
+        bar_sync_n(kBarDone, 64);        // storer: iteration it-1's stores are complete
+        stamp(tr, b, it, 2);
+        raise_iter(it - 1);
+        stamp(tr, b, it, 4);
+      }
+    }
+    if (!*(volatile int*)&s_abort) {
+      bar_sync_n(kBarDone, 64);
+      raise_iter(iters - 1);
+    }
+  } else if (warp == 1) {
+    // =============================== producer warp ==============================
+    int slot = 0;  // running ring position (same sequence the consumers follow)
+    bool aborted = false;
+    for (int it = 0; it < iters; ++it) {
+      if (!aborted) {
+        bar_sync_n(kBarReady, 64);
+        aborted = *(volatile int*)&s_abort != 0;
+      }
+      if (lane == 0) {
+        fence_proxy_async();  // peers' data acquired by the control warp -> async proxy
+        for_jobs(it, [&](const Job& jb) {
+          const int nl = job_loads(jb), ns = job_scratch(jb);
+          const unsigned bytes = (unsigned)((jb.p.p1 - jb.p.p0) * kVecBytes);
+          for (int o = 0; o < nl + ns; ++o, ++slot) {
+            const int bi = slot % NB;
+            mbar_wait(&empty[bi], ((slot / NB) & 1) ^ 1);
+            if (o >= nl || aborted) {  // scratch buffer, or a poisoned call: no data
+              mbar_arrive(&full[bi]);
+              continue;
+            }
+            const char* src;
+            if (jb.kind == kB) {      // h_in slot of source column (c+1+o) % X
+              const int jsrc = (c + 1 + o) % X;
+              src = myws + a.hin_off + (size_t)jsrc * a.hin_stride + (jb.p.so + jb.p.p0 * VE) * SW;
+            } else if (jb.kind == kC) {  // v_in slot of row (rho+1+o) % Y
+              const int isrc = (rho + 1 + o) % Y;
+              src = myws + a.vin_off + (size_t)isrc * a.vin_stride + jb.p.p0 * VE * SW;
+            } else if (jb.kind == kD) {  // column peer (s, c)'s chunk slot
+              src = R->ws[jb.s * X + c] + a.chunk_off + (jb.p.so + jb.p.p0 * VE) * SW;
+            } else {                     // row peer (rho, j)'s chunk slot
+              src = R->ws[rho * X + jb.j] + a.chunk_off + (jb.p.so + jb.p.p0 * VE) * SW;
+            }
+            mbar_expect_tx(&full[bi], bytes);
+            tma_load(smem + (size_t)bi * PB, src, bytes, &full[bi]);
+          }
+        });
+      }
+      __syncwarp();
+    }
+  } else {
+    // =============================== consumer warps =============================
+    const int ct = tid - 64;               // consumer thread index
+    const bool storer = (ct == 0);         // issues every TMA store (bulk groups are per thread)
+    const bool storer_warp = (warp == 2);
+    int slot = 0;
+    // storer state: ring buffers waiting for their TMA store to finish reading, and the
+    // iteration whose stores still have to complete before DONE may be reported
+    int relq[8];
+    int rq_head = 0, rq_tail = 0;
+    int drain_it = -1, since = 0;
+    unsigned long long* const tr = (ct == 0 && lr == 0) ? a.trace : nullptr;
+    for (int it = 0; it < iters; ++it) {
+      stamp(tr, b, it, 5);
+      for_jobs(it, [&](const Job& jb) {
+        const int nl = job_loads(jb), ns = job_scratch(jb);
+        const int b0 = slot;
+        slot += nl + ns;
+        for (int o = 0; o < nl + ns; ++o) mbar_wait(&full[(b0 + o) % NB], ((b0 + o) / NB) & 1);
+        const unsigned long long nv = jb.p.p1 - jb.p.p0;
+        const unsigned bytes = (unsigned)(nv * kVecBytes);
+        const int bs = (b0 + nl) % NB;       // scratch buffer (if any)
+        unsigned char* const sbuf = smem + (size_t)bs * PB;
+        int store_src = -1;                  // ring buffer a TMA store reads from
+        char* dst0 = nullptr;                // TMA store destination
+        if (jb.kind == kA) {
+          // cast my buffer's share of chunk j into the wire type, push to (rho, j).h_in[c]
+          for (unsigned long long v = ct; v < nv; v += kCons) {
+            const unsigned long long el = jb.p.so + (jb.p.p0 + v) * VE;
+            const int nrem = (int)min((unsigned long long)VE, jb.p.cl - el);
+            *reinterpret_cast<uint4*>(sbuf + v * kVecBytes) =
+                load_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem, aligned);
+          }
+          store_src = bs;
+          dst0 = R->ws[rho * X + jb.j] + a.hin_off + (size_t)c * a.hin_stride +
+                 (jb.p.so + jb.p.p0 * VE) * SW;
+        } else if (jb.kind == kB || jb.kind == kC) {
+          const int nops = (jb.kind == kB) ? X : Y;
+          for (unsigned long long v = ct; v < nv; v += kCons) {
+            const unsigned long long el = jb.p.so + (jb.p.p0 + v) * VE;
+            const int nrem = (int)min((unsigned long long)VE, jb.p.cl - el);
+            Acc acc[VE];
+            for (int k = 0; k < nops; ++k) {  // ring order: sources c+1.. / rho+1.. (C5/C6)
+              uint4 w;
+              if (jb.kind == kB && k == X - 1)  // my own contribution comes last
+                w = load_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem, aligned);
+              else
+                w = *reinterpret_cast<const uint4*>(smem + (size_t)((b0 + k) % NB) * PB + v * kVecBytes);
+              Acc t[VE];
+              unpack<W>(w, t);
+              if (k == 0) {
+#pragma unroll
+                for (int i = 0; i < VE; ++i) acc[i] = t[i];
+              } else {
+                acc_add<W>(acc, t);
+              }
+            }
+            const bool last_reduce = (jb.kind == kC) || (Y == 1);
+            if (last_reduce && a.op == 1) acc_mean<W>(acc, a.inv_n, N);
+            const uint4 out = pack<W>(acc);
+            *reinterpret_cast<uint4*>(sbuf + v * kVecBytes) = out;
+            if (last_reduce) store_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem, out, aligned);
+          }
+          store_src = bs;
+          if (jb.kind == kB && Y > 1)         // P1 -> v_in[rho] of the sub-chunk owner (s, c)
+            dst0 = R->ws[jb.s * X + c] + a.vin_off + (size_t)rho * a.vin_stride + jb.p.p0 * VE * SW;
+          else if (jb.kind == kC || X > 1)    // final value -> my chunk slot (pulled by peers)
+            dst0 = myws + a.chunk_off + (jb.p.so + jb.p.p0 * VE) * SW;
+          else
+            store_src = -1;                   // 1-by-1 row and column: nothing to publish
+        } else {
+          // D / E: pulled wire data -> my user buffer (cast fused); D also fills my chunk slot
+          const unsigned char* lb = smem + (size_t)(b0 % NB) * PB;
+          for (unsigned long long v = ct; v < nv; v += kCons) {
+            const unsigned long long el = jb.p.so + (jb.p.p0 + v) * VE;
+            const int nrem = (int)min((unsigned long long)VE, jb.p.cl - el);
+            store_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem,
+                              *reinterpret_cast<const uint4*>(lb + v * kVecBytes), aligned);
+          }
+          if (jb.kind == kD && X > 1) {
+            store_src = b0 % NB;
+            dst0 = myws + a.chunk_off + (jb.p.so + jb.p.p0 * VE) * SW;
+          }
+        }
+        fence_proxy_async_smem();             // generic smem writes -> async-proxy readers
+        bar_sync_n(kBarCons, kCons);
+        if (storer_warp) {
+          int drained = 0;
+          if (storer) {
+            for (int o = 0; o < nl + ns; ++o) {  // release what no store reads
+              const int bi = (b0 + o) % NB;
+              if (bi != store_src) mbar_arrive(&empty[bi]);
+            }
+            if (store_src >= 0) {
+              if (!*(volatile int*)&s_abort) tma_store(dst0, smem + (size_t)store_src * PB, bytes);
+              tma_commit();                      // one bulk group per job
+              relq[rq_tail++ & 7] = store_src;
+              if (rq_tail - rq_head > kStoreLag) {
+                tma_wait_read<kStoreLag>();
+                while (rq_tail - rq_head > kStoreLag) mbar_arrive(&empty[relq[rq_head++ & 7]]);
+              }
+              if (drain_it >= 0 && ++since >= kStoreLag) {
+                tma_wait_all<kStoreLag>();       // every group of iteration drain_it is done
+                fence_proxy_async();
+                drain_it = -1;
+                drained = 1;
+              }
+            }
+          }
+          if (__shfl_sync(0xffffffffu, drained, 0)) bar_arrive_n(kBarDone, 64);
+        }
+      });
+      // iteration boundary: the previous iteration's stores, if not yet reported
+      if (storer_warp) {
+        int drained = 0;
+        if (storer) {
+          if (drain_it >= 0) {
+            tma_wait_all_dyn(since);
+            fence_proxy_async();
+            drained = 1;
+          }
+          drain_it = it;
+          since = 0;
+        }
+        if (__shfl_sync(0xffffffffu, drained, 0)) bar_arrive_n(kBarDone, 64);
+      }
+      stamp(tr, b, it, 6);
+    }
+    if (storer_warp) {
+      if (storer) {
+        tma_wait_all<0>();
+        fence_proxy_async();
+        while (rq_head < rq_tail) mbar_arrive(&empty[relq[rq_head++ & 7]]);
+      }
+      __syncwarp();
+      bar_arrive_n(kBarDone, 64);            // the last iteration
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && !s_abort) R->epoch[b] = seq + (uint32_t)T;
+}
+
 // N = 1: buf = from_wire(to_wire(buf)); the mean scale is x * 1.0 (identity).
 template <int W>
 __global__ void __launch_bounds__(256) castscale_kernel(float* buf, unsigned long long n) {
@@ -707,6 +1154,23 @@ __global__ void barrier_kernel(const RankDev* ranks, unsigned long long bar_off,
 template <int DT, int W>
 cudaError_t launch_typed(const LaunchArgs& a, bool cooperative, cudaStream_t stream) {
   const dim3 grid(a.nlocal * a.G), block(kThreads);
+  if (a.nbufs > 0) {  // TMA-staged kernel
+    const int smem = tma_smem_bytes(a.nbufs, a.tile_vecs);
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaError_t e = cudaFuncSetAttribute(torus_tma_kernel<DT, W>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmemMax);
+      if (e != cudaSuccess) return e;
+      attr_set = true;
+    }
+    if (cooperative) {
+      void* args[] = {const_cast<LaunchArgs*>(&a)};
+      return cudaLaunchCooperativeKernel((const void*)torus_tma_kernel<DT, W>, grid, block, args, smem,
+                                         stream);
+    }
+    torus_tma_kernel<DT, W><<<grid, block, smem, stream>>>(a);
+    return cudaGetLastError();
+  }
   if (cooperative) {
     void* args[] = {const_cast<LaunchArgs*>(&a)};
     return cudaLaunchCooperativeKernel((const void*)torus_kernel<DT, W>, grid, block, args, 0,
