@@ -543,13 +543,14 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   a.trace = c->d_trace;
   a.nbufs = 0;
   if (c->tma) {
-    // ring buffers of one piece each; every fold job needs max(X,Y)+1 of them at once plus
-    // the storer's in-flight stores, so shrink the piece until enough fit
-    const int need = std::max(c->X, c->Y) + 1 + 4 + 4;
+    // ring buffers of one piece each; a fold job holds max(X,Y)+2 of them at once and the
+    // storer keeps kStoreLag more in flight, so shrink the piece until enough fit
+    const int ratio = (int)(wire_size(dtype) / sw);
+    const int need = std::max(c->X, c->Y) + 2 + 4 + 4;
     int tv = a.tile_vecs;
-    while (tv > 32 && (kTmaSmemMax - 1024) / (tv * 16 + 16) < need) tv /= 2;
+    while (tv > 32 && kTmaSmemMax / (tma_buf_bytes(tv, ratio) + 24) < need) tv /= 2;
     a.tile_vecs = tv;
-    a.nbufs = std::min(48, (kTmaSmemMax - 1024) / (tv * 16 + 16));
+    a.nbufs = std::min(64, kTmaSmemMax / (tma_buf_bytes(tv, ratio) + 24));
     if (a.nbufs < need) return fail(TORUS_ERR_UNSUPPORTED, "grid %dx%d too large for the TMA ring", c->X, c->Y);
   }
   const unsigned long long Lc = R / c->X, Lcs = R / ((unsigned long long)c->X * c->Y);

@@ -75,9 +75,14 @@ struct LaunchArgs {
   int nbufs;                     // > 0: TMA-staged kernel with this many ring buffers
 };
 
-// TMA kernel shared memory: nbufs ring buffers of tile_vecs * 16 bytes + 2 mbarriers each
-constexpr int kTmaSmemMax = 227 * 1024;
-inline int tma_smem_bytes(int nbufs, int tile_vecs) { return nbufs * tile_vecs * 16 + nbufs * 16; }
+// TMA kernel shared memory: nbufs ring buffers of one piece each (tile_vecs 16-byte wire
+// vectors, or the same elements in the user dtype: `ratio` = sizeof(dtype)/sizeof(wire),
+// at least 1) + 3 mbarriers per buffer
+constexpr int kTmaSmemMax = 227 * 1024 - 2048;  // dynamic part; static smem needs the rest
+inline int tma_buf_bytes(int tile_vecs, int ratio) { return tile_vecs * 16 * (ratio > 1 ? ratio : 1); }
+inline int tma_smem_bytes(int nbufs, int tile_vecs, int ratio) {
+  return nbufs * tma_buf_bytes(tile_vecs, ratio) + nbufs * 24;
+}
 
 
 // Nested quantum-aligned partition (SPEC.md:67-75 when q == 1).  Host and

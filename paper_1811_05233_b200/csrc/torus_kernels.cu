@@ -51,6 +51,16 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -666,27 +676,26 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
 // ------------------------------------------------------------------------------------
 // the TMA-staged torus kernel (product path)
 // ------------------------------------------------------------------------------------
-// Same wavefront and flag protocol as torus_kernel, but every transfer that touches a
-// workspace slot -- local or an NVLink peer's -- is a TMA bulk copy (cp.async.bulk):
-//   warp 0      control: polls the iteration's input flags, releases the producer
-//               (READY), and after the storer reports the iteration's stores complete
-//               (DONE) raises the output flags behind one fence.acq_rel.sys
-//   warp 1      producer: lane 0 streams the operands of every job (h_in / v_in slots,
-//               peers' chunk slots) into a ring of shared-memory buffers, one mbarrier
-//               per buffer (full: complete_tx bytes; empty: released by the storer)
-//   warps 2-15  consumers: fold operands out of shared memory (ring order, f32), read and
-//               write the user buffer through registers with the dtype<->wire cast fused,
-//               stage results in shared memory; consumer lane 0 of warp 2 ("storer")
-//               issues the TMA stores (pushes into peers' h_in / v_in, my chunk slot) and
-//               tracks them with bulk async-groups
-// Jobs per tile (X-by-Y grid): A (X-1)*Y pushes, B Y folds of X operands, C one fold of Y
-// operands, D Y-1 pulls, E (X-1)*Y pulls.
-constexpr int kCons = kThreads - 2 * 32;   // consumer threads (warps 2..15)
-constexpr int kBarCons = 3;                // named barrier among the consumers
-constexpr int kTmaMaxBufs = 48;
-constexpr int kStoreLag = 4;               // bulk groups left in flight before a release
-
-enum JobKind { kJobA = 0, kJobB = 1, kJobC = 2, kJobD = 3, kJobE = 4 };
+// Same wavefront and flag protocol as torus_kernel (stage p of iteration it works on
+// tile it - 2p), with every bulk transfer done by TMA (cp.async.bulk) and four roles
+// that only meet at per-buffer mbarriers:
+//   warp 0      control: polls the iteration's input flags (ld.acquire.sys), releases
+//               the producer (READY), and once the storer reports the iteration's stores
+//               complete (DONE) raises the output flags behind one fence.acq_rel.sys
+//   warp 1      producer (lane 0): streams every operand -- my user buffer, my h_in /
+//               v_in slots, the peers' chunk slots over NVLink -- into a ring of shared
+//               memory buffers (full[b]: complete_tx; waits empty[b])
+//   warp 2      storer (lane 0): per job, waits until the consumers are done with the
+//               buffers (consumed[b]) or the data landed (full[b], pure copies), issues
+//               the TMA stores (pushes into peers' h_in / v_in, my chunk slot), releases
+//               buffers (empty[b]) once their store has read them, and drains every
+//               iteration's stores (bulk async-groups) before reporting DONE
+//   warps 3-15  consumers: fold operands out of shared memory in ring order (f32
+//               accumulation), apply the mean, round once, stage results in
+//               shared memory and write the user buffer (wire->dtype cast fused)
+constexpr int kConsWarps = kThreads / 32 - 3;  // warps 3..15
+constexpr int kCons = kConsWarps * 32;
+constexpr int kStoreLag = 4;                    // bulk groups in flight before a release
 
 struct Job {
   int kind;
@@ -706,29 +715,22 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-// wait until at most n bulk groups are pending (n only known at run time)
-__device__ __forceinline__ void tma_wait_all_dyn(int n) {
-  switch (n) {
-    case 0: tma_wait_all<0>(); break;
-    case 1: tma_wait_all<1>(); break;
-    case 2: tma_wait_all<2>(); break;
-    case 3: tma_wait_all<3>(); break;
-    default: tma_wait_all<4>(); break;
-  }
-}
 
 template <int DT, int W>
 __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs a) {
   using Acc = typename Wire<W>::Acc;
+  using UT = typename Elem<DT>::T;
   constexpr int VE = Wire<W>::VE;
   constexpr int SW = kVecBytes / VE;
+  constexpr int ST = (int)sizeof(UT);
 
   extern __shared__ __align__(1024) unsigned char smem[];
   const int NB = a.nbufs;
   const int TV = a.tile_vecs;
-  const unsigned PB = (unsigned)TV * kVecBytes;  // bytes per ring buffer (one piece)
+  const unsigned PB = (unsigned)TV * VE * (ST > SW ? ST : SW);  // one piece, user or wire layout
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NB * PB);
   uint64_t* empty = full + NB;
+  uint64_t* consumed = empty + NB;
 
   const int lr = blockIdx.x / a.G;
   const int b = blockIdx.x - lr * a.G;
@@ -743,12 +745,17 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
 
   __shared__ uint32_t s_seq;
   __shared__ int s_abort;
+  __shared__ int s_ready;  // control -> producer: iterations whose inputs are visible
+  __shared__ int s_done;   // storer -> control: iterations whose stores are complete
   if (tid == 0) {
     s_seq = R->epoch[b];
     s_abort = 0;
+    s_ready = 0;
+    s_done = 0;
     for (int i = 0; i < NB; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
+      mbar_init(&consumed[i], kConsWarps);
     }
     fence_mbar_init();
   }
@@ -766,68 +773,72 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
   if (X > 1) kinds[P++] = kE;
   const int iters = T + 2 * (P - 1);
 
-  // Enumerate the jobs of iteration `it` in a fixed order (identical in every role).
+  // Jobs of iteration `it` in a fixed order (identical in every role).
   auto for_jobs = [&](int it, auto visit) {
     for (int pp = 0; pp < P; ++pp) {
       const int t = it - 2 * pp;
       if (t < 0 || t >= T) continue;
       Job jb;
       jb.kind = kinds[pp];
-      switch (jb.kind) {
-        case kA:
-          for (int jj = 1; jj < X; ++jj)
-            for (int s = 0; s < Y; ++s) {
-              jb.j = (c + jj) % X;
-              jb.s = s;
-              jb.p = make_piece(n, X, Y, q, G, b, TV, jb.j, s, t);
-              if (jb.p.p1 > jb.p.p0) visit(jb);
-            }
-          break;
-        case kB:
+      if (jb.kind == kA || jb.kind == kE) {
+        for (int jj = 1; jj < X; ++jj)
           for (int s = 0; s < Y; ++s) {
-            jb.j = c;
+            jb.j = (c + jj) % X;
             jb.s = s;
-            jb.p = make_piece(n, X, Y, q, G, b, TV, c, s, t);
+            jb.p = make_piece(n, X, Y, q, G, b, TV, jb.j, s, t);
             if (jb.p.p1 > jb.p.p0) visit(jb);
           }
-          break;
-        case kC:
+      } else if (jb.kind == kB) {
+        for (int s = 0; s < Y; ++s) {
           jb.j = c;
-          jb.s = rho;
-          jb.p = make_piece(n, X, Y, q, G, b, TV, c, rho, t);
+          jb.s = s;
+          jb.p = make_piece(n, X, Y, q, G, b, TV, c, s, t);
           if (jb.p.p1 > jb.p.p0) visit(jb);
-          break;
-        case kD:
-          for (int ii = 1; ii < Y; ++ii) {
-            jb.j = c;
-            jb.s = (rho + ii) % Y;
-            jb.p = make_piece(n, X, Y, q, G, b, TV, c, jb.s, t);
-            if (jb.p.p1 > jb.p.p0) visit(jb);
-          }
-          break;
-        default:
-          for (int jj = 1; jj < X; ++jj)
-            for (int s = 0; s < Y; ++s) {
-              jb.j = (c + jj) % X;
-              jb.s = s;
-              jb.p = make_piece(n, X, Y, q, G, b, TV, jb.j, s, t);
-              if (jb.p.p1 > jb.p.p0) visit(jb);
-            }
-          break;
+        }
+      } else if (jb.kind == kC) {
+        jb.j = c;
+        jb.s = rho;
+        jb.p = make_piece(n, X, Y, q, G, b, TV, c, rho, t);
+        if (jb.p.p1 > jb.p.p0) visit(jb);
+      } else {
+        for (int ii = 1; ii < Y; ++ii) {
+          jb.j = c;
+          jb.s = (rho + ii) % Y;
+          jb.p = make_piece(n, X, Y, q, G, b, TV, c, jb.s, t);
+          if (jb.p.p1 > jb.p.p0) visit(jb);
+        }
       }
     }
   };
-  // ring buffers a job uses: TMA-loaded operands first, then (optionally) one scratch
-  auto job_loads = [&](const Job& jb) -> int {
-    switch (jb.kind) {
-      case kA: return 0;
-      case kB: return X - 1;
-      case kC: return Y;
-      default: return 1;
-    }
+  // Vectors of a piece whose user-buffer side can go through TMA (16-byte aligned full
+  // vectors); a ragged last vector is handled by the consumers with scalar accesses.
+  auto user_tma_vecs = [&](const Job& jb) -> unsigned long long {
+    if (!aligned) return 0;
+    const unsigned long long nv = jb.p.p1 - jb.p.p0;
+    const unsigned long long last_el = jb.p.so + (jb.p.p1 - 1) * VE;
+    return (last_el + VE > jb.p.cl) ? nv - 1 : nv;
   };
-  auto job_scratch = [&](const Job& jb) -> int {
-    return (jb.kind == kA || jb.kind == kB || jb.kind == kC) ? 1 : 0;
+  // Buffer plan of a job: [TMA loads ...][user piece?][scratch?]
+  //   A: user (if TMA) + scratch when consumers must touch it (cast / ragged / unaligned)
+  //   B: X-1 h_in loads + user (if TMA) + scratch      C: Y v_in loads + scratch
+  //   D, E: one peer chunk load
+  auto wire_loads = [&](const Job& jb) -> int {
+    return jb.kind == kB ? X - 1 : jb.kind == kC ? Y : (jb.kind == kA ? 0 : 1);
+  };
+  auto has_user_load = [&](const Job& jb) -> bool {
+    return (jb.kind == kA || jb.kind == kB) && user_tma_vecs(jb) > 0;
+  };
+  // A is a pure copy (no consumer work) when the whole piece moves by TMA unchanged.
+  auto a_is_copy = [&](const Job& jb) -> bool {
+    return DT == W && user_tma_vecs(jb) == jb.p.p1 - jb.p.p0;
+  };
+  auto has_scratch = [&](const Job& jb) -> bool {
+    if (jb.kind == kA) return !a_is_copy(jb);
+    return jb.kind == kB || jb.kind == kC;
+  };
+  auto consumer_work = [&](const Job& jb) -> bool { return !(jb.kind == kA && a_is_copy(jb)); };
+  auto nbufs_of = [&](const Job& jb) -> int {
+    return wire_loads(jb) + (has_user_load(jb) ? 1 : 0) + (has_scratch(jb) ? 1 : 0);
   };
 
   if (warp == 0) {
@@ -902,60 +913,70 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
       }
     };
     unsigned long long* const tr = (lane == 0 && lr == 0) ? a.trace : nullptr;
+    bool aborted = false;
     for (int it = 0; it < iters; ++it) {
       stamp(tr, b, it, 0);
-      const bool ok = poll_iter(it);
-      stamp(tr, b, it, 1);
-      if (!ok) {  // watchdog: poison the call; the producer walks the rest without loads
+      if (!poll_iter(it)) {  // watchdog: poison; the producer walks the rest without loads
         if (lane == 0) {
           atomicExch_system(R->err, kErrTimeout);
           s_abort = 1;
+          st_release_cta(&s_ready, iters);
         }
         __syncwarp();
-        bar_arrive_n(kBarReady, 64);
+        aborted = true;
         break;
       }
-      bar_arrive_n(kBarReady, 64);       // producer may load iteration it
+      stamp(tr, b, it, 1);
+      if (lane == 0) st_release_cta(&s_ready, it + 1);  // producer may load iteration it
+      __syncwarp();
       stamp(tr, b, it, 3);
       if (it > 0) {
-        bar_sync_n(kBarDone, 64);        // storer: iteration it-1's stores are complete
+        while (ld_acquire_cta(&s_done) < it) {}      // iteration it-1's stores complete
         stamp(tr, b, it, 2);
         raise_iter(it - 1);
         stamp(tr, b, it, 4);
       }
     }
-    if (!*(volatile int*)&s_abort) {
-      bar_sync_n(kBarDone, 64);
+    if (!aborted) {
+      while (ld_acquire_cta(&s_done) < iters) {}
       raise_iter(iters - 1);
     }
   } else if (warp == 1) {
     // =============================== producer warp ==============================
-    int slot = 0;  // running ring position (same sequence the consumers follow)
+    int slot = 0;
     bool aborted = false;
     for (int it = 0; it < iters; ++it) {
-      if (!aborted) {
-        bar_sync_n(kBarReady, 64);
-        aborted = *(volatile int*)&s_abort != 0;
-      }
       if (lane == 0) {
-        fence_proxy_async();  // peers' data acquired by the control warp -> async proxy
+        if (!aborted) {
+          while (ld_acquire_cta(&s_ready) <= it) {}
+          aborted = *(volatile int*)&s_abort != 0;
+        }
+        fence_proxy_async();  // data the control warp acquired -> async-proxy loads
         for_jobs(it, [&](const Job& jb) {
-          const int nl = job_loads(jb), ns = job_scratch(jb);
-          const unsigned bytes = (unsigned)((jb.p.p1 - jb.p.p0) * kVecBytes);
-          for (int o = 0; o < nl + ns; ++o, ++slot) {
+          const int nw = wire_loads(jb);
+          const bool ul = has_user_load(jb);
+          const int nbj = nbufs_of(jb);
+          const unsigned wbytes = (unsigned)((jb.p.p1 - jb.p.p0) * kVecBytes);
+          for (int o = 0; o < nbj; ++o, ++slot) {
             const int bi = slot % NB;
             mbar_wait(&empty[bi], ((slot / NB) & 1) ^ 1);
-            if (o >= nl || aborted) {  // scratch buffer, or a poisoned call: no data
+            const bool is_user = ul && o == nw;
+            if (aborted || o > nw || (o == nw && !ul)) {  // scratch / poisoned: no data
               mbar_arrive(&full[bi]);
               continue;
             }
             const char* src;
-            if (jb.kind == kB) {      // h_in slot of source column (c+1+o) % X
-              const int jsrc = (c + 1 + o) % X;
-              src = myws + a.hin_off + (size_t)jsrc * a.hin_stride + (jb.p.so + jb.p.p0 * VE) * SW;
+            unsigned bytes = wbytes;
+            if (is_user) {
+              bytes = (unsigned)(user_tma_vecs(jb) * VE * ST);
+              src = reinterpret_cast<const char*>(buf) +
+                    (a.buf_off + jb.p.co + jb.p.so + jb.p.p0 * VE) * ST;
+            } else if (jb.kind == kB) {  // h_in slot of source column (c+1+o) % X
+              src = myws + a.hin_off + (size_t)((c + 1 + o) % X) * a.hin_stride +
+                    (jb.p.so + jb.p.p0 * VE) * SW;
             } else if (jb.kind == kC) {  // v_in slot of row (rho+1+o) % Y
-              const int isrc = (rho + 1 + o) % Y;
-              src = myws + a.vin_off + (size_t)isrc * a.vin_stride + jb.p.p0 * VE * SW;
+              src = myws + a.vin_off + (size_t)((rho + 1 + o) % Y) * a.vin_stride +
+                    jb.p.p0 * VE * SW;
             } else if (jb.kind == kD) {  // column peer (s, c)'s chunk slot
               src = R->ws[jb.s * X + c] + a.chunk_off + (jb.p.so + jb.p.p0 * VE) * SW;
             } else {                     // row peer (rho, j)'s chunk slot
@@ -968,54 +989,104 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
       }
       __syncwarp();
     }
-  } else {
-    // =============================== consumer warps =============================
-    const int ct = tid - 64;               // consumer thread index
-    const bool storer = (ct == 0);         // issues every TMA store (bulk groups are per thread)
-    const bool storer_warp = (warp == 2);
+  } else if (warp == 2) {
+    // =============================== storer warp ================================
     int slot = 0;
-    // storer state: ring buffers waiting for their TMA store to finish reading, and the
-    // iteration whose stores still have to complete before DONE may be reported
     int relq[8];
     int rq_head = 0, rq_tail = 0;
-    int drain_it = -1, since = 0;
+    for (int it = 0; it < iters; ++it) {
+      if (lane == 0) {
+        for_jobs(it, [&](const Job& jb) {
+          const int b0 = slot, nbj = nbufs_of(jb);
+          slot += nbj;
+          const int last = (b0 + nbj - 1) % NB;
+          const unsigned long long nv = jb.p.p1 - jb.p.p0;
+          if (consumer_work(jb)) mbar_wait(&consumed[last], ((b0 + nbj - 1) / NB) & 1);
+          else mbar_wait(&full[last], ((b0 + nbj - 1) / NB) & 1);
+          // the buffer a TMA store reads and where it goes
+          int src_b = -1;
+          char* dst = nullptr;
+          if (jb.kind == kA) {
+            src_b = last;  // pure copy: the user piece itself; else the cast scratch
+            dst = R->ws[rho * X + jb.j] + a.hin_off + (size_t)c * a.hin_stride +
+                  (jb.p.so + jb.p.p0 * VE) * SW;
+          } else if (jb.kind == kB && Y > 1) {  // P1 -> v_in[rho] of sub-chunk owner (s, c)
+            src_b = last;
+            dst = R->ws[jb.s * X + c] + a.vin_off + (size_t)rho * a.vin_stride + jb.p.p0 * VE * SW;
+          } else if ((jb.kind == kB && X > 1) || jb.kind == kC || (jb.kind == kD && X > 1)) {
+            src_b = last;  // final values -> my chunk slot, pulled by row / column peers
+            dst = myws + a.chunk_off + (jb.p.so + jb.p.p0 * VE) * SW;
+          }
+          for (int o = 0; o < nbj; ++o) {
+            const int bi = (b0 + o) % NB;
+            if (bi != src_b) mbar_arrive(&empty[bi]);
+          }
+          if (src_b >= 0) {
+            if (!*(volatile int*)&s_abort)
+              tma_store(dst, smem + (size_t)src_b * PB, (unsigned)(nv * kVecBytes));
+            tma_commit();
+            relq[rq_tail++ & 7] = src_b;
+            if (rq_tail - rq_head > kStoreLag) {
+              tma_wait_read<kStoreLag>();
+              while (rq_tail - rq_head > kStoreLag) mbar_arrive(&empty[relq[rq_head++ & 7]]);
+            }
+          }
+        });
+        // every store of iteration it must be complete before its flags are raised
+        tma_wait_all<0>();
+        fence_proxy_async();
+        while (rq_head < rq_tail) mbar_arrive(&empty[relq[rq_head++ & 7]]);
+        st_release_cta(&s_done, it + 1);
+      }
+      __syncwarp();
+    }
+  } else {
+    // =============================== consumer warps =============================
+    const int ct = tid - 96;
+    int slot = 0;
     unsigned long long* const tr = (ct == 0 && lr == 0) ? a.trace : nullptr;
     for (int it = 0; it < iters; ++it) {
       stamp(tr, b, it, 5);
       for_jobs(it, [&](const Job& jb) {
-        const int nl = job_loads(jb), ns = job_scratch(jb);
-        const int b0 = slot;
-        slot += nl + ns;
-        for (int o = 0; o < nl + ns; ++o) mbar_wait(&full[(b0 + o) % NB], ((b0 + o) / NB) & 1);
+        const int b0 = slot, nbj = nbufs_of(jb);
+        slot += nbj;
+        if (!consumer_work(jb)) return;
+        for (int o = 0; o < nbj; ++o) mbar_wait(&full[(b0 + o) % NB], ((b0 + o) / NB) & 1);
+        const bool write_user = *(volatile int*)&s_abort == 0;  // a poisoned call leaves it
+        const int nw = wire_loads(jb);
+        const bool ul = has_user_load(jb);
         const unsigned long long nv = jb.p.p1 - jb.p.p0;
-        const unsigned bytes = (unsigned)(nv * kVecBytes);
-        const int bs = (b0 + nl) % NB;       // scratch buffer (if any)
-        unsigned char* const sbuf = smem + (size_t)bs * PB;
-        int store_src = -1;                  // ring buffer a TMA store reads from
-        char* dst0 = nullptr;                // TMA store destination
-        if (jb.kind == kA) {
-          // cast my buffer's share of chunk j into the wire type, push to (rho, j).h_in[c]
-          for (unsigned long long v = ct; v < nv; v += kCons) {
-            const unsigned long long el = jb.p.so + (jb.p.p0 + v) * VE;
-            const int nrem = (int)min((unsigned long long)VE, jb.p.cl - el);
-            *reinterpret_cast<uint4*>(sbuf + v * kVecBytes) =
-                load_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem, aligned);
+        const unsigned long long nut = user_tma_vecs(jb);
+        const unsigned char* const ubuf = smem + (size_t)((b0 + nw) % NB) * PB;  // user piece
+        unsigned char* const out = smem + (size_t)((b0 + nbj - 1) % NB) * PB;     // last buffer
+        // my user-buffer vector v of the piece, converted to the wire type
+        auto user_vec = [&](unsigned long long v, unsigned long long el, int nrem) -> uint4 {
+          if (ul && v < nut) {
+            if constexpr (DT == W) {
+              return *reinterpret_cast<const uint4*>(ubuf + v * kVecBytes);
+            } else {
+              const float* f = reinterpret_cast<const float*>(ubuf + v * VE * ST);
+              float t[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) t[i] = f[i];
+              return pack<W>(t);
+            }
           }
-          store_src = bs;
-          dst0 = R->ws[rho * X + jb.j] + a.hin_off + (size_t)c * a.hin_stride +
-                 (jb.p.so + jb.p.p0 * VE) * SW;
-        } else if (jb.kind == kB || jb.kind == kC) {
-          const int nops = (jb.kind == kB) ? X : Y;
-          for (unsigned long long v = ct; v < nv; v += kCons) {
-            const unsigned long long el = jb.p.so + (jb.p.p0 + v) * VE;
-            const int nrem = (int)min((unsigned long long)VE, jb.p.cl - el);
+          return load_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem, aligned);
+        };
+        for (unsigned long long v = ct; v < nv; v += kCons) {
+          const unsigned long long el = jb.p.so + (jb.p.p0 + v) * VE;
+          const int nrem = (int)min((unsigned long long)VE, jb.p.cl - el);
+          if (jb.kind == kA) {
+            *reinterpret_cast<uint4*>(out + v * kVecBytes) = user_vec(v, el, nrem);
+          } else if (jb.kind == kB || jb.kind == kC) {
+            const int nops = (jb.kind == kB) ? X : Y;
             Acc acc[VE];
-            for (int k = 0; k < nops; ++k) {  // ring order: sources c+1.. / rho+1.. (C5/C6)
-              uint4 w;
-              if (jb.kind == kB && k == X - 1)  // my own contribution comes last
-                w = load_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem, aligned);
-              else
-                w = *reinterpret_cast<const uint4*>(smem + (size_t)((b0 + k) % NB) * PB + v * kVecBytes);
+            for (int k = 0; k < nops; ++k) {  // ring order; my own contribution last in B
+              const uint4 w = (jb.kind == kB && k == X - 1)
+                                  ? user_vec(v, el, nrem)
+                                  : *reinterpret_cast<const uint4*>(smem + (size_t)((b0 + k) % NB) * PB +
+                                                                    v * kVecBytes);
               Acc t[VE];
               unpack<W>(w, t);
               if (k == 0) {
@@ -1027,83 +1098,20 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
             }
             const bool last_reduce = (jb.kind == kC) || (Y == 1);
             if (last_reduce && a.op == 1) acc_mean<W>(acc, a.inv_n, N);
-            const uint4 out = pack<W>(acc);
-            *reinterpret_cast<uint4*>(sbuf + v * kVecBytes) = out;
-            if (last_reduce) store_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem, out, aligned);
-          }
-          store_src = bs;
-          if (jb.kind == kB && Y > 1)         // P1 -> v_in[rho] of the sub-chunk owner (s, c)
-            dst0 = R->ws[jb.s * X + c] + a.vin_off + (size_t)rho * a.vin_stride + jb.p.p0 * VE * SW;
-          else if (jb.kind == kC || X > 1)    // final value -> my chunk slot (pulled by peers)
-            dst0 = myws + a.chunk_off + (jb.p.so + jb.p.p0 * VE) * SW;
-          else
-            store_src = -1;                   // 1-by-1 row and column: nothing to publish
-        } else {
-          // D / E: pulled wire data -> my user buffer (cast fused); D also fills my chunk slot
-          const unsigned char* lb = smem + (size_t)(b0 % NB) * PB;
-          for (unsigned long long v = ct; v < nv; v += kCons) {
-            const unsigned long long el = jb.p.so + (jb.p.p0 + v) * VE;
-            const int nrem = (int)min((unsigned long long)VE, jb.p.cl - el);
+            const uint4 o = pack<W>(acc);
+            *reinterpret_cast<uint4*>(out + v * kVecBytes) = o;
+            if (last_reduce && write_user)
+              store_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem, o, aligned);
+          } else if (write_user) {  // D / E: pulled wire data -> my user buffer
             store_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem,
-                              *reinterpret_cast<const uint4*>(lb + v * kVecBytes), aligned);
-          }
-          if (jb.kind == kD && X > 1) {
-            store_src = b0 % NB;
-            dst0 = myws + a.chunk_off + (jb.p.so + jb.p.p0 * VE) * SW;
+                              *reinterpret_cast<const uint4*>(out + v * kVecBytes), aligned);
           }
         }
-        fence_proxy_async_smem();             // generic smem writes -> async-proxy readers
-        bar_sync_n(kBarCons, kCons);
-        if (storer_warp) {
-          int drained = 0;
-          if (storer) {
-            for (int o = 0; o < nl + ns; ++o) {  // release what no store reads
-              const int bi = (b0 + o) % NB;
-              if (bi != store_src) mbar_arrive(&empty[bi]);
-            }
-            if (store_src >= 0) {
-              if (!*(volatile int*)&s_abort) tma_store(dst0, smem + (size_t)store_src * PB, bytes);
-              tma_commit();                      // one bulk group per job
-              relq[rq_tail++ & 7] = store_src;
-              if (rq_tail - rq_head > kStoreLag) {
-                tma_wait_read<kStoreLag>();
-                while (rq_tail - rq_head > kStoreLag) mbar_arrive(&empty[relq[rq_head++ & 7]]);
-              }
-              if (drain_it >= 0 && ++since >= kStoreLag) {
-                tma_wait_all<kStoreLag>();       // every group of iteration drain_it is done
-                fence_proxy_async();
-                drain_it = -1;
-                drained = 1;
-              }
-            }
-          }
-          if (__shfl_sync(0xffffffffu, drained, 0)) bar_arrive_n(kBarDone, 64);
-        }
+        fence_proxy_async_smem();  // staged results -> the storer's async-proxy reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&consumed[(b0 + nbj - 1) % NB]);
       });
-      // iteration boundary: the previous iteration's stores, if not yet reported
-      if (storer_warp) {
-        int drained = 0;
-        if (storer) {
-          if (drain_it >= 0) {
-            tma_wait_all_dyn(since);
-            fence_proxy_async();
-            drained = 1;
-          }
-          drain_it = it;
-          since = 0;
-        }
-        if (__shfl_sync(0xffffffffu, drained, 0)) bar_arrive_n(kBarDone, 64);
-      }
       stamp(tr, b, it, 6);
-    }
-    if (storer_warp) {
-      if (storer) {
-        tma_wait_all<0>();
-        fence_proxy_async();
-        while (rq_head < rq_tail) mbar_arrive(&empty[relq[rq_head++ & 7]]);
-      }
-      __syncwarp();
-      bar_arrive_n(kBarDone, 64);            // the last iteration
     }
   }
   __syncthreads();
@@ -1155,7 +1163,7 @@ template <int DT, int W>
 cudaError_t launch_typed(const LaunchArgs& a, bool cooperative, cudaStream_t stream) {
   const dim3 grid(a.nlocal * a.G), block(kThreads);
   if (a.nbufs > 0) {  // TMA-staged kernel
-    const int smem = tma_smem_bytes(a.nbufs, a.tile_vecs);
+    const int smem = tma_smem_bytes(a.nbufs, a.tile_vecs, (int)(sizeof(typename Elem<DT>::T) * Wire<W>::VE / 16));
     static bool attr_set = false;
     if (!attr_set) {
       cudaError_t e = cudaFuncSetAttribute(torus_tma_kernel<DT, W>,

@@ -14,6 +14,11 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+# GPU test runs use a short device watchdog so a protocol bug fails fast instead of
+# spinning for the default 30 s per call.
+os.environ.setdefault("TORUS_TIMEOUT_MS", "5000")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "multigpu: needs >= 2 CUDA devices")
