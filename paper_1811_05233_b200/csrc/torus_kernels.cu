@@ -1001,8 +1001,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
           slot += nbj;
           const int last = (b0 + nbj - 1) % NB;
           const unsigned long long nv = jb.p.p1 - jb.p.p0;
-          if (consumer_work(jb)) mbar_wait(&consumed[last], ((b0 + nbj - 1) / NB) & 1);
-          else mbar_wait(&full[last], ((b0 + nbj - 1) / NB) & 1);
+          for (int o = 0; o < nbj; ++o) mbar_wait(&consumed[(b0 + o) % NB], ((b0 + o) / NB) & 1);
           // the buffer a TMA store reads and where it goes
           int src_b = -1;
           char* dst = nullptr;
@@ -1050,8 +1049,19 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
       for_jobs(it, [&](const Job& jb) {
         const int b0 = slot, nbj = nbufs_of(jb);
         slot += nbj;
-        if (!consumer_work(jb)) return;
+        // Every buffer's full / consumed / empty barriers advance exactly once per use, so
+        // the consumers wait for and sign off every buffer of every job, even pure copies.
         for (int o = 0; o < nbj; ++o) mbar_wait(&full[(b0 + o) % NB], ((b0 + o) / NB) & 1);
+        auto sign_off = [&]() {
+          fence_proxy_async_smem();  // staged results -> the storer's async-proxy reads
+          __syncwarp();
+          if (lane == 0)
+            for (int o = 0; o < nbj; ++o) mbar_arrive(&consumed[(b0 + o) % NB]);
+        };
+        if (!consumer_work(jb)) {
+          sign_off();
+          return;
+        }
         const bool write_user = *(volatile int*)&s_abort == 0;  // a poisoned call leaves it
         const int nw = wire_loads(jb);
         const bool ul = has_user_load(jb);
@@ -1107,9 +1117,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
                               *reinterpret_cast<const uint4*>(out + v * kVecBytes), aligned);
           }
         }
-        fence_proxy_async_smem();  // staged results -> the storer's async-proxy reads
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&consumed[(b0 + nbj - 1) % NB]);
+        sign_off();
       });
       stamp(tr, b, it, 6);
     }
