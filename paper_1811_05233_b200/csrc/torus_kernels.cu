@@ -1036,6 +1036,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
         fence_proxy_async();
         while (rq_head < rq_tail) mbar_arrive(&empty[relq[rq_head++ & 7]]);
         st_release_cta(&s_done, it + 1);
+        stamp(lr == 0 ? a.trace : nullptr, b, it, 7);
       }
       __syncwarp();
     }

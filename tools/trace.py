@@ -45,18 +45,17 @@ def main():
         rel = (tr - t0) / 1e3
         print(json.dumps({"grid": f"{X}x{Y}", "ctas": G, "iters": iters,
                           "kernel_span_us": float(rel[:, :iters, 6].max())}))
-        names = ["poll", "doneWait", "readyArr", "raise", "wkIdle", "wkWork"]
         for it in range(iters):
             r = rel[:, it, :]
-            prev6 = rel[:, it - 1, 6] if it > 0 else rel[:, it, 0]
             d = {"it": it,
-                 "start_cta0": round(float(r[0, 0]), 2),
+                 "t_poll0": round(float(r[:, 0].mean()), 2),
                  "poll": round(float((r[:, 1] - r[:, 0]).mean()), 2),
-                 "doneWait": round(float((r[:, 2] - r[:, 1]).mean()), 2),
-                 "raise": round(float((r[:, 4] - r[:, 3]).mean()), 2),
-                 "wkIdle": round(float((r[:, 5] - prev6).mean()), 2),
-                 "wkWork": round(float((r[:, 6] - r[:, 5]).mean()), 2),
-                 "wkWork_max": round(float((r[:, 6] - r[:, 5]).max()), 2)}
+                 "doneWait": round(float((r[:, 2] - r[:, 3]).mean()), 2) if it else 0,
+                 "raise": round(float((r[:, 4] - r[:, 2]).mean()), 2) if it else 0,
+                 "cons_start": round(float(r[:, 5].mean()), 2),
+                 "cons_busy": round(float((r[:, 6] - r[:, 5]).mean()), 2),
+                 "storer_done": round(float(r[:, 7].mean()), 2),
+                 "drain_after_cons": round(float((r[:, 7] - r[:, 6]).mean()), 2)}
             print(json.dumps(d))
     comm.destroy()
     dist.destroy_process_group()
