@@ -1358,6 +1358,19 @@ __global__ void __launch_bounds__(32) tma_probe_kernel(const RankDev* ranks, uns
   const RankDev* R = ranks;
   const int N = R->N, me = R->rank, G = gridDim.x, b = blockIdx.x;
   if (threadIdx.x != 0) return;
+  if (mode == 6 || mode == 7) {
+    // fence.acq_rel.sys latency: CTA 0 times 200 fences (mode 6: while the other CTAs
+    // stream TMA pushes; mode 7: on a quiet GPU); ns/fence -> barrier area + 8 KiB
+    // (data_off = bar_off + 64 KiB, see SlabLayout)
+    if (b == 0) {
+      const unsigned long long t0 = gtimer();
+      for (int i = 0; i < 200; ++i) asm volatile("fence.acq_rel.sys;" ::: "memory");
+      *reinterpret_cast<unsigned long long*>(R->ws[me] + data_off - 65536 + 8192) = (gtimer() - t0) / 200;
+      return;
+    }
+    if (mode == 7) return;
+    mode = 4;
+  }
   for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
   fence_mbar_init();
   const unsigned long long per = (bytes / (N - 1)) / kTmaChunk * kTmaChunk;
@@ -1405,7 +1418,7 @@ __global__ void __launch_bounds__(32) tma_probe_kernel(const RankDev* ranks, uns
 
 cudaError_t launch_probe(const RankDev* ranks, unsigned long long data_off, unsigned long long bytes,
                          int mode, int iters, int ctas, unsigned long long* out, cudaStream_t stream) {
-  if (mode == 4 || mode == 5) {
+  if (mode >= 4 && mode <= 7) {
     const int smem = kTmaStages * kTmaChunk + kTmaStages * 8;
     cudaError_t e = cudaFuncSetAttribute(tma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;

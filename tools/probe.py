@@ -44,6 +44,14 @@ def main():
             if rank == 0:
                 print(json.dumps(rec), flush=True)
             dist.barrier()
+    for mode, name in ((7, "fence_quiet"), (6, "fence_under_tma_push")):
+        torch.cuda.synchronize()
+        dist.barrier()
+        ns = comm.probe(mode, nbytes, ctas=148)
+        torch.cuda.synchronize()
+        if rank == 0:
+            print(json.dumps({"probe": name, "ns_per_fence": ns}), flush=True)
+        dist.barrier()
     if world >= 2:
         torch.cuda.synchronize()
         dist.barrier()
