@@ -464,7 +464,7 @@ int torus_comm_trace(torus_comm_t c, unsigned long long* host, size_t bytes) {
 
 int torus_probe(torus_comm_t c, int mode, size_t bytes, int iters, int ctas, unsigned long long* ns_out,
                 torus_stream_t stream) {
-  if (!c || c->virt || mode < 0 || mode > 7) return fail(TORUS_ERR_INVALID_ARG, "probe args");
+  if (!c || c->virt || mode < 0 || mode > 9) return fail(TORUS_ERR_INVALID_ARG, "probe args");
   const size_t room = c->slab_size - c->layout.data_off;
   if (mode != 2 && (bytes == 0 || (bytes / 16) * 16 * (size_t)(c->world + 1) > room))
     return fail(TORUS_ERR_INVALID_ARG, "probe bytes %zu exceed the slab", bytes);
@@ -475,7 +475,7 @@ int torus_probe(torus_comm_t c, int mode, size_t bytes, int iters, int ctas, uns
   const unsigned long long off = mode == 2 ? c->layout.bar_off + 4096 : c->layout.data_off;
   cudaError_t e = launch_probe(c->d_ranks, off, bytes, mode, iters,
                                ctas > 0 ? ctas : c->G, d_out, s);
-  if (e == cudaSuccess && ns_out && (mode == 6 || mode == 7))
+  if (e == cudaSuccess && ns_out && mode >= 6)
     e = cudaMemcpyAsync(d_out, static_cast<char*>(c->own_slabs[0]) + c->layout.bar_off + 8192, 8,
                         cudaMemcpyDeviceToDevice, s);
   if (e == cudaSuccess && ns_out) e = cudaMemcpyAsync(ns_out, d_out, 8, cudaMemcpyDeviceToHost, s);

@@ -1351,12 +1351,32 @@ __global__ void __launch_bounds__(512) probe_kernel(const RankDev* ranks, unsign
 constexpr int kTmaChunk = 16384;
 constexpr int kTmaStages = 8;
 
-__global__ void __launch_bounds__(32) tma_probe_kernel(const RankDev* ranks, unsigned long long data_off,
+__global__ void __launch_bounds__(64) tma_probe_kernel(const RankDev* ranks, unsigned long long data_off,
                                                       unsigned long long bytes, int mode) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTmaStages * kTmaChunk);
   const RankDev* R = ranks;
   const int N = R->N, me = R->rank, G = gridDim.x, b = blockIdx.x;
+  if (mode == 8 || mode == 9) {
+    // fence latency inside a CTA whose warp 0 streams TMA (8: pushes, 9: pulls):
+    // warp 1 lane 0 of CTA 0 times fences while its sibling warp keeps traffic in flight
+    if (threadIdx.x == 32) {
+      if (b == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < 100; ++i) {
+          const unsigned long long t0 = gtimer();
+          asm volatile("fence.acq_rel.sys;" ::: "memory");
+          t += gtimer() - t0;
+          const unsigned long long w0 = gtimer();
+          while (gtimer() - w0 < 2000) {}
+        }
+        *reinterpret_cast<unsigned long long*>(R->ws[me] + data_off - 65536 + 8192) = t / 100;
+      }
+      return;
+    }
+    if (threadIdx.x != 0) return;
+    mode = mode == 8 ? 4 : 5;
+  }
   if (threadIdx.x != 0) return;
   if (mode == 6 || mode == 7) {
     // fence.acq_rel.sys latency: CTA 0 times 200 fences (mode 6: while the other CTAs
@@ -1418,11 +1438,11 @@ __global__ void __launch_bounds__(32) tma_probe_kernel(const RankDev* ranks, uns
 
 cudaError_t launch_probe(const RankDev* ranks, unsigned long long data_off, unsigned long long bytes,
                          int mode, int iters, int ctas, unsigned long long* out, cudaStream_t stream) {
-  if (mode >= 4 && mode <= 7) {
+  if (mode >= 4 && mode <= 9) {
     const int smem = kTmaStages * kTmaChunk + kTmaStages * 8;
     cudaError_t e = cudaFuncSetAttribute(tma_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    tma_probe_kernel<<<ctas, 32, smem, stream>>>(ranks, data_off, bytes, mode);
+    tma_probe_kernel<<<ctas, mode >= 8 ? 64 : 32, smem, stream>>>(ranks, data_off, bytes, mode);
     return cudaGetLastError();
   }
   probe_kernel<<<mode == 2 ? 1 : ctas, 512, 0, stream>>>(ranks, data_off, bytes, mode, iters, out);

@@ -76,7 +76,7 @@ class _CommBase:
         """Calibration probe (torus_probe); returns ns for mode 2, else 0 (time it yourself)."""
         ns = ctypes.c_ulonglong(0)
         check(_lib.load().torus_probe(self._comm, mode, nbytes, iters, ctas,
-                                      ctypes.byref(ns) if mode in (2, 6, 7) else None,
+                                      ctypes.byref(ns) if mode in (2, 6, 7, 8, 9) else None,
                                       _stream_ptr(stream)), "torus_probe")
         return ns.value
 

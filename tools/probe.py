@@ -23,7 +23,10 @@ def main():
     s = torch.cuda.current_stream()
     nbytes = 51_114_064 * 2 * (world - 1) // world // 16 * 16  # 2(N-1)/N * S
     out = []
+    only = os.environ.get("PROBE_ONLY")
     for mode, name in ((0, "push"), (1, "pull"), (4, "tma_push"), (5, "tma_pull"), (3, "local_copy")):
+        if only and name not in only.split(","):
+            continue
         for ctas in ((16, 32, 64, 148, 296) if mode < 4 else (16, 32, 64, 148)):
             for _ in range(3):
                 comm.probe(mode, nbytes, ctas=ctas)
@@ -44,7 +47,7 @@ def main():
             if rank == 0:
                 print(json.dumps(rec), flush=True)
             dist.barrier()
-    for mode, name in ((7, "fence_quiet"), (6, "fence_under_tma_push")):
+    for mode, name in ((7, "fence_quiet"), (6, "fence_under_tma_push"), (8, "fence_in_cta_pushing"), (9, "fence_in_cta_pulling")):
         torch.cuda.synchronize()
         dist.barrier()
         ns = comm.probe(mode, nbytes, ctas=148)
