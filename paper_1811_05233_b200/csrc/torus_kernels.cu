@@ -677,25 +677,25 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
 // the TMA-staged torus kernel (product path)
 // ------------------------------------------------------------------------------------
 // Same wavefront and flag protocol as torus_kernel (stage p of iteration it works on
-// tile it - 2p), with every bulk transfer done by TMA (cp.async.bulk) and four roles
-// that only meet at per-buffer mbarriers:
-//   warp 0      control: polls the iteration's input flags (ld.acquire.sys), releases
-//               the producer (READY), and once the storer reports the iteration's stores
-//               complete (DONE) raises the output flags behind one fence.acq_rel.sys
-//   warp 1      producer (lane 0): streams every operand -- my user buffer, my h_in /
-//               v_in slots, the peers' chunk slots over NVLink -- into a ring of shared
-//               memory buffers (full[b]: complete_tx; waits empty[b])
-//   warp 2      storer (lane 0): per job, waits until the consumers are done with the
-//               buffers (consumed[b]) or the data landed (full[b], pure copies), issues
-//               the TMA stores (pushes into peers' h_in / v_in, my chunk slot), releases
-//               buffers (empty[b]) once their store has read them, and drains every
-//               iteration's stores (bulk async-groups) before reporting DONE
-//   warps 3-15  consumers: fold operands out of shared memory in ring order (f32
-//               accumulation), apply the mean, round once, stage results in
-//               shared memory and write the user buffer (wire->dtype cast fused)
+// tile it - 2p), with every bulk transfer -- reads AND writes of the user buffer, the
+// workspace slots and the peers' slots over NVLink -- done by TMA (cp.async.bulk)
+// through a ring of shared-memory buffers.  Keeping ordinary st.global traffic out of
+// the CTA keeps the system-scope fence behind every flag at ~1.3 us (measured; with
+// thousands of in-flight st.global it took 5-9 us).  Roles, meeting only at mbarriers
+// (full[b] / consumed[b] / empty[b] per buffer) and two shared-memory counters:
+//   warp 0      control: polls the iteration's input flags (ld.acquire.sys), posts
+//               s_ready, waits until the storer posts the iteration's stores complete
+//               (s_done) and raises the output flags behind one fence.acq_rel.sys
+//   warp 1      producer (lane 0): TMA-loads every job's operands into ring buffers
+//   warp 2      storers (lanes 0/1, alternating iterations so one drains while the other
+//               works): after the consumers sign off a job, TMA-store its results,
+//               release buffers once read, drain the iteration's bulk groups, post s_done
+//   warps 3-15  consumers: folds (ring order, f32 accumulation, mean, one rounding) and
+//               dtype<->wire casts from shared memory into shared memory; scalar
+//               st/ld.global only for a ragged last vector or an unaligned user buffer
 constexpr int kConsWarps = kThreads / 32 - 3;  // warps 3..15
 constexpr int kCons = kConsWarps * 32;
-constexpr int kStoreLag = 4;                    // bulk groups in flight before a release
+constexpr int kStoreLag = 3;                    // bulk groups in flight per storer lane
 
 struct Job {
   int kind;
@@ -703,12 +703,6 @@ struct Job {
   Piece p;
 };
 
-__device__ __forceinline__ void bar_sync_n(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive_n(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -723,11 +717,12 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
   constexpr int VE = Wire<W>::VE;
   constexpr int SW = kVecBytes / VE;
   constexpr int ST = (int)sizeof(UT);
+  constexpr bool kCast = DT != W;
 
   extern __shared__ __align__(1024) unsigned char smem[];
   const int NB = a.nbufs;
   const int TV = a.tile_vecs;
-  const unsigned PB = (unsigned)TV * VE * (ST > SW ? ST : SW);  // one piece, user or wire layout
+  const unsigned PB = (unsigned)TV * VE * (ST > SW ? ST : SW);  // one piece, user or wire
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NB * PB);
   uint64_t* empty = full + NB;
   uint64_t* consumed = empty + NB;
@@ -745,13 +740,13 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
 
   __shared__ uint32_t s_seq;
   __shared__ int s_abort;
-  __shared__ int s_ready;  // control -> producer: iterations whose inputs are visible
-  __shared__ int s_done;   // storer -> control: iterations whose stores are complete
+  __shared__ int s_ready;    // control -> producer: iterations whose inputs are visible
+  __shared__ int s_done[2];  // storer lane it&1 -> control: iterations whose stores completed
   if (tid == 0) {
     s_seq = R->epoch[b];
     s_abort = 0;
     s_ready = 0;
-    s_done = 0;
+    s_done[0] = s_done[1] = 0;
     for (int i = 0; i < NB; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -810,35 +805,34 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
       }
     }
   };
-  // Vectors of a piece whose user-buffer side can go through TMA (16-byte aligned full
-  // vectors); a ragged last vector is handled by the consumers with scalar accesses.
-  auto user_tma_vecs = [&](const Job& jb) -> unsigned long long {
+  // Leading vectors of a piece whose user-buffer side moves by TMA (full 16-byte-aligned
+  // vectors); a ragged last vector, or all of an unaligned buffer, goes through registers.
+  auto nut_of = [&](const Job& jb) -> unsigned long long {
     if (!aligned) return 0;
-    const unsigned long long nv = jb.p.p1 - jb.p.p0;
     const unsigned long long last_el = jb.p.so + (jb.p.p1 - 1) * VE;
-    return (last_el + VE > jb.p.cl) ? nv - 1 : nv;
+    return (last_el + VE > jb.p.cl) ? jb.p.p1 - jb.p.p0 - 1 : jb.p.p1 - jb.p.p0;
   };
-  // Buffer plan of a job: [TMA loads ...][user piece?][scratch?]
-  //   A: user (if TMA) + scratch when consumers must touch it (cast / ragged / unaligned)
-  //   B: X-1 h_in loads + user (if TMA) + scratch      C: Y v_in loads + scratch
-  //   D, E: one peer chunk load
-  auto wire_loads = [&](const Job& jb) -> int {
-    return jb.kind == kB ? X - 1 : jb.kind == kC ? Y : (jb.kind == kA ? 0 : 1);
+  // Buffer plan: [wire loads (nw)][user load?][scratch (wire result)?][ustage (f32)?]
+  struct Plan {
+    int nw, ul, sc, us, nb;
+    bool cons;  // consumers have work
   };
-  auto has_user_load = [&](const Job& jb) -> bool {
-    return (jb.kind == kA || jb.kind == kB) && user_tma_vecs(jb) > 0;
+  auto plan_of = [&](const Job& jb) -> Plan {
+    Plan pl;
+    const unsigned long long nv = jb.p.p1 - jb.p.p0, nut = nut_of(jb);
+    const bool ragged = nut < nv;
+    const bool reads_user = jb.kind == kA || jb.kind == kB;
+    const bool writes_user = jb.kind == kC || jb.kind == kD || jb.kind == kE || (jb.kind == kB && Y == 1);
+    pl.nw = jb.kind == kB ? X - 1 : jb.kind == kC ? Y : (jb.kind == kA ? 0 : 1);
+    pl.ul = (reads_user && nut > 0) ? 1 : 0;
+    pl.sc = (jb.kind == kB || jb.kind == kC || (jb.kind == kA && (kCast || ragged))) ? 1 : 0;
+    pl.us = (kCast && writes_user && nut > 0) ? 1 : 0;
+    pl.nb = pl.nw + pl.ul + pl.sc + pl.us;
+    pl.cons = jb.kind == kB || jb.kind == kC || kCast || ragged;
+    return pl;
   };
-  // A is a pure copy (no consumer work) when the whole piece moves by TMA unchanged.
-  auto a_is_copy = [&](const Job& jb) -> bool {
-    return DT == W && user_tma_vecs(jb) == jb.p.p1 - jb.p.p0;
-  };
-  auto has_scratch = [&](const Job& jb) -> bool {
-    if (jb.kind == kA) return !a_is_copy(jb);
-    return jb.kind == kB || jb.kind == kC;
-  };
-  auto consumer_work = [&](const Job& jb) -> bool { return !(jb.kind == kA && a_is_copy(jb)); };
-  auto nbufs_of = [&](const Job& jb) -> int {
-    return wire_loads(jb) + (has_user_load(jb) ? 1 : 0) + (has_scratch(jb) ? 1 : 0);
+  auto user_ptr = [&](const Job& jb) -> char* {
+    return reinterpret_cast<char*>(buf) + (a.buf_off + jb.p.co + jb.p.so + jb.p.p0 * VE) * ST;
   };
 
   if (warp == 0) {
@@ -912,65 +906,69 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
         });
       }
     };
-    unsigned long long* const tr = (lane == 0 && lr == 0) ? a.trace : nullptr;
-    bool aborted = false;
-    for (int it = 0; it < iters; ++it) {
-      stamp(tr, b, it, 0);
-      if (!poll_iter(it)) {  // watchdog: poison; the producer walks the rest without loads
-        if (lane == 0) {
-          atomicExch_system(R->err, kErrTimeout);
-          s_abort = 1;
-          st_release_cta(&s_ready, iters);
-        }
-        __syncwarp();
-        aborted = true;
-        break;
+    auto wait_done = [&](int it) -> bool {  // storer finished iteration it (watchdog)
+      unsigned spin = 0;
+      while (ld_acquire_cta(&s_done[it & 1]) <= it) {
+        if ((++spin & 255u) == 0 && gtimer() > deadline) return false;
       }
+      return true;
+    };
+    unsigned long long* const tr = (lane == 0 && lr == 0) ? a.trace : nullptr;
+    bool ok = true;
+    for (int it = 0; it < iters && ok; ++it) {
+      stamp(tr, b, it, 0);
+      ok = poll_iter(it);
       stamp(tr, b, it, 1);
+      if (!ok) break;
       if (lane == 0) st_release_cta(&s_ready, it + 1);  // producer may load iteration it
       __syncwarp();
       stamp(tr, b, it, 3);
       if (it > 0) {
-        while (ld_acquire_cta(&s_done) < it) {}      // iteration it-1's stores complete
+        ok = __all_sync(0xffffffffu, wait_done(it - 1));
+        if (!ok) break;
         stamp(tr, b, it, 2);
         raise_iter(it - 1);
         stamp(tr, b, it, 4);
       }
     }
-    if (!aborted) {
-      while (ld_acquire_cta(&s_done) < iters) {}
+    if (ok) ok = __all_sync(0xffffffffu, wait_done(iters - 1));
+    if (ok) {
       raise_iter(iters - 1);
+    } else {  // watchdog: poison the call; the producer walks the rest without loads
+      if (lane == 0) {
+        atomicExch_system(R->err, kErrTimeout);
+        s_abort = 1;
+        st_release_cta(&s_ready, iters);
+      }
+      __syncwarp();
     }
   } else if (warp == 1) {
     // =============================== producer warp ==============================
-    int slot = 0;
-    bool aborted = false;
-    for (int it = 0; it < iters; ++it) {
-      if (lane == 0) {
+    if (lane == 0) {
+      int slot = 0;
+      bool aborted = false;
+      for (int it = 0; it < iters; ++it) {
         if (!aborted) {
           while (ld_acquire_cta(&s_ready) <= it) {}
           aborted = *(volatile int*)&s_abort != 0;
         }
         fence_proxy_async();  // data the control warp acquired -> async-proxy loads
         for_jobs(it, [&](const Job& jb) {
-          const int nw = wire_loads(jb);
-          const bool ul = has_user_load(jb);
-          const int nbj = nbufs_of(jb);
+          const Plan pl = plan_of(jb);
           const unsigned wbytes = (unsigned)((jb.p.p1 - jb.p.p0) * kVecBytes);
-          for (int o = 0; o < nbj; ++o, ++slot) {
+          for (int o = 0; o < pl.nb; ++o, ++slot) {
             const int bi = slot % NB;
             mbar_wait(&empty[bi], ((slot / NB) & 1) ^ 1);
-            const bool is_user = ul && o == nw;
-            if (aborted || o > nw || (o == nw && !ul)) {  // scratch / poisoned: no data
+            const bool is_wire = o < pl.nw, is_user = pl.ul && o == pl.nw;
+            if (aborted || !(is_wire || is_user)) {  // scratch / staging / poisoned call
               mbar_arrive(&full[bi]);
               continue;
             }
             const char* src;
             unsigned bytes = wbytes;
             if (is_user) {
-              bytes = (unsigned)(user_tma_vecs(jb) * VE * ST);
-              src = reinterpret_cast<const char*>(buf) +
-                    (a.buf_off + jb.p.co + jb.p.so + jb.p.p0 * VE) * ST;
+              bytes = (unsigned)(nut_of(jb) * VE * ST);
+              src = user_ptr(jb);
             } else if (jb.kind == kB) {  // h_in slot of source column (c+1+o) % X
               src = myws + a.hin_off + (size_t)((c + 1 + o) % X) * a.hin_stride +
                     (jb.p.so + jb.p.p0 * VE) * SW;
@@ -987,58 +985,88 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
           }
         });
       }
-      __syncwarp();
     }
   } else if (warp == 2) {
-    // =============================== storer warp ================================
-    int slot = 0;
-    int relq[8];
-    int rq_head = 0, rq_tail = 0;
-    for (int it = 0; it < iters; ++it) {
-      if (lane == 0) {
+    // =============================== storer lanes ===============================
+    if (lane < 2) {
+      const int L = lane;      // this lane serves iterations with it % 2 == L
+      int slot = 0;
+      int relq[8];
+      int rq_head = 0, rq_tail = 0;
+      auto release_read = [&](bool all) {
+        if (all) {
+          tma_wait_read<0>();
+          while (rq_head < rq_tail) mbar_arrive(&empty[relq[rq_head++ & 7]]);
+        } else if (rq_tail - rq_head > kStoreLag) {
+          tma_wait_read<kStoreLag>();
+          while (rq_tail - rq_head > kStoreLag) mbar_arrive(&empty[relq[rq_head++ & 7]]);
+        }
+      };
+      for (int it = 0; it < iters; ++it) {
+        const bool mine = (it & 1) == L;
         for_jobs(it, [&](const Job& jb) {
-          const int b0 = slot, nbj = nbufs_of(jb);
-          slot += nbj;
-          const int last = (b0 + nbj - 1) % NB;
-          const unsigned long long nv = jb.p.p1 - jb.p.p0;
-          for (int o = 0; o < nbj; ++o) mbar_wait(&consumed[(b0 + o) % NB], ((b0 + o) / NB) & 1);
-          // the buffer a TMA store reads and where it goes
-          int src_b = -1;
-          char* dst = nullptr;
-          if (jb.kind == kA) {
-            src_b = last;  // pure copy: the user piece itself; else the cast scratch
-            dst = R->ws[rho * X + jb.j] + a.hin_off + (size_t)c * a.hin_stride +
-                  (jb.p.so + jb.p.p0 * VE) * SW;
+          const Plan pl = plan_of(jb);
+          const int b0 = slot;
+          slot += pl.nb;
+          if (!mine) return;
+          for (int o = 0; o < pl.nb; ++o) mbar_wait(&consumed[(b0 + o) % NB], ((b0 + o) / NB) & 1);
+          const bool live = *(volatile int*)&s_abort == 0;
+          const unsigned long long nv = jb.p.p1 - jb.p.p0, nut = nut_of(jb);
+          const unsigned wbytes = (unsigned)(nv * kVecBytes);
+          const unsigned ubytes = (unsigned)(nut * VE * ST);
+          // the wire result of the job (the buffer a wire-side store reads)
+          const int wbuf = (jb.kind == kA) ? (b0 + (pl.sc ? pl.nw + pl.ul : pl.nw)) % NB
+                         : (jb.kind == kB || jb.kind == kC) ? (b0 + pl.nw + pl.ul) % NB
+                         : b0 % NB;
+          // the user-layout data a user-side store reads
+          const int ubuf = pl.us ? (b0 + pl.nb - 1) % NB : wbuf;
+          int src1 = -1, src2 = -1;
+          if (jb.kind == kA) {  // push my share into (rho, j).h_in[c]
+            src1 = wbuf;
+            if (live)
+              tma_store(R->ws[rho * X + jb.j] + a.hin_off + (size_t)c * a.hin_stride +
+                            (jb.p.so + jb.p.p0 * VE) * SW,
+                        smem + (size_t)wbuf * PB, wbytes);
           } else if (jb.kind == kB && Y > 1) {  // P1 -> v_in[rho] of sub-chunk owner (s, c)
-            src_b = last;
-            dst = R->ws[jb.s * X + c] + a.vin_off + (size_t)rho * a.vin_stride + jb.p.p0 * VE * SW;
-          } else if ((jb.kind == kB && X > 1) || jb.kind == kC || (jb.kind == kD && X > 1)) {
-            src_b = last;  // final values -> my chunk slot, pulled by row / column peers
-            dst = myws + a.chunk_off + (jb.p.so + jb.p.p0 * VE) * SW;
-          }
-          for (int o = 0; o < nbj; ++o) {
-            const int bi = (b0 + o) % NB;
-            if (bi != src_b) mbar_arrive(&empty[bi]);
-          }
-          if (src_b >= 0) {
-            if (!*(volatile int*)&s_abort)
-              tma_store(dst, smem + (size_t)src_b * PB, (unsigned)(nv * kVecBytes));
-            tma_commit();
-            relq[rq_tail++ & 7] = src_b;
-            if (rq_tail - rq_head > kStoreLag) {
-              tma_wait_read<kStoreLag>();
-              while (rq_tail - rq_head > kStoreLag) mbar_arrive(&empty[relq[rq_head++ & 7]]);
+            src1 = wbuf;
+            if (live)
+              tma_store(R->ws[jb.s * X + c] + a.vin_off + (size_t)rho * a.vin_stride +
+                            jb.p.p0 * VE * SW,
+                        smem + (size_t)wbuf * PB, wbytes);
+          } else {
+            // final values: my chunk slot (pulled by peers) and my user buffer
+            const bool to_chunk = (jb.kind == kB && X > 1) || jb.kind == kC || (jb.kind == kD && X > 1);
+            if (to_chunk) {
+              src1 = wbuf;
+              if (live)
+                tma_store(myws + a.chunk_off + (jb.p.so + jb.p.p0 * VE) * SW,
+                          smem + (size_t)wbuf * PB, wbytes);
+            }
+            if (nut > 0) {
+              src2 = ubuf;
+              if (live) tma_store(user_ptr(jb), smem + (size_t)ubuf * PB, ubytes);
             }
           }
+          for (int o = 0; o < pl.nb; ++o) {
+            const int bi = (b0 + o) % NB;
+            if (bi != src1 && bi != src2) mbar_arrive(&empty[bi]);
+          }
+          if (src1 >= 0 || src2 >= 0) {
+            tma_commit();  // one bulk group per job
+            if (src1 >= 0) relq[rq_tail++ & 7] = src1;
+            if (src2 >= 0 && src2 != src1) relq[rq_tail++ & 7] = src2;
+            release_read(false);
+          }
         });
-        // every store of iteration it must be complete before its flags are raised
-        tma_wait_all<0>();
-        fence_proxy_async();
-        while (rq_head < rq_tail) mbar_arrive(&empty[relq[rq_head++ & 7]]);
-        st_release_cta(&s_done, it + 1);
-        stamp(lr == 0 ? a.trace : nullptr, b, it, 7);
+        if (mine) {
+          // every store of iteration it is complete (writes performed) before its flags
+          tma_wait_all<0>();
+          fence_proxy_async();
+          release_read(true);
+          st_release_cta(&s_done[L], it + 1);
+          stamp(lr == 0 ? a.trace : nullptr, b, it, 7);
+        }
       }
-      __syncwarp();
     }
   } else {
     // =============================== consumer warps =============================
@@ -1048,77 +1076,82 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
     for (int it = 0; it < iters; ++it) {
       stamp(tr, b, it, 5);
       for_jobs(it, [&](const Job& jb) {
-        const int b0 = slot, nbj = nbufs_of(jb);
-        slot += nbj;
-        // Every buffer's full / consumed / empty barriers advance exactly once per use, so
+        const Plan pl = plan_of(jb);
+        const int b0 = slot;
+        slot += pl.nb;
+        // Every buffer's full / consumed / empty barriers advance exactly once per use:
         // the consumers wait for and sign off every buffer of every job, even pure copies.
-        for (int o = 0; o < nbj; ++o) mbar_wait(&full[(b0 + o) % NB], ((b0 + o) / NB) & 1);
-        auto sign_off = [&]() {
-          fence_proxy_async_smem();  // staged results -> the storer's async-proxy reads
-          __syncwarp();
-          if (lane == 0)
-            for (int o = 0; o < nbj; ++o) mbar_arrive(&consumed[(b0 + o) % NB]);
-        };
-        if (!consumer_work(jb)) {
-          sign_off();
-          return;
-        }
-        const bool write_user = *(volatile int*)&s_abort == 0;  // a poisoned call leaves it
-        const int nw = wire_loads(jb);
-        const bool ul = has_user_load(jb);
-        const unsigned long long nv = jb.p.p1 - jb.p.p0;
-        const unsigned long long nut = user_tma_vecs(jb);
-        const unsigned char* const ubuf = smem + (size_t)((b0 + nw) % NB) * PB;  // user piece
-        unsigned char* const out = smem + (size_t)((b0 + nbj - 1) % NB) * PB;     // last buffer
-        // my user-buffer vector v of the piece, converted to the wire type
-        auto user_vec = [&](unsigned long long v, unsigned long long el, int nrem) -> uint4 {
-          if (ul && v < nut) {
-            if constexpr (DT == W) {
-              return *reinterpret_cast<const uint4*>(ubuf + v * kVecBytes);
-            } else {
-              const float* f = reinterpret_cast<const float*>(ubuf + v * VE * ST);
-              float t[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) t[i] = f[i];
-              return pack<W>(t);
-            }
-          }
-          return load_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem, aligned);
-        };
-        for (unsigned long long v = ct; v < nv; v += kCons) {
-          const unsigned long long el = jb.p.so + (jb.p.p0 + v) * VE;
-          const int nrem = (int)min((unsigned long long)VE, jb.p.cl - el);
-          if (jb.kind == kA) {
-            *reinterpret_cast<uint4*>(out + v * kVecBytes) = user_vec(v, el, nrem);
-          } else if (jb.kind == kB || jb.kind == kC) {
-            const int nops = (jb.kind == kB) ? X : Y;
-            Acc acc[VE];
-            for (int k = 0; k < nops; ++k) {  // ring order; my own contribution last in B
-              const uint4 w = (jb.kind == kB && k == X - 1)
-                                  ? user_vec(v, el, nrem)
-                                  : *reinterpret_cast<const uint4*>(smem + (size_t)((b0 + k) % NB) * PB +
-                                                                    v * kVecBytes);
-              Acc t[VE];
-              unpack<W>(w, t);
-              if (k == 0) {
-#pragma unroll
-                for (int i = 0; i < VE; ++i) acc[i] = t[i];
+        for (int o = 0; o < pl.nb; ++o) mbar_wait(&full[(b0 + o) % NB], ((b0 + o) / NB) & 1);
+        if (pl.cons) {
+          const bool live = *(volatile int*)&s_abort == 0;
+          const unsigned long long nv = jb.p.p1 - jb.p.p0, nut = nut_of(jb);
+          const unsigned char* const uin = smem + (size_t)((b0 + pl.nw) % NB) * PB;    // user load
+          unsigned char* const wout =                                                  // wire result
+              smem + (size_t)((jb.kind == kD || jb.kind == kE) ? b0 % NB : (b0 + pl.nw + pl.ul) % NB) * PB;
+          unsigned char* const uout = smem + (size_t)((b0 + pl.nb - 1) % NB) * PB;      // f32 staging
+          auto user_in = [&](unsigned long long v, unsigned long long el, int nrem) -> uint4 {
+            if (v < nut) {
+              if constexpr (!kCast) {
+                return *reinterpret_cast<const uint4*>(uin + v * kVecBytes);
               } else {
-                acc_add<W>(acc, t);
+                const float* f = reinterpret_cast<const float*>(uin + v * VE * ST);
+                float t[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) t[i] = f[i];
+                return pack<W>(t);
               }
             }
-            const bool last_reduce = (jb.kind == kC) || (Y == 1);
-            if (last_reduce && a.op == 1) acc_mean<W>(acc, a.inv_n, N);
-            const uint4 o = pack<W>(acc);
-            *reinterpret_cast<uint4*>(out + v * kVecBytes) = o;
-            if (last_reduce && write_user)
-              store_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem, o, aligned);
-          } else if (write_user) {  // D / E: pulled wire data -> my user buffer
-            store_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem,
-                              *reinterpret_cast<const uint4*>(out + v * kVecBytes), aligned);
+            return load_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem, aligned);
+          };
+          auto user_out = [&](unsigned long long v, unsigned long long el, int nrem, uint4 w) {
+            if (v < nut) {
+              if constexpr (kCast) {
+                float f[8];
+                unpack<W>(w, f);
+                float4* d = reinterpret_cast<float4*>(uout + v * VE * ST);
+                d[0] = make_float4(f[0], f[1], f[2], f[3]);
+                d[1] = make_float4(f[4], f[5], f[6], f[7]);
+              }  // same dtype: the TMA store reads the wire result directly
+            } else if (live) {
+              store_user<DT, W>(buf, a.buf_off + jb.p.co + el, nrem, w, aligned);
+            }
+          };
+          for (unsigned long long v = ct; v < nv; v += kCons) {
+            const unsigned long long el = jb.p.so + (jb.p.p0 + v) * VE;
+            const int nrem = (int)min((unsigned long long)VE, jb.p.cl - el);
+            if (jb.kind == kA) {
+              *reinterpret_cast<uint4*>(wout + v * kVecBytes) = user_in(v, el, nrem);
+            } else if (jb.kind == kB || jb.kind == kC) {
+              const int nops = (jb.kind == kB) ? X : Y;
+              Acc acc[VE];
+              for (int k = 0; k < nops; ++k) {  // ring order; my own contribution last in B
+                const uint4 w = (jb.kind == kB && k == X - 1)
+                                    ? user_in(v, el, nrem)
+                                    : *reinterpret_cast<const uint4*>(smem + (size_t)((b0 + k) % NB) * PB +
+                                                                      v * kVecBytes);
+                Acc t[VE];
+                unpack<W>(w, t);
+                if (k == 0) {
+#pragma unroll
+                  for (int i = 0; i < VE; ++i) acc[i] = t[i];
+                } else {
+                  acc_add<W>(acc, t);
+                }
+              }
+              const bool last_reduce = (jb.kind == kC) || (Y == 1);
+              if (last_reduce && a.op == 1) acc_mean<W>(acc, a.inv_n, N);
+              const uint4 o = pack<W>(acc);
+              *reinterpret_cast<uint4*>(wout + v * kVecBytes) = o;
+              if (last_reduce) user_out(v, el, nrem, o);
+            } else {  // D / E: pulled wire data -> my user buffer
+              user_out(v, el, nrem, *reinterpret_cast<const uint4*>(wout + v * kVecBytes));
+            }
           }
+          fence_proxy_async_smem();  // staged results -> the storers' async-proxy reads
         }
-        sign_off();
+        __syncwarp();
+        if (lane == 0)
+          for (int o = 0; o < pl.nb; ++o) mbar_arrive(&consumed[(b0 + o) % NB]);
       });
       stamp(tr, b, it, 6);
     }
