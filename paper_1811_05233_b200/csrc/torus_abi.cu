@@ -546,11 +546,11 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   a.trace = c->d_trace;
   a.nbufs = 0;
   if (c->tma) {
-    // ring buffers of one piece each: the largest job holds max(X,Y)+3 at once, each of
-    // the two storer lanes keeps up to kStoreLag(3)+2 in flight; shrink the piece until
-    // that fits with slack
+    // ring buffers of one piece each: jobs in flight across the producer, the consumers
+    // and the 8 storer lanes; the largest job holds max(X,Y)+3 at once -- keep room for
+    // a few of those so the producer runs ahead
     const int ratio = (int)(wire_size(dtype) / sw);
-    const int need = std::max(c->X, c->Y) + 3 + 2 * (3 + 2) + 2;
+    const int need = 3 * (std::max(c->X, c->Y) + 3) + 4;
     int tv = a.tile_vecs;
     while (tv > 32 && kTmaSmemMax / (tma_buf_bytes(tv, ratio) + 24) < need) tv /= 2;
     a.tile_vecs = tv;

@@ -683,19 +683,21 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
 // the CTA keeps the system-scope fence behind every flag at ~1.3 us (measured; with
 // thousands of in-flight st.global it took 5-9 us).  Roles, meeting only at mbarriers
 // (full[b] / consumed[b] / empty[b] per buffer) and two shared-memory counters:
-//   warp 0      control: polls the iteration's input flags (ld.acquire.sys), posts
-//               s_ready, waits until the storer posts the iteration's stores complete
-//               (s_done) and raises the output flags behind one fence.acq_rel.sys
+//   warp 0      poller: waits for the iteration's input flags (ld.acquire.sys) and posts
+//               s_ready; it never waits on this CTA's own stores or fences
 //   warp 1      producer (lane 0): TMA-loads every job's operands into ring buffers
-//   warp 2      storers (lanes 0/1, alternating iterations so one drains while the other
-//               works): after the consumers sign off a job, TMA-store its results,
-//               release buffers once read, drain the iteration's bulk groups, post s_done
-//   warps 3-15  consumers: folds (ring order, f32 accumulation, mean, one rounding) and
+//   warp 2      storers (lanes 0..kStorers-1, jobs dealt round-robin): after the
+//               consumers sign off a job, TMA-store its results and free its buffers as
+//               soon as the stores have read them; at each iteration end drain the
+//               lane's bulk groups and post s_done[lane]
+//   warp 3      raiser: once every storer lane has drained iteration it, raise its output
+//               flags behind one fence.acq_rel.sys (off the throughput path)
+//   warps 4-15  consumers: folds (ring order, f32 accumulation, mean, one rounding) and
 //               dtype<->wire casts from shared memory into shared memory; scalar
 //               st/ld.global only for a ragged last vector or an unaligned user buffer
-constexpr int kConsWarps = kThreads / 32 - 3;  // warps 3..15
+constexpr int kConsWarps = kThreads / 32 - 4;  // warps 4..15
 constexpr int kCons = kConsWarps * 32;
-constexpr int kStoreLag = 3;                    // bulk groups in flight per storer lane
+constexpr int kStorers = 8;                     // storer lanes in warp 2
 
 struct Job {
   int kind;
@@ -741,12 +743,12 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
   __shared__ uint32_t s_seq;
   __shared__ int s_abort;
   __shared__ int s_ready;    // control -> producer: iterations whose inputs are visible
-  __shared__ int s_done[2];  // storer lane it&1 -> control: iterations whose stores completed
+  __shared__ int s_done[kStorers];  // storer lane -> raiser: iterations it has drained
   if (tid == 0) {
     s_seq = R->epoch[b];
     s_abort = 0;
     s_ready = 0;
-    s_done[0] = s_done[1] = 0;
+    for (int i = 0; i < kStorers; ++i) s_done[i] = 0;
     for (int i = 0; i < NB; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -835,8 +837,8 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
     return reinterpret_cast<char*>(buf) + (a.buf_off + jb.p.co + jb.p.so + jb.p.p0 * VE) * ST;
   };
 
-  if (warp == 0) {
-    // =============================== control warp ===============================
+  if (warp == 0 || warp == 3) {
+    // ========================== poller (0) and raiser (3) ==========================
     const unsigned long long deadline = gtimer() + a.timeout_ns;
     auto flagp = [&](char* ws, int kind, int src) -> uint32_t* {
       return reinterpret_cast<uint32_t*>(ws) + ((size_t)(kind * kMaxDim + src) * G + b);
@@ -906,41 +908,51 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
         });
       }
     };
-    auto wait_done = [&](int it) -> bool {  // storer finished iteration it (watchdog)
-      unsigned spin = 0;
-      while (ld_acquire_cta(&s_done[it & 1]) <= it) {
-        if ((++spin & 255u) == 0 && gtimer() > deadline) return false;
+    auto wait_done = [&](int it) -> bool {  // every storer lane drained iteration it
+      bool ok = true;
+      if (lane < kStorers) {
+        unsigned spin = 0;
+        while (ld_acquire_cta(&s_done[lane]) <= it) {
+          if ((++spin & 255u) == 0 && gtimer() > deadline) {
+            ok = false;
+            break;
+          }
+        }
       }
-      return true;
+      return __all_sync(0xffffffffu, ok);
     };
     unsigned long long* const tr = (lane == 0 && lr == 0) ? a.trace : nullptr;
-    bool ok = true;
-    for (int it = 0; it < iters && ok; ++it) {
-      stamp(tr, b, it, 0);
-      ok = poll_iter(it);
-      stamp(tr, b, it, 1);
-      if (!ok) break;
-      if (lane == 0) st_release_cta(&s_ready, it + 1);  // producer may load iteration it
-      __syncwarp();
-      stamp(tr, b, it, 3);
-      if (it > 0) {
-        ok = __all_sync(0xffffffffu, wait_done(it - 1));
-        if (!ok) break;
+    if (warp == 0) {
+      for (int it = 0; it < iters; ++it) {
+        stamp(tr, b, it, 0);
+        if (!poll_iter(it)) {  // watchdog: poison; the producer walks the rest without loads
+          if (lane == 0) {
+            atomicExch_system(R->err, kErrTimeout);
+            s_abort = 1;
+            st_release_cta(&s_ready, iters);
+          }
+          __syncwarp();
+          break;
+        }
+        stamp(tr, b, it, 1);
+        if (lane == 0) st_release_cta(&s_ready, it + 1);  // producer may load iteration it
+        __syncwarp();
+      }
+    } else {
+      for (int it = 0; it < iters; ++it) {
+        if (!wait_done(it)) {
+          if (lane == 0) {
+            atomicExch_system(R->err, kErrTimeout);
+            s_abort = 1;
+          }
+          __syncwarp();
+          break;
+        }
+        if (*(volatile int*)&s_abort) break;
         stamp(tr, b, it, 2);
-        raise_iter(it - 1);
+        raise_iter(it);
         stamp(tr, b, it, 4);
       }
-    }
-    if (ok) ok = __all_sync(0xffffffffu, wait_done(iters - 1));
-    if (ok) {
-      raise_iter(iters - 1);
-    } else {  // watchdog: poison the call; the producer walks the rest without loads
-      if (lane == 0) {
-        atomicExch_system(R->err, kErrTimeout);
-        s_abort = 1;
-        st_release_cta(&s_ready, iters);
-      }
-      __syncwarp();
     }
   } else if (warp == 1) {
     // =============================== producer warp ==============================
@@ -988,27 +1000,14 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
     }
   } else if (warp == 2) {
     // =============================== storer lanes ===============================
-    if (lane < 2) {
-      const int L = lane;      // this lane serves iterations with it % 2 == L
-      int slot = 0;
-      int relq[8];
-      int rq_head = 0, rq_tail = 0;
-      auto release_read = [&](bool all) {
-        if (all) {
-          tma_wait_read<0>();
-          while (rq_head < rq_tail) mbar_arrive(&empty[relq[rq_head++ & 7]]);
-        } else if (rq_tail - rq_head > kStoreLag) {
-          tma_wait_read<kStoreLag>();
-          while (rq_tail - rq_head > kStoreLag) mbar_arrive(&empty[relq[rq_head++ & 7]]);
-        }
-      };
+    if (lane < kStorers) {
+      int slot = 0, jobno = 0;
       for (int it = 0; it < iters; ++it) {
-        const bool mine = (it & 1) == L;
         for_jobs(it, [&](const Job& jb) {
           const Plan pl = plan_of(jb);
           const int b0 = slot;
           slot += pl.nb;
-          if (!mine) return;
+          if ((jobno++ % kStorers) != lane) return;
           for (int o = 0; o < pl.nb; ++o) mbar_wait(&consumed[(b0 + o) % NB], ((b0 + o) / NB) & 1);
           const bool live = *(volatile int*)&s_abort == 0;
           const unsigned long long nv = jb.p.p1 - jb.p.p0, nut = nut_of(jb);
@@ -1020,57 +1019,47 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
                          : b0 % NB;
           // the user-layout data a user-side store reads
           const int ubuf = pl.us ? (b0 + pl.nb - 1) % NB : wbuf;
-          int src1 = -1, src2 = -1;
-          if (jb.kind == kA) {  // push my share into (rho, j).h_in[c]
-            src1 = wbuf;
-            if (live)
+          bool stored = false;
+          if (live) {
+            if (jb.kind == kA) {  // push my share into (rho, j).h_in[c]
               tma_store(R->ws[rho * X + jb.j] + a.hin_off + (size_t)c * a.hin_stride +
                             (jb.p.so + jb.p.p0 * VE) * SW,
                         smem + (size_t)wbuf * PB, wbytes);
-          } else if (jb.kind == kB && Y > 1) {  // P1 -> v_in[rho] of sub-chunk owner (s, c)
-            src1 = wbuf;
-            if (live)
+              stored = true;
+            } else if (jb.kind == kB && Y > 1) {  // P1 -> v_in[rho] of sub-chunk owner (s, c)
               tma_store(R->ws[jb.s * X + c] + a.vin_off + (size_t)rho * a.vin_stride +
                             jb.p.p0 * VE * SW,
                         smem + (size_t)wbuf * PB, wbytes);
-          } else {
-            // final values: my chunk slot (pulled by peers) and my user buffer
-            const bool to_chunk = (jb.kind == kB && X > 1) || jb.kind == kC || (jb.kind == kD && X > 1);
-            if (to_chunk) {
-              src1 = wbuf;
-              if (live)
+              stored = true;
+            } else {
+              // final values: my chunk slot (pulled by peers) and my user buffer
+              if ((jb.kind == kB && X > 1) || jb.kind == kC || (jb.kind == kD && X > 1)) {
                 tma_store(myws + a.chunk_off + (jb.p.so + jb.p.p0 * VE) * SW,
                           smem + (size_t)wbuf * PB, wbytes);
+                stored = true;
+              }
+              if (nut > 0) {
+                tma_store(user_ptr(jb), smem + (size_t)ubuf * PB, ubytes);
+                stored = true;
+              }
             }
-            if (nut > 0) {
-              src2 = ubuf;
-              if (live) tma_store(user_ptr(jb), smem + (size_t)ubuf * PB, ubytes);
-            }
           }
-          for (int o = 0; o < pl.nb; ++o) {
-            const int bi = (b0 + o) % NB;
-            if (bi != src1 && bi != src2) mbar_arrive(&empty[bi]);
+          if (stored) {
+            tma_commit();
+            tma_wait_read<0>();  // the stores have read their shared-memory sources
           }
-          if (src1 >= 0 || src2 >= 0) {
-            tma_commit();  // one bulk group per job
-            if (src1 >= 0) relq[rq_tail++ & 7] = src1;
-            if (src2 >= 0 && src2 != src1) relq[rq_tail++ & 7] = src2;
-            release_read(false);
-          }
+          for (int o = 0; o < pl.nb; ++o) mbar_arrive(&empty[(b0 + o) % NB]);
         });
-        if (mine) {
-          // every store of iteration it is complete (writes performed) before its flags
-          tma_wait_all<0>();
-          fence_proxy_async();
-          release_read(true);
-          st_release_cta(&s_done[L], it + 1);
-          stamp(lr == 0 ? a.trace : nullptr, b, it, 7);
-        }
+        // this lane's stores of iteration it are complete before the raiser's fence
+        tma_wait_all<0>();
+        fence_proxy_async();
+        st_release_cta(&s_done[lane], it + 1);
+        if (lane == 0) stamp(lr == 0 ? a.trace : nullptr, b, it, 7);
       }
     }
   } else {
     // =============================== consumer warps =============================
-    const int ct = tid - 96;
+    const int ct = tid - 128;
     int slot = 0;
     unsigned long long* const tr = (ct == 0 && lr == 0) ? a.trace : nullptr;
     for (int it = 0; it < iters; ++it) {

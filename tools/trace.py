@@ -47,16 +47,12 @@ def main():
                           "kernel_span_us": float(rel[:, :iters, 6].max())}))
         for it in range(iters):
             r = rel[:, it, :]
-            d = {"it": it,
-                 "t_poll0": round(float(r[:, 0].mean()), 2),
-                 "poll": round(float((r[:, 1] - r[:, 0]).mean()), 2),
-                 "doneWait": round(float((r[:, 2] - r[:, 3]).mean()), 2) if it else 0,
-                 "raise": round(float((r[:, 4] - r[:, 2]).mean()), 2) if it else 0,
-                 "cons_start": round(float(r[:, 5].mean()), 2),
-                 "cons_busy": round(float((r[:, 6] - r[:, 5]).mean()), 2),
-                 "storer_done": round(float(r[:, 7].mean()), 2),
-                 "drain_after_cons": round(float((r[:, 7] - r[:, 6]).mean()), 2)}
-            print(json.dumps(d))
+            m = lambda x: round(float(x.mean()), 2)
+            print(json.dumps({
+                "it": it, "poll_start": m(r[:, 0]), "poll": m(r[:, 1] - r[:, 0]),
+                "cons_start": m(r[:, 5]), "cons_busy": m(r[:, 6] - r[:, 5]),
+                "storer_done": m(r[:, 7]), "done_after_cons": m(r[:, 7] - r[:, 6]),
+                "raiser_sees_done": m(r[:, 2] - r[:, 7]), "raise": m(r[:, 4] - r[:, 2])}))
     comm.destroy()
     dist.destroy_process_group()
 
