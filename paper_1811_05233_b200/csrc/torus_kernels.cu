@@ -683,21 +683,25 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
 // the CTA keeps the system-scope fence behind every flag at ~1.3 us (measured; with
 // thousands of in-flight st.global it took 5-9 us).  Roles, meeting only at mbarriers
 // (full[b] / consumed[b] / empty[b] per buffer) and two shared-memory counters:
-//   warp 0      poller: waits for the iteration's input flags (ld.acquire.sys) and posts
-//               s_ready; it never waits on this CTA's own stores or fences
+//   warp 0      poller: waits for the iteration's input flags (ld.acquire.sys) and for my
+//               own stores of iteration it-2 (stage C reads the v_in slot my stage B
+//               filled), then posts s_ready; never waits on a fence
 //   warp 1      producer (lane 0): TMA-loads every job's operands into ring buffers
-//   warp 2      storers (lanes 0..kStorers-1, jobs dealt round-robin): after the
-//               consumers sign off a job, TMA-store its results and free its buffers as
-//               soon as the stores have read them; at each iteration end drain the
-//               lane's bulk groups and post s_done[lane]
-//   warp 3      raiser: once every storer lane has drained iteration it, raise its output
+//   warps 2-5   storers (lane 0 each, jobs dealt round-robin): after the consumers sign
+//               off a job, TMA-store its results and free its buffers as soon as the
+//               stores have read them; at each iteration end drain the warp's bulk groups
+//               and post s_done[storer] (one warp each: a lane blocked in wait_group
+//               stalls its whole warp)
+//   warp 6      raiser: once every storer has drained iteration it, raise its output
 //               flags behind one fence.acq_rel.sys (off the throughput path)
-//   warps 4-15  consumers: folds (ring order, f32 accumulation, mean, one rounding) and
+//   warps 7-15  consumers: folds (ring order, f32 accumulation, mean, one rounding) and
 //               dtype<->wire casts from shared memory into shared memory; scalar
 //               st/ld.global only for a ragged last vector or an unaligned user buffer
-constexpr int kConsWarps = kThreads / 32 - 4;  // warps 4..15
+constexpr int kStorers = 4;                     // storer warps 2..5
+constexpr int kRaiserWarp = 2 + kStorers;       // warp 6
+constexpr int kConsWarp0 = kRaiserWarp + 1;     // consumers: warps 7..15
+constexpr int kConsWarps = kThreads / 32 - kConsWarp0;
 constexpr int kCons = kConsWarps * 32;
-constexpr int kStorers = 8;                     // storer lanes in warp 2
 
 struct Job {
   int kind;
@@ -837,8 +841,8 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
     return reinterpret_cast<char*>(buf) + (a.buf_off + jb.p.co + jb.p.so + jb.p.p0 * VE) * ST;
   };
 
-  if (warp == 0 || warp == 3) {
-    // ========================== poller (0) and raiser (3) ==========================
+  if (warp == 0 || warp == kRaiserWarp) {
+    // ========================== poller (0) and raiser (6) ==========================
     const unsigned long long deadline = gtimer() + a.timeout_ns;
     auto flagp = [&](char* ws, int kind, int src) -> uint32_t* {
       return reinterpret_cast<uint32_t*>(ws) + ((size_t)(kind * kMaxDim + src) * G + b);
@@ -934,6 +938,16 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
           __syncwarp();
           break;
         }
+        // my own stores of iteration it-2 (stage B's local v_in slot, read by stage C)
+        if (it >= 2 && !wait_done(it - 2)) {
+          if (lane == 0) {
+            atomicExch_system(R->err, kErrTimeout);
+            s_abort = 1;
+            st_release_cta(&s_ready, iters);
+          }
+          __syncwarp();
+          break;
+        }
         stamp(tr, b, it, 1);
         if (lane == 0) st_release_cta(&s_ready, it + 1);  // producer may load iteration it
         __syncwarp();
@@ -998,16 +1012,17 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
         });
       }
     }
-  } else if (warp == 2) {
-    // =============================== storer lanes ===============================
-    if (lane < kStorers) {
+  } else if (warp >= 2 && warp < 2 + kStorers) {
+    // =============================== storer warps ===============================
+    const int sw_id = warp - 2;
+    if (lane == 0) {
       int slot = 0, jobno = 0;
       for (int it = 0; it < iters; ++it) {
         for_jobs(it, [&](const Job& jb) {
           const Plan pl = plan_of(jb);
           const int b0 = slot;
           slot += pl.nb;
-          if ((jobno++ % kStorers) != lane) return;
+          if ((jobno++ % kStorers) != sw_id) return;
           for (int o = 0; o < pl.nb; ++o) mbar_wait(&consumed[(b0 + o) % NB], ((b0 + o) / NB) & 1);
           const bool live = *(volatile int*)&s_abort == 0;
           const unsigned long long nv = jb.p.p1 - jb.p.p0, nut = nut_of(jb);
@@ -1050,16 +1065,16 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
           }
           for (int o = 0; o < pl.nb; ++o) mbar_arrive(&empty[(b0 + o) % NB]);
         });
-        // this lane's stores of iteration it are complete before the raiser's fence
+        // this warp's stores of iteration it are complete before the raiser's fence
         tma_wait_all<0>();
         fence_proxy_async();
-        st_release_cta(&s_done[lane], it + 1);
-        if (lane == 0) stamp(lr == 0 ? a.trace : nullptr, b, it, 7);
+        st_release_cta(&s_done[sw_id], it + 1);
+        if (sw_id == 0) stamp(lr == 0 ? a.trace : nullptr, b, it, 7);
       }
     }
   } else {
     // =============================== consumer warps =============================
-    const int ct = tid - 128;
+    const int ct = tid - kConsWarp0 * 32;
     int slot = 0;
     unsigned long long* const tr = (ct == 0 && lr == 0) ? a.trace : nullptr;
     for (int it = 0; it < iters; ++it) {
