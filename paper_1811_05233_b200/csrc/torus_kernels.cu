@@ -45,6 +45,11 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -66,6 +71,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Wait until *f >= v (wrap-safe).  Spin with relaxed loads and a short sleep -- a hot
+// loop of ld.acquire.sys (each one an L1 invalidate) slows every fence on the SM -- and
+// take the acquire once the value is there.  Returns false once `deadline` passes.
+__device__ __forceinline__ bool wait_flag_ge(const uint32_t* f, uint32_t v, unsigned long long deadline) {
+  unsigned spin = 0;
+  while ((int32_t)(ld_relaxed_sys(f) - v) < 0) {
+    __nanosleep(64);
+    if ((++spin & 63u) == 0 && gtimer() > deadline) return false;
+  }
+  (void)ld_acquire_sys(f);
+  return true;
+}
+
 // Workspace traffic goes through L2 only (.cg): slots are written by peers over NVLink
 // during the kernel, so L1 must never hold a stale line.
 __device__ __forceinline__ uint4 ld_ws(const void* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
@@ -436,15 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
         const int t = it - 2 * p;
         if (t < 0 || t >= T) continue;
         for_flags(kinds[p], t, true, [&](uint32_t* f, uint32_t v) {
-          if ((e++ & 31) == lane && ok) {
-            unsigned spin = 0;
-            while ((int32_t)(ld_acquire_sys(f) - v) < 0) {
-              if ((++spin & 255u) == 0 && gtimer() > deadline) {
-                ok = false;
-                break;
-              }
-            }
-          }
+          if ((e++ & 31) == lane && ok) ok = wait_flag_ge(f, v, deadline);
         });
       }
       return __all_sync(0xffffffffu, ok);
@@ -888,15 +898,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
         const int t = it - 2 * pp;
         if (t < 0 || t >= T) continue;
         for_flags(kinds[pp], t, true, [&](uint32_t* f, uint32_t v) {
-          if ((e++ & 31) == lane && ok) {
-            unsigned spin = 0;
-            while ((int32_t)(ld_acquire_sys(f) - v) < 0) {
-              if ((++spin & 255u) == 0 && gtimer() > deadline) {
-                ok = false;
-                break;
-              }
-            }
-          }
+          if ((e++ & 31) == lane && ok) ok = wait_flag_ge(f, v, deadline);
         });
       }
       return __all_sync(0xffffffffu, ok);
