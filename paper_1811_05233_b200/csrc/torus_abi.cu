@@ -75,8 +75,8 @@ struct torus_comm {
   int rank = 0, world = 1, X = 1, Y = 1;
   int device = 0;
   int G = 0;
-  int tile_vecs = 512;      // 16-byte vectors per tile piece (env TORUS_TILE)
-  bool tma = true;          // TMA-staged kernel (env TORUS_KERNEL=ldg selects the LDG/STG one)
+  int tile_vecs = 3840;     // 16-byte vectors per tile piece (env TORUS_TILE)
+  bool tma = false;         // env TORUS_KERNEL=tma selects the TMA-staged kernel
   int nlocal = 1;           // > 1: virtual ranks on one device
   bool virt = false;
   size_t slab_size = 0;
@@ -327,8 +327,8 @@ int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t*
   c->slab_size = own.size;
   c->own_slabs.push_back(own.ptr);
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
-  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", 512));
-  { const char* k = getenv("TORUS_KERNEL"); c->tma = !(k && strcmp(k, "ldg") == 0); }
+  { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
+  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", c->tma ? 512 : 3840));
   int rc = TORUS_OK;
   std::vector<char*> bases(world, nullptr);
   if (cudaSetDevice(c->device) != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "cudaSetDevice");
@@ -382,8 +382,8 @@ int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_
   if (ws_bytes == 0) ws_bytes = env_size("TORUS_WS_BYTES", kDefaultSlab);
   c->slab_size = (ws_bytes + 65535) & ~(size_t)65535;
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
-  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", 512));
-  { const char* k = getenv("TORUS_KERNEL"); c->tma = !(k && strcmp(k, "ldg") == 0); }
+  { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
+  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", c->tma ? 512 : 3840));
   if (ctas > 0) setenv("TORUS_CTAS", std::to_string(ctas).c_str(), 1);
   c->G = pick_ctas(device, c->nlocal);
   c->layout = make_layout(c->slab_size, c->G);
