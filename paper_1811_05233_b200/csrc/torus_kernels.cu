@@ -905,6 +905,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
     };
     auto raise_iter = [&](int it) {
       asm volatile("fence.acq_rel.sys;" ::: "memory");
+      stamp((lane == 0 && lr == 0) ? a.trace : nullptr, b, it, 3);
       int e = 0;
       for (int pp = 0; pp < P; ++pp) {
         const int t = it - 2 * pp;

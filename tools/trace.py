@@ -52,7 +52,7 @@ def main():
                 "it": it, "poll_start": m(r[:, 0]), "poll": m(r[:, 1] - r[:, 0]),
                 "cons_start": m(r[:, 5]), "cons_busy": m(r[:, 6] - r[:, 5]),
                 "storer_done": m(r[:, 7]), "done_after_cons": m(r[:, 7] - r[:, 6]),
-                "raiser_sees_done": m(r[:, 2] - r[:, 7]), "raise": m(r[:, 4] - r[:, 2])}))
+                "raiser_sees_done": m(r[:, 2] - r[:, 7]), "fence": m(r[:, 3] - r[:, 2]), "flag_stores": m(r[:, 4] - r[:, 3])}))
     comm.destroy()
     dist.destroy_process_group()
 
