@@ -53,6 +53,38 @@ def partition(n: int, parts: int, q: int) -> tuple[list[int], list[int]]:
     return list(off), list(ln)
 
 
+def exchange_blobs(blob: bytes, world: int, group=None) -> list[bytes]:
+    """All-gather one opaque blob per rank (the exported IPC handle), in rank order."""
+    if world == 1:
+        return [blob]
+    import torch.distributed as dist
+    out: list = [None] * world
+    dist.all_gather_object(out, blob, group=group)
+    return out
+
+
+def handles_array(blobs: Sequence[bytes]):
+    """Marshal gathered blobs into the C array torus_comm_init takes."""
+    n = ctypes.sizeof(torus_ipc_handle_t)
+    arr = (torus_ipc_handle_t * len(blobs))()
+    for r, blob in enumerate(blobs):
+        if len(blob) != n:
+            raise ValueError(f"rank {r}: IPC handle blob of {len(blob)} bytes, expected {n}")
+        ctypes.memmove(ctypes.byref(arr[r]), blob, n)
+    return arr
+
+
+def agree_status(rc: int, msg: str, world: int, group=None) -> list:
+    """Every rank learns every rank's init status; returns [(rank, (rc, msg))] failures."""
+    if world == 1:
+        status = [(rc, msg)]
+    else:
+        import torch.distributed as dist
+        status = [None] * world
+        dist.all_gather_object(status, (rc, msg), group=group)
+    return [(r, s) for r, s in enumerate(status) if s[0] != 0]
+
+
 class _CommBase:
     _comm: ctypes.c_void_p
 
@@ -111,6 +143,9 @@ class TorusComm(_CommBase):
     @classmethod
     def init(cls, group=None, X: int = 0, Y: int = 0, ws_bytes: int = 0,
              device: int | None = None) -> "TorusComm":
+        """Collective: every rank of `group` allocates and exports its slab, the 64-byte
+        IPC handles are all-gathered in rank order, every rank opens its peers' slabs,
+        and all ranks agree on success (no half-built communicator survives)."""
         import torch.distributed as dist
         L = _lib.load()
         rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -119,27 +154,15 @@ class TorusComm(_CommBase):
         torch.cuda.set_device(dev)
         h = torus_ipc_handle_t()
         check(L.torus_workspace_alloc(dev, ws_bytes, ctypes.byref(h)), "torus_workspace_alloc")
-        if world > 1:
-            blobs: list = [None] * world
-            dist.all_gather_object(blobs, bytes(h), group=group)
-        else:
-            blobs = [bytes(h)]
-        arr = (torus_ipc_handle_t * world)()
-        for r, blob in enumerate(blobs):
-            ctypes.memmove(ctypes.byref(arr[r]), blob, ctypes.sizeof(torus_ipc_handle_t))
+        arr = handles_array(exchange_blobs(bytes(h), world, group))
         comm = ctypes.c_void_p()
         rc = L.torus_comm_init(rank, world, X, Y, arr, ctypes.byref(comm))
         msg = "" if rc == 0 else L.torus_last_error().decode(errors="replace")
-        if world > 1:  # every rank learns whether every peer succeeded (no half-built comm)
-            status: list = [None] * world
-            dist.all_gather_object(status, (rc, msg), group=group)
-        else:
-            status = [(rc, msg)]
-        bad = [(r, s) for r, s in enumerate(status) if s[0] != 0]
+        bad = agree_status(rc, msg, world, group)
         if bad:
             if rc == 0:
                 L.torus_comm_destroy(comm)  # peers failed: no collective barrier possible
-            elif rc != 0:
+            else:
                 L.torus_workspace_release(ctypes.byref(h))
             raise RuntimeError(f"torus_comm_init failed on ranks {bad}")
         return cls(comm, rank, world, dev)

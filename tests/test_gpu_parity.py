@@ -64,26 +64,44 @@ def run_virtual(vt, ins, dtype, wire, op):
     return [from_dev(t, dtype) for t in ts]
 
 
+KERNELS = ["ldg", "tma"]  # the default LDG/STG kernel and the TMA-staged one
+
+
+def make_vt(X, Y, ws=0, kernel="ldg"):
+    """The kernel is chosen from TORUS_KERNEL when the communicator is built."""
+    import os
+    from paper_1811_05233_b200 import VirtualTorus
+    old = os.environ.get("TORUS_KERNEL")
+    os.environ["TORUS_KERNEL"] = kernel
+    try:
+        return VirtualTorus(X, Y, device=0, ws_bytes=ws)
+    finally:
+        if old is None:
+            del os.environ["TORUS_KERNEL"]
+        else:
+            os.environ["TORUS_KERNEL"] = old
+
+
 @pytest.fixture(scope="module")
 def vgrids():
-    from paper_1811_05233_b200 import VirtualTorus
     made = {}
 
-    def get(X, Y, ws=0):
-        key = (X, Y, ws)
+    def get(X, Y, ws=0, kernel="ldg"):
+        key = (X, Y, ws, kernel)
         if key not in made:
-            made[key] = VirtualTorus(X, Y, device=0, ws_bytes=ws)
+            made[key] = make_vt(X, Y, ws, kernel)
         return made[key]
     yield get
     for vt in made.values():
         vt.destroy()
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("X,Y", GRIDS)
 @pytest.mark.parametrize("dtype,wire", PAIRS)
 @pytest.mark.parametrize("op", ["sum", "mean"])
-def test_virtual_grid_bit_exact(vgrids, X, Y, dtype, wire, op):
-    vt = vgrids(X, Y)
+def test_virtual_grid_bit_exact(vgrids, X, Y, dtype, wire, op, kernel):
+    vt = vgrids(X, Y, kernel=kernel)
     N = X * Y
     R = vt.round_elems(TD[wire])
     for D in (1, 7, 1000, 4099, 200_003):
@@ -96,11 +114,12 @@ def test_virtual_grid_bit_exact(vgrids, X, Y, dtype, wire, op):
             assert_same(got[r], ref[r], f"{X}x{Y} {dtype}/{wire} {op} D={D} rank {r}")
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
 @pytest.mark.parametrize("X,Y", [(2, 2), (2, 4), (1, 4)])
 @pytest.mark.parametrize("dtype,wire", [("f16", "f16"), ("f32", "bf16"), ("i32", "i32")])
-def test_multi_round(vgrids, X, Y, dtype, wire):
+def test_multi_round(vgrids, X, Y, dtype, wire, kernel):
     """A slab far smaller than the message forces several rounds."""
-    vt = vgrids(X, Y, ws=1 << 20)  # 1 MiB slab
+    vt = vgrids(X, Y, ws=1 << 20, kernel=kernel)  # 1 MiB slab
     R = vt.round_elems(TD[wire])
     assert 0 < R < 300_000
     D = 3 * R + 12345
@@ -113,10 +132,11 @@ def test_multi_round(vgrids, X, Y, dtype, wire):
     assert vt.launches(D, TD[dtype], TD[wire]) == 4
 
 
-def test_unaligned_buffers(vgrids):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_unaligned_buffers(vgrids, kernel):
     """Buffers offset by one element take the scalar (non-vector) user-buffer path."""
     X, Y, D = 2, 2, 5001
-    vt = vgrids(X, Y)
+    vt = vgrids(X, Y, kernel=kernel)
     ins = synthetic.make_all("normal", D, 4, "f32")
     ts = []
     for a in ins:
@@ -131,10 +151,11 @@ def test_unaligned_buffers(vgrids):
         assert_same(ts[r].cpu().numpy(), ref[r], f"unaligned rank {r}")
 
 
-def test_repeated_calls_and_zero_count(vgrids):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_repeated_calls_and_zero_count(vgrids, kernel):
     """Back-to-back calls (epoch flags advance, slots are reused) with varying counts."""
     X, Y = 2, 4
-    vt = vgrids(X, Y)
+    vt = vgrids(X, Y, kernel=kernel)
     R = vt.round_elems(torch.float16)
     for it, D in enumerate((0, 33, 100_000, 8, 77_777, 1)):
         ins = synthetic.make_all("normal", D, 8, "f16", salt=it)
@@ -146,10 +167,11 @@ def test_repeated_calls_and_zero_count(vgrids):
             assert_same(got[r], ref[r], f"call {it} D={D} rank {r}")
 
 
-def test_special_values(vgrids):
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_special_values(vgrids, kernel):
     """inf / nan / subnormal / signed zero go through the same rounding as the oracle."""
     X, Y, D = 2, 2, 64
-    vt = vgrids(X, Y)
+    vt = vgrids(X, Y, kernel=kernel)
     specials = np.array([np.inf, -np.inf, np.nan, 0.0, -0.0, 1e-45, -1e-45, 6e-8, 65504.0,
                          65520.0, -65536.0, 3.4e38, 1e-38, 5.9e-8, 2.98e-8], dtype=np.float32)
     g = np.random.Generator(np.random.PCG64(5))
@@ -179,13 +201,13 @@ def test_single_rank_cast_scale():
         vt.destroy()
 
 
-def test_full_size_resnet50_sampled():
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_full_size_resnet50_sampled(kernel):
     """BASELINE config 2 at full size, in the bench's launch configuration (2x4 grid,
     fp16, mean, default slab -> one round): sampled outputs vs the oracle's closed form,
     plus all-ranks-identical and the f64 error bound on the sample."""
-    from paper_1811_05233_b200 import VirtualTorus
     X, Y, D = 2, 4, synthetic.RESNET50_NUMEL
-    vt = VirtualTorus(X, Y, device=0)
+    vt = make_vt(X, Y, kernel=kernel)
     try:
         R = vt.round_elems(torch.float16)
         assert R >= D, "north-star message must be a single round"
