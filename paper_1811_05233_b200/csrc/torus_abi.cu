@@ -91,6 +91,8 @@ struct torus_comm {
   int* d_err = nullptr;
   bool poisoned = false;
   unsigned long long* d_trace = nullptr;  // TORUS_TRACE=1: [G][kTraceIters][kTraceEvents]
+  uint32_t* d_done_local = nullptr;       // TMA kernel: [nlocal][G][8] stage tiles done
+  uint32_t* d_sig_ack = nullptr;          // TMA kernel: [nlocal][G] signal-lane acks
 };
 
 namespace {
@@ -123,6 +125,13 @@ int alloc_comm_common(torus_comm* c) {
   *c->h_err = 0;
   CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_err), c->h_err, 0));
   CU(cudaMalloc(&c->d_ranks, sizeof(RankDev) * c->nlocal));
+  {
+    const size_t nd = (size_t)c->nlocal * c->G;
+    CU(cudaMalloc(&c->d_done_local, nd * 8 * sizeof(uint32_t)));
+    CU(cudaMemset(c->d_done_local, 0, nd * 8 * sizeof(uint32_t)));
+    CU(cudaMalloc(&c->d_sig_ack, nd * sizeof(uint32_t)));
+    CU(cudaMemset(c->d_sig_ack, 0, nd * sizeof(uint32_t)));
+  }
   if (env_size("TORUS_TRACE", 0)) {
     const size_t tb = (size_t)c->G * kTraceIters * kTraceEvents * sizeof(unsigned long long);
     CU(cudaMalloc(&c->d_trace, tb));
@@ -162,7 +171,10 @@ int pick_ctas(int device, int nlocal) {
   int want = (int)env_size("TORUS_CTAS", nlocal > 1 ? 16 : sms);
   want = std::max(1, want);
   // every CTA of every rank that waits on another must be co-resident
-  return std::min(want, std::max(1, resident / nlocal));
+  // the TMA kernel appends one signal CTA on its own SM
+  const char* k = getenv("TORUS_KERNEL");
+  const int spare = (k && strcmp(k, "tma") == 0) ? 1 : 0;
+  return std::min(want, std::max(1, (resident - spare) / nlocal));
 }
 
 void destroy_resources(torus_comm* c) {
@@ -171,6 +183,8 @@ void destroy_resources(torus_comm* c) {
   if (c->d_ranks) cudaFree(c->d_ranks);
   if (c->d_epochs) cudaFree(c->d_epochs);
   if (c->d_trace) cudaFree(c->d_trace);
+  if (c->d_done_local) cudaFree(c->d_done_local);
+  if (c->d_sig_ack) cudaFree(c->d_sig_ack);
   if (c->h_err) cudaFreeHost(c->h_err);
   delete c;
 }
@@ -545,6 +559,9 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   a.tile_vecs = c->tile_vecs;
   a.trace = c->d_trace;
   a.nbufs = 0;
+  a.done_local = c->d_done_local;
+  a.sig_ack = c->d_sig_ack;
+  a.nsig = c->tma ? (c->nlocal * c->G + kThreads - 1) / kThreads : 0;
   if (c->tma) {
     // ring buffers of one piece each: jobs in flight across the producer, the consumers
     // and the 8 storer lanes; the largest job holds max(X,Y)+3 at once -- keep room for

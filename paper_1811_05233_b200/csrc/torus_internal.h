@@ -73,6 +73,11 @@ struct LaunchArgs {
   int T;                         // pipeline tiles per CTA slice (same on every rank)
   int tile_vecs;                 // vectors per tile piece
   int nbufs;                     // > 0: TMA-staged kernel with this many ring buffers
+  // TMA kernel: per data CTA, the last tile each stage has completed (5 words, stride 8),
+  // published at gpu scope for the signal CTA(s), and the signal lane's end-of-call ack
+  uint32_t* done_local;          // [nlocal * G * 8]
+  uint32_t* sig_ack;             // [nlocal * G]
+  int nsig;                      // signal CTAs appended after the nlocal * G data CTAs
 };
 
 // TMA kernel shared memory: nbufs ring buffers of one piece each (tile_vecs 16-byte wire

@@ -53,6 +53,14 @@ __device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t* p) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -702,8 +710,12 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
 //               stores have read them; at each iteration end drain the warp's bulk groups
 //               and post s_done[storer] (one warp each: a lane blocked in wait_group
 //               stalls its whole warp)
-//   warp 6      raiser: once every storer has drained iteration it, raise its output
-//               flags behind one fence.acq_rel.sys (off the throughput path)
+//   warp 6      publisher: once every storer has drained iteration it, post each stage's
+//               completed tile to global memory (st.release.gpu; no system fence here)
+//   signal CTA  (appended after the data CTAs, on its own quiet SM) one lane per data
+//               CTA: when a posted tile advances, one fence.acq_rel.sys and the flag
+//               stores to the peers.  A system-scope fence issued from an SM that is
+//               streaming bulk traffic took ~8 us (traced); from a quiet SM ~1 us.
 //   warps 7-15  consumers: folds (ring order, f32 accumulation, mean, one rounding) and
 //               dtype<->wire casts from shared memory into shared memory; scalar
 //               st/ld.global only for a ragged last vector or an unaligned user buffer
@@ -734,6 +746,63 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
   constexpr int SW = kVecBytes / VE;
   constexpr int ST = (int)sizeof(UT);
   constexpr bool kCast = DT != W;
+
+  if (blockIdx.x >= a.nlocal * a.G) {
+    // ================================ signal CTA ================================
+    const int gidx = (blockIdx.x - a.nlocal * a.G) * blockDim.x + threadIdx.x;
+    if (gidx >= a.nlocal * a.G) return;
+    const int lr = gidx / a.G, b = gidx - (gidx / a.G) * a.G, G = a.G;
+    const RankDev* __restrict__ R = a.ranks + lr;
+    const int X = R->X, Y = R->Y, rho = R->rho, c = R->c;
+    const uint32_t seq = R->epoch[b];
+    const uint32_t target = seq + (uint32_t)a.T;
+    // output flag of each stage: A -> H, B -> V (Y > 1) or R, C -> AG, D -> R
+    const int okind[kStages] = {X > 1 ? kFlagH : -1, Y > 1 ? kFlagV : (X > 1 ? kFlagR : -1),
+                                Y > 1 ? kFlagAG : -1, (Y > 1 && X > 1) ? kFlagR : -1, -1};
+    uint32_t raised[kStages];
+    for (int k2 = 0; k2 < kStages; ++k2) raised[k2] = seq;
+    const uint32_t* const dl = a.done_local + (size_t)gidx * 8;
+    const unsigned long long deadline = gtimer() + a.timeout_ns;
+    bool ok = true;
+    while (true) {
+      bool all = true, fresh = false;
+      uint32_t v[kStages];
+      for (int k2 = 0; k2 < kStages; ++k2) {
+        if (okind[k2] < 0) continue;
+        v[k2] = ld_acquire_gpu(dl + k2);
+        if ((int32_t)(v[k2] - raised[k2]) > 0) fresh = true;
+        if (v[k2] != target) all = false;
+      }
+      if (fresh) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        for (int k2 = 0; k2 < kStages; ++k2) {
+          if (okind[k2] < 0 || (int32_t)(v[k2] - raised[k2]) <= 0) continue;
+          const int kind = okind[k2];
+          const bool row = (kind == kFlagH || kind == kFlagR);
+          const int cnt = row ? X - 1 : Y - 1;
+          for (int l = 0; l < cnt; ++l) {
+            const int other = row ? (c + 1 + l) % X : (rho + 1 + l) % Y;
+            const int peer = row ? rho * X + other : other * X + c;
+            uint32_t* f = reinterpret_cast<uint32_t*>(R->ws[peer]) +
+                          ((size_t)(kind * kMaxDim + (row ? c : rho)) * G + b);
+            st_relaxed_sys(f, v[k2]);
+          }
+          raised[k2] = v[k2];
+        }
+      }
+      if (all) break;
+      if (!fresh) {
+        __nanosleep(64);
+        if (gtimer() > deadline) {
+          atomicExch_system(R->err, kErrTimeout);
+          ok = false;
+          break;
+        }
+      }
+    }
+    if (ok) st_release_gpu(a.sig_ack + gidx, target);
+    return;
+  }
 
   extern __shared__ __align__(1024) unsigned char smem[];
   const int NB = a.nbufs;
@@ -956,6 +1025,9 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
         __syncwarp();
       }
     } else {
+      // publisher: each stage's newest completed tile -> global (gpu scope) for the
+      // signal CTA, which fences on a quiet SM and forwards it to the peers' flags
+      uint32_t* const dl = a.done_local + (size_t)(lr * G + b) * 8;
       for (int it = 0; it < iters; ++it) {
         if (!wait_done(it)) {
           if (lane == 0) {
@@ -967,7 +1039,12 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
         }
         if (*(volatile int*)&s_abort) break;
         stamp(tr, b, it, 2);
-        raise_iter(it);
+        if (lane == 0)
+          for (int pp = 0; pp < P; ++pp) {
+            const int t = it - 2 * pp;
+            if (t >= 0 && t < T) st_release_gpu(dl + kinds[pp], seq + (uint32_t)t + 1u);
+          }
+        __syncwarp();
         stamp(tr, b, it, 4);
       }
     }
@@ -1164,7 +1241,21 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
     }
   }
   __syncthreads();
-  if (tid == 0 && !s_abort) R->epoch[b] = seq + (uint32_t)T;
+  if (tid == 0 && !s_abort) {
+    // the signal lane has read this call's epoch and forwarded every flag
+    const unsigned long long deadline = gtimer() + a.timeout_ns;
+    const uint32_t* ack = a.sig_ack + (size_t)(lr * G + b);
+    bool ok = true;
+    while ((int32_t)(ld_acquire_gpu(ack) - (seq + (uint32_t)T)) < 0) {
+      __nanosleep(64);
+      if (gtimer() > deadline) {
+        atomicExch_system(R->err, kErrTimeout);
+        ok = false;
+        break;
+      }
+    }
+    if (ok) R->epoch[b] = seq + (uint32_t)T;
+  }
 }
 
 // N = 1: buf = from_wire(to_wire(buf)); the mean scale is x * 1.0 (identity).
@@ -1211,7 +1302,8 @@ __global__ void barrier_kernel(const RankDev* ranks, unsigned long long bar_off,
 template <int DT, int W>
 cudaError_t launch_typed(const LaunchArgs& a, bool cooperative, cudaStream_t stream) {
   const dim3 grid(a.nlocal * a.G), block(kThreads);
-  if (a.nbufs > 0) {  // TMA-staged kernel
+  if (a.nbufs > 0) {  // TMA-staged kernel: data CTAs + signal CTAs
+    const dim3 grid(a.nlocal * a.G + a.nsig), block(kThreads);
     const int smem = tma_smem_bytes(a.nbufs, a.tile_vecs, (int)(sizeof(typename Elem<DT>::T) * Wire<W>::VE / 16));
     static bool attr_set = false;
     if (!attr_set) {
