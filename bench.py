@@ -351,8 +351,9 @@ def load_traffic(kernel):
     """dram bytes per launch from a committed ncu --set full capture, if present."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        return json.load(open(p)).get(kernel)
-    except (OSError, ValueError):
+        v = json.load(open(p)).get(kernel)
+        return float(v) if v is not None else None
+    except (OSError, ValueError, TypeError):
         return None
 
 

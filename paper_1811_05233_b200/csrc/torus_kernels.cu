@@ -1259,16 +1259,27 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
 }
 
 // N = 1: buf = from_wire(to_wire(buf)); the mean scale is x * 1.0 (identity).
+// HBM-bound: 8 B per element.  Each thread keeps kCastUnroll 32-byte vectors in flight
+// (4 x LDG.E.128 before the first store) over a grid of 4 CTAs per SM.
+constexpr int kCastUnroll = 4;
 template <int W>
 __global__ void __launch_bounds__(256) castscale_kernel(float* buf, unsigned long long n) {
   const unsigned long long nv = (n + 7) / 8;
   const bool aligned = (reinterpret_cast<uintptr_t>(buf) & 15) == 0;
-  for (unsigned long long v = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; v < nv;
-       v += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long e = v * 8;
-    const int nrem = (int)min(8ull, n - e);
-    const uint4 w = load_user<DT_F32, W>(buf, e, nrem, aligned);
-    store_user<DT_F32, W>(buf, e, nrem, w, aligned);
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long v0 = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; v0 < nv;
+       v0 += stride * kCastUnroll) {
+    uint4 w[kCastUnroll];
+#pragma unroll
+    for (int u = 0; u < kCastUnroll; ++u) {
+      const unsigned long long v = v0 + u * stride;
+      if (v < nv) w[u] = load_user<DT_F32, W>(buf, v * 8, (int)min(8ull, n - v * 8), aligned);
+    }
+#pragma unroll
+    for (int u = 0; u < kCastUnroll; ++u) {
+      const unsigned long long v = v0 + u * stride;
+      if (v < nv) store_user<DT_F32, W>(buf, v * 8, (int)min(8ull, n - v * 8), w[u], aligned);
+    }
   }
 }
 
@@ -1376,9 +1387,11 @@ int torus_kernel_max_ctas_per_sm(int dtype, int wire) {
 cudaError_t launch_castscale(void* buf, unsigned long long n, int dtype, int wire,
                              cudaStream_t stream) {
   if (dtype != DT_F32) return cudaErrorInvalidValue;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const unsigned long long nv = (n + 7) / 8;
-  unsigned long long want = (nv + 255) / 256;
-  int blocks = (int)(want < 148ull * 8 ? want : 148ull * 8);
+  const unsigned long long want = (nv + 256ull * kCastUnroll - 1) / (256ull * kCastUnroll);
+  int blocks = (int)(want < (unsigned long long)sms * 4 ? want : (unsigned long long)sms * 4);
   if (blocks < 1) blocks = 1;
   if (wire == DT_F16)
     castscale_kernel<DT_F16><<<blocks, 256, 0, stream>>>(reinterpret_cast<float*>(buf), n);
