@@ -559,7 +559,6 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   a.tile_vecs = c->tile_vecs;
   a.trace = c->d_trace;
   a.nbufs = 0;
-  a.copy_tma = (int)env_size("TORUS_COPY", 1);
   a.done_local = c->d_done_local;
   a.sig_ack = c->d_sig_ack;
   a.nsig = c->tma ? (c->nlocal * c->G + kThreads - 1) / kThreads : 0;

@@ -78,7 +78,6 @@ struct LaunchArgs {
   uint32_t* done_local;          // [nlocal * G * 8]
   uint32_t* sig_ack;             // [nlocal * G]
   int nsig;                      // signal CTAs appended after the nlocal * G data CTAs
-  int copy_tma;                  // LDG kernel: pure-copy stages via the TMA copy warp
 };
 
 // TMA kernel shared memory: nbufs ring buffers of one piece each (tile_vecs 16-byte wire

@@ -148,17 +148,6 @@ __device__ __forceinline__ void tma_wait_all() {
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async;" ::: "memory");
 }
-// wait until at most n bulk groups are still reading their sources (n known at run time)
-__device__ __forceinline__ void tma_wait_read_dyn(int n) {
-  switch (n) {
-    case 0: tma_wait_read<0>(); break;
-    case 1: tma_wait_read<1>(); break;
-    case 2: tma_wait_read<2>(); break;
-    case 3: tma_wait_read<3>(); break;
-    case 4: tma_wait_read<4>(); break;
-    default: tma_wait_read<5>(); break;
-  }
-}
 
 // ------------------------------------------------------------------------------------
 // wire traits: a 16-byte vector holds VE wire elements; Acc is the accumulation type
@@ -340,11 +329,7 @@ __device__ __forceinline__ Piece make_piece(unsigned long long n, int X, int Y, 
 }
 
 constexpr int kCtrlThreads = 32;                     // warp 0: flags, fences, signals
-constexpr int kCopyWarp = 1;                         // warp 1: TMA copies (A, D, E)
-constexpr int kWorkers = kThreads - 64;              // warps 2..15: folds (+ fallbacks)
-constexpr int kCopyStages = 6;                       // TMA copy ring: 6 x 16 KiB
-constexpr int kCopyChunk = 16384;
-constexpr int kCopySmem = kCopyStages * kCopyChunk;
+constexpr int kWorkers = kThreads - kCtrlThreads;    // warps 1..15: data movement
 constexpr int kUnroll = 4;                           // vectors per worker per pass (copies)
 constexpr int kUnrollFold = 2;                       // vectors per worker per pass (folds)
 
@@ -405,22 +390,11 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
   char* const vin = myws + a.vin_off;
   char* const chunk = myws + a.chunk_off;
 
-  // Pure-copy stages (A push, D / E pulls) go through the TMA copy warp when the user
-  // buffer is the wire type and 16-byte aligned; a piece holding the ragged last vector
-  // (and every piece otherwise) stays with the register workers.
-  extern __shared__ __align__(1024) unsigned char csmem[];
-  __shared__ uint64_t cbar[kCopyStages];
-  const bool tma_copy = (DT == W) && aligned && a.copy_tma != 0;
-  auto ragged = [&](const Piece& p) -> bool { return p.so + p.p1 * VE > p.cl; };
-  auto by_copy_warp = [&](const Piece& p) -> bool { return tma_copy && !ragged(p); };
-
   __shared__ uint32_t s_seq;
   __shared__ int s_abort;
   if (tid == 0) {
     s_seq = R->epoch[b];
     s_abort = 0;
-    for (int i = 0; i < kCopyStages; ++i) mbar_init(&cbar[i], 1);
-    fence_mbar_init();
   }
   __syncthreads();
   const uint32_t seq = s_seq;
@@ -528,103 +502,9 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
     }
     bar_sync(kBarDone);
     raise_iter(iters - 1);
-  } else if (tid < 64) {
-    // ============================== TMA copy warp ===============================
-    if (!tma_copy) {
-      for (int it = 0; it < iters; ++it) {
-        bar_sync(kBarReady);
-        if (*(volatile int*)&s_abort) return;
-        bar_arrive(kBarDone);
-      }
-    } else {
-      const int lane = tid - 32;
-      struct CopyDesc {
-        char* d1;
-        char* d2;
-        unsigned bytes;
-      };
-      CopyDesc cq[kCopyStages];
-      int loaded = 0, stored = 0;
-      auto store_oldest = [&]() {
-        const int sl = stored % kCopyStages;
-        mbar_wait(&cbar[sl], (stored / kCopyStages) & 1);
-        tma_store(cq[sl].d1, csmem + (size_t)sl * kCopyChunk, cq[sl].bytes);
-        if (cq[sl].d2) tma_store(cq[sl].d2, csmem + (size_t)sl * kCopyChunk, cq[sl].bytes);
-        tma_commit();
-        ++stored;
-      };
-      // stream one piece: chunks of 16 KiB through the ring, loads kept ahead of stores
-      auto copy_piece = [&](const char* src, char* d1, char* d2, unsigned long long bytes) {
-        for (unsigned long long o = 0; o < bytes; o += kCopyChunk) {
-          const unsigned cb = (unsigned)min((unsigned long long)kCopyChunk, bytes - o);
-          if (loaded - stored == kCopyStages) store_oldest();
-          const int sl = loaded % kCopyStages;
-          if (loaded >= kCopyStages) tma_wait_read_dyn(stored - (loaded - kCopyStages) - 1);
-          cq[sl].d1 = d1 + o;
-          cq[sl].d2 = d2 ? d2 + o : nullptr;
-          cq[sl].bytes = cb;
-          mbar_expect_tx(&cbar[sl], cb);
-          tma_load(csmem + (size_t)sl * kCopyChunk, src + o, cb, &cbar[sl]);
-          ++loaded;
-        }
-      };
-      for (int it = 0; it < iters; ++it) {
-        bar_sync(kBarReady);
-        if (*(volatile int*)&s_abort) return;
-        if (lane == 0) {
-          fence_proxy_async();  // data the control warp acquired -> async-proxy loads
-          for (int p = 0; p < P; ++p) {
-            const int t = it - 2 * p;
-            if (t < 0 || t >= T) continue;
-            const int k = kinds[p];
-            if (k == kA) {        // my share of chunk j -> (rho, j).h_in[c]
-              for (int jj = 1; jj < X; ++jj) {
-                const int j = (c + jj) % X;
-                char* const dst = R->ws[rho * X + j] + a.hin_off + (size_t)c * a.hin_stride;
-                for (int s2 = 0; s2 < Y; ++s2) {
-                  const Piece pc = make_piece(n, X, Y, q, G, b, TV, j, s2, t);
-                  if (pc.p1 <= pc.p0 || ragged(pc)) continue;
-                  const unsigned long long el = pc.so + pc.p0 * VE;
-                  copy_piece(reinterpret_cast<const char*>(buf) + (a.buf_off + pc.co + el) * SW,
-                             dst + el * SW, nullptr, (pc.p1 - pc.p0) * kVecBytes);
-                }
-              }
-            } else if (k == kD) {  // column peers' reduced sub-chunks -> my buffer (+ slot)
-              for (int ii = 1; ii < Y; ++ii) {
-                const int i = (rho + ii) % Y;
-                const Piece pc = make_piece(n, X, Y, q, G, b, TV, c, i, t);
-                if (pc.p1 <= pc.p0 || ragged(pc)) continue;
-                const unsigned long long el = pc.so + pc.p0 * VE;
-                copy_piece(R->ws[i * X + c] + a.chunk_off + el * SW,
-                           reinterpret_cast<char*>(buf) + (a.buf_off + pc.co + el) * SW,
-                           X > 1 ? chunk + el * SW : nullptr, (pc.p1 - pc.p0) * kVecBytes);
-              }
-            } else if (k == kE) {  // row peers' completed chunks -> my buffer
-              for (int jj = 1; jj < X; ++jj) {
-                const int j = (c + jj) % X;
-                for (int s2 = 0; s2 < Y; ++s2) {
-                  const Piece pc = make_piece(n, X, Y, q, G, b, TV, j, s2, t);
-                  if (pc.p1 <= pc.p0 || ragged(pc)) continue;
-                  const unsigned long long el = pc.so + pc.p0 * VE;
-                  copy_piece(R->ws[rho * X + j] + a.chunk_off + el * SW,
-                             reinterpret_cast<char*>(buf) + (a.buf_off + pc.co + el) * SW, nullptr,
-                             (pc.p1 - pc.p0) * kVecBytes);
-                }
-              }
-            }
-          }
-          // this iteration's stores complete before DONE (the control warp then fences)
-          while (stored < loaded) store_oldest();
-          tma_wait_all<0>();
-          fence_proxy_async();
-        }
-        __syncwarp();
-        bar_arrive(kBarDone);
-      }
-    }
   } else {
     // =============================== worker warps ===============================
-    const int w = tid - 64;
+    const int w = tid - kCtrlThreads;
     unsigned long long* const tr = (w == 0 && lr == 0) ? a.trace : nullptr;
     for (int it = 0; it < iters; ++it) {
       bar_sync(kBarReady);
@@ -641,7 +521,6 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
             char* const dst = R->ws[rho * X + j] + a.hin_off + (size_t)c * a.hin_stride;
             for (int s = 0; s < Y; ++s) {
               const Piece p = make_piece(n, X, Y, q, G, b, TV, j, s, t);
-              if (by_copy_warp(p)) continue;
               for (unsigned long long v0 = p.p0 + w; v0 < p.p1; v0 += kUnroll * kWorkers) {
                 uint4 r[kUnroll];
 #pragma unroll
@@ -759,7 +638,6 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
             const int i = (rho + ii) % Y;
             const char* const src = R->ws[i * X + c] + a.chunk_off;
             const Piece p = make_piece(n, X, Y, q, G, b, TV, c, i, t);
-            if (by_copy_warp(p)) continue;
             for (unsigned long long v0 = p.p0 + w; v0 < p.p1; v0 += kUnroll * kWorkers) {
               uint4 r[kUnroll];
 #pragma unroll
@@ -785,7 +663,6 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
             const char* const src = R->ws[rho * X + j] + a.chunk_off;
             for (int s = 0; s < Y; ++s) {
               const Piece p = make_piece(n, X, Y, q, G, b, TV, j, s, t);
-              if (by_copy_warp(p)) continue;
               for (unsigned long long v0 = p.p0 + w; v0 < p.p1; v0 += kUnroll * kWorkers) {
                 uint4 r[kUnroll];
 #pragma unroll
@@ -1454,19 +1331,12 @@ cudaError_t launch_typed(const LaunchArgs& a, bool cooperative, cudaStream_t str
     torus_tma_kernel<DT, W><<<grid, block, smem, stream>>>(a);
     return cudaGetLastError();
   }
-  static bool ldg_attr = false;
-  if (!ldg_attr) {
-    cudaError_t e = cudaFuncSetAttribute(torus_kernel<DT, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kCopySmem);
-    if (e != cudaSuccess) return e;
-    ldg_attr = true;
-  }
   if (cooperative) {
     void* args[] = {const_cast<LaunchArgs*>(&a)};
-    return cudaLaunchCooperativeKernel((const void*)torus_kernel<DT, W>, grid, block, args, kCopySmem,
+    return cudaLaunchCooperativeKernel((const void*)torus_kernel<DT, W>, grid, block, args, 0,
                                        stream);
   }
-  torus_kernel<DT, W><<<grid, block, kCopySmem, stream>>>(a);
+  torus_kernel<DT, W><<<grid, block, 0, stream>>>(a);
   return cudaGetLastError();
 }
 
