@@ -51,6 +51,8 @@ def parse():
     p.add_argument("--dtype", default=None, help="buffer dtype (default f16; f32 at N=1)")
     p.add_argument("--wire", default="f16")
     p.add_argument("--op", default="mean", choices=["sum", "mean"])
+    p.add_argument("--algo", default="torus", choices=["torus", "ring"],
+                   help="ring = the flat-ring baseline kernel (config 3 comparison)")
     p.add_argument("--no-nccl", action="store_true", help="skip the NCCL comparison")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
@@ -178,8 +180,10 @@ def run_torus(args):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    reduce_fn = comm.ring_all_reduce if args.algo == "ring" else comm.all_reduce
+
     def call():
-        comm.all_reduce(buf, op=args.op, wire=TD[wire_s], stream=stream)
+        reduce_fn(buf, op=args.op, wire=TD[wire_s], stream=stream)
 
     # sanity (not the parity gate -- that is tests/): all ranks agree, and the result is
     # within the north-star tolerance of an f64 all-reduce done with NCCL in f64.
@@ -328,7 +332,10 @@ def run_torus(args):
         "config": {"workload": ("resnet50-grad-allreduce" if world > 1 else
                                 "resnet50-grad-castscale-degenerate (N=1)"),
                    "count": D, "buffer_dtype": dtype_s, "wire_dtype": wire_s, "op": args.op,
-                   "grid": f"{X}x{Y}", "parallelism": f"torus{X}x{Y}", "ctas_per_rank": comm_ctas(),
+                   "grid": f"{X}x{Y}" if args.algo == "torus" else f"ring{world}",
+                   "algo": args.algo,
+                   "parallelism": f"torus{X}x{Y}" if args.algo == "torus" else f"ring{world}",
+                   "ctas_per_rank": comm_ctas(),
                    "message_bytes": S, "l2": "flushed (256 MiB write) before every timed call",
                    "value_is": "busbw" if world > 1 else "algbw (busbw is 0 at N=1)"},
         "algbw": algbw, "busbw": busbw, "us_per_call": t * 1e6, "us_per_call_min": t_min * 1e6,

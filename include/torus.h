@@ -123,6 +123,19 @@ TORUS_API int torus_allreduce_ex(torus_comm_t comm, void* buf, size_t count, tor
 TORUS_API int torus_vallreduce(torus_comm_t comm, void* const* bufs, size_t count, torus_dtype_t dtype,
                      torus_dtype_t wire, torus_op_t op, torus_stream_t stream);
 
+/* Flat ring all-reduce over the rank ring 0 -> 1 -> ... -> N-1 -> 0 -- the BASELINE the
+ * torus replaces ("Ring all-reduce scheme executes 2(N-1) GPU-to-GPU
+ * operations", ref [14]).  N-1 reduce-scatter then N-1 all-gather steps, each a push
+ * to the next rank; every message is rounded to the wire type (HOP policy),
+ * the mean is applied once by the chunk's owner.  Same comm, arguments, ownership and
+ * errors as torus_allreduce_ex; rounds of torus_comm_ring_round_elems() elements. */
+TORUS_API int torus_ring_allreduce(torus_comm_t comm, void* buf, size_t count, torus_dtype_t dtype,
+                                   torus_dtype_t wire, torus_op_t op, torus_stream_t stream);
+TORUS_API int torus_vring_allreduce(torus_comm_t comm, void* const* bufs, size_t count,
+                                    torus_dtype_t dtype, torus_dtype_t wire, torus_op_t op,
+                                    torus_stream_t stream);
+TORUS_API size_t torus_comm_ring_round_elems(torus_comm_t comm, torus_dtype_t wire);
+
 /* ---------------------------------------------------------------------------------------
  * Queries, topology, host logic, errors
  * ------------------------------------------------------------------------------------- */

@@ -117,6 +117,16 @@ unsigned long long round_elems(const torus_comm* c, int wire) {
   return k * q * (unsigned long long)c->X * (unsigned long long)c->Y;
 }
 
+// Flat ring baseline: 2(N-1) slots of one chunk (R/N elements) per round.
+unsigned long long ring_round_elems(const torus_comm* c, int wire) {
+  const unsigned long long sw = wire_size(wire), q = kVecBytes / sw;
+  const unsigned long long N = (unsigned long long)c->world;
+  if (N < 2 || c->slab_size <= c->layout.data_off) return 0;
+  const unsigned long long data_elems = (c->slab_size - c->layout.data_off) / sw;
+  const unsigned long long k = data_elems / (2 * (N - 1) * q);
+  return k * q * N;
+}
+
 int alloc_comm_common(torus_comm* c) {
   const size_t n_ep = (size_t)c->nlocal * c->G + c->nlocal;
   CU(cudaMalloc(&c->d_epochs, n_ep * sizeof(uint32_t)));
@@ -612,6 +622,83 @@ int torus_vallreduce(torus_comm_t c, void* const* bufs, size_t count, torus_dtyp
   if (!c || !bufs) return fail(TORUS_ERR_INVALID_ARG, "null argument");
   if (!c->virt) return fail(TORUS_ERR_INVALID_ARG, "not a virtual comm");
   return allreduce_impl(c, bufs, count, dtype, wire, op, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+namespace {
+
+int ring_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, int wire, int op,
+              cudaStream_t stream) {
+  if (!c) return fail(TORUS_ERR_INVALID_ARG, "comm is NULL");
+  if (!valid_pair(dtype, wire))
+    return valid_dtype(dtype) && valid_dtype(wire)
+               ? fail(TORUS_ERR_UNSUPPORTED, "dtype %d with wire %d", dtype, wire)
+               : fail(TORUS_ERR_INVALID_ARG, "bad dtype/wire code");
+  if (op != TORUS_SUM && op != TORUS_MEAN) return fail(TORUS_ERR_INVALID_ARG, "bad op %d", op);
+  if (c->poisoned || *reinterpret_cast<volatile int*>(c->h_err)) {
+    c->poisoned = true;
+    return fail(TORUS_ERR_TIMEOUT, "communicator has an async error; destroy it");
+  }
+  if (count == 0) return TORUS_OK;
+  const size_t esz = wire_size(dtype);
+  bool aligned = true;
+  for (int l = 0; l < c->nlocal; ++l) {
+    if (!bufs[l]) return fail(TORUS_ERR_INVALID_ARG, "buffer %d is NULL", l);
+    const uintptr_t p = reinterpret_cast<uintptr_t>(bufs[l]);
+    if (p % esz) return fail(TORUS_ERR_INVALID_ARG, "buffer %d not element-aligned", l);
+    if (p % kVecBytes) aligned = false;
+  }
+  if (c->world == 1) {
+    if (dtype == wire) return TORUS_OK;
+    cudaError_t e = launch_castscale(bufs[0], count, dtype, wire, stream);
+    return e == cudaSuccess ? TORUS_OK : cuda_fail(e, "castscale launch");
+  }
+  const unsigned long long R = ring_round_elems(c, wire), sw = wire_size(wire);
+  if (R == 0) return fail(TORUS_ERR_INVALID_ARG, "workspace too small for the ring");
+  LaunchArgs a;
+  memset(&a, 0, sizeof a);
+  a.ranks = c->d_ranks;
+  for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];
+  a.nlocal = c->nlocal;
+  a.G = c->G;
+  a.q = (int)(kVecBytes / sw);
+  a.op = op;
+  a.inv_n = 1.0f / (float)c->world;
+  a.aligned = aligned ? 1 : 0;
+  a.timeout_ns = c->timeout_ns;
+  a.hin_off = c->layout.data_off;
+  a.hin_stride = (R / (unsigned long long)c->world) * sw;  // one chunk slot
+  for (unsigned long long r0 = 0; r0 < count; r0 += R) {
+    a.n = std::min<unsigned long long>(R, count - r0);
+    a.buf_off = r0;
+    cudaError_t e = launch_ring(a, dtype, wire, c->virt, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "ring kernel launch");
+  }
+  return TORUS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int torus_ring_allreduce(torus_comm_t c, void* buf, size_t count, torus_dtype_t dtype,
+                         torus_dtype_t wire, torus_op_t op, torus_stream_t stream) {
+  if (c && c->virt) return fail(TORUS_ERR_INVALID_ARG, "virtual comm: use torus_vring_allreduce");
+  void* bufs[1] = {buf};
+  return ring_impl(c, bufs, count, dtype, wire, op, static_cast<cudaStream_t>(stream));
+}
+
+int torus_vring_allreduce(torus_comm_t c, void* const* bufs, size_t count, torus_dtype_t dtype,
+                          torus_dtype_t wire, torus_op_t op, torus_stream_t stream) {
+  if (!c || !bufs) return fail(TORUS_ERR_INVALID_ARG, "null argument");
+  if (!c->virt) return fail(TORUS_ERR_INVALID_ARG, "not a virtual comm");
+  return ring_impl(c, bufs, count, dtype, wire, op, static_cast<cudaStream_t>(stream));
+}
+
+size_t torus_comm_ring_round_elems(torus_comm_t c, torus_dtype_t wire) {
+  if (!c || !valid_dtype(wire)) return 0;
+  return (size_t)ring_round_elems(c, wire);
 }
 
 }  // extern "C"

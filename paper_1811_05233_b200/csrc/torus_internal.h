@@ -134,6 +134,7 @@ cudaError_t launch_castscale(void* buf, unsigned long long n, int dtype, int wir
 cudaError_t launch_barrier(const RankDev* ranks, int nlocal, unsigned long long bar_off,
                            unsigned long long timeout_ns, cudaStream_t stream);
 int torus_kernel_max_ctas_per_sm(int dtype, int wire);
+cudaError_t launch_ring(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
 cudaError_t launch_probe(const RankDev* ranks, unsigned long long data_off, unsigned long long bytes,
                          int mode, int iters, int ctas, unsigned long long* out, cudaStream_t stream);
 

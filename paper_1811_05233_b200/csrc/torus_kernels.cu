@@ -1595,3 +1595,148 @@ cudaError_t launch_probe(const RankDev* ranks, unsigned long long data_off, unsi
 }
 
 }  // namespace torus
+
+// ------------------------------------------------------------------------------------
+// Flat ring all-reduce (baseline, PAPER.md:66-70 and its ref [14]): N-1
+// reduce-scatter steps then N-1 all-gather steps around the rank ring, HOP policy (every
+// message rounded to the wire type, as an NCCL ring does).  Not the product path: it
+// exists so the torus can be compared against the ring it replaces (config 3).
+// Workspace: 2(N-1) slots of one chunk (RS steps, then AG steps), never reused within a
+// call; flag kinds H (RS step s) / R (AG step t), source index = step.
+// ------------------------------------------------------------------------------------
+namespace torus {
+namespace {
+
+template <int DT, int W>
+__global__ void __launch_bounds__(512, 1) ring_kernel(const LaunchArgs a) {
+  using Acc = typename Wire<W>::Acc;
+  constexpr int VE = Wire<W>::VE;
+  constexpr int SW = kVecBytes / VE;
+  const int lr = blockIdx.x / a.G;
+  const int b = blockIdx.x - lr * a.G;
+  const RankDev* __restrict__ R = a.ranks + lr;
+  const int N = R->N, p = R->rank, G = a.G, q = a.q, tid = threadIdx.x;
+  const int next = (p + 1) % N;
+  const unsigned long long n = a.n;
+  const bool aligned = a.aligned != 0;
+  void* const buf = a.buf[lr];
+  char* const myws = R->ws[p];
+  const unsigned long long slot_bytes = a.hin_stride;  // one chunk of wire data
+
+  __shared__ uint32_t s_e;
+  __shared__ int s_abort;
+  if (tid == 0) {
+    s_e = R->epoch[b] + 1u;
+    s_abort = 0;
+  }
+  __syncthreads();
+  const uint32_t e = s_e;
+  const unsigned long long deadline = gtimer() + a.timeout_ns;
+  auto flag = [&](char* ws, int kind, int step) -> uint32_t* {
+    return reinterpret_cast<uint32_t*>(ws) + ((size_t)(kind * kMaxDim + step) * G + b);
+  };
+  auto slot = [&](char* ws, int kind, int step) -> char* {
+    return ws + a.hin_off + ((size_t)kind * (N - 1) + step) * slot_bytes;
+  };
+  auto wait_prev = [&](int kind, int step) -> bool {
+    if (tid == 0 && !wait_flag_ge(flag(myws, kind, step), e, deadline)) {
+      atomicExch_system(R->err, kErrTimeout);
+      s_abort = 1;
+    }
+    __syncthreads();
+    return s_abort == 0;
+  };
+  auto signal_next = [&](int kind, int step) {
+    __syncthreads();
+    if (tid == 0) st_release_sys(flag(R->ws[next], kind, step), e);
+  };
+  auto slice = [&](int k, unsigned long long* co, unsigned long long* cl, unsigned long long* va,
+                   unsigned long long* vz) {
+    qpart(n, N, q, k, co, cl);
+    const unsigned long long nv = (*cl + VE - 1) / VE;
+    *va = nv * (unsigned long long)b / G;
+    *vz = nv * (unsigned long long)(b + 1) / G;
+  };
+
+  // ---- reduce-scatter: at step s send the partial of chunk (p - s - 1) mod N ----
+  for (int s = 0; s <= N - 1; ++s) {
+    const int k = ((p - s - 1) % N + N) % N;  // s == N-1: k == p, my finished chunk
+    unsigned long long co, cl, va, vz;
+    slice(k, &co, &cl, &va, &vz);
+    if (s > 0 && !wait_prev(0, s - 1)) return;
+    const char* in = slot(myws, 0, s - 1 < 0 ? 0 : s - 1);
+    for (unsigned long long v = va + tid; v < vz; v += blockDim.x) {
+      const unsigned long long el = v * VE;
+      const int nrem = (int)min((unsigned long long)VE, cl - el);
+      const uint4 own = load_user<DT, W>(buf, a.buf_off + co + el, nrem, aligned);
+      Acc acc[VE];
+      unpack<W>(own, acc);
+      if (s > 0) {  // partial = incoming message + my own contribution
+        Acc t[VE];
+        unpack<W>(ld_ws(in + el * SW), t);
+        acc_add<W>(t, acc);
+#pragma unroll
+        for (int i = 0; i < VE; ++i) acc[i] = t[i];
+      }
+      if (s < N - 1) {
+        st_ws(slot(R->ws[next], 0, s) + el * SW, pack<W>(acc));  // HOP: the message is rounded
+      } else {
+        if (a.op == 1) acc_mean<W>(acc, a.inv_n, N);
+        const uint4 out = pack<W>(acc);
+        store_user<DT, W>(buf, a.buf_off + co + el, nrem, out, aligned);
+        if (N > 1) st_ws(slot(R->ws[next], 1, 0) + el * SW, out);  // all-gather step 0
+      }
+    }
+    if (s < N - 1) signal_next(0, s);
+  }
+  if (N > 1) signal_next(1, 0);
+  // ---- all-gather: at step t forward chunk (p - t) mod N, received at step t-1 ----
+  for (int t = 1; t <= N - 1; ++t) {
+    const int k = ((p - t) % N + N) % N;
+    unsigned long long co, cl, va, vz;
+    slice(k, &co, &cl, &va, &vz);
+    if (!wait_prev(1, t - 1)) return;
+    const char* in = slot(myws, 1, t - 1);
+    for (unsigned long long v = va + tid; v < vz; v += blockDim.x) {
+      const unsigned long long el = v * VE;
+      const int nrem = (int)min((unsigned long long)VE, cl - el);
+      const uint4 w = ld_ws(in + el * SW);
+      store_user<DT, W>(buf, a.buf_off + co + el, nrem, w, aligned);
+      if (t < N - 1) st_ws(slot(R->ws[next], 1, t) + el * SW, w);
+    }
+    if (t < N - 1) signal_next(1, t);
+  }
+  __syncthreads();
+  if (tid == 0) R->epoch[b] = e;
+}
+
+template <int DT, int W>
+cudaError_t launch_ring_typed(const LaunchArgs& a, bool cooperative, cudaStream_t stream) {
+  const dim3 grid(a.nlocal * a.G), block(512);
+  if (cooperative) {
+    void* args[] = {const_cast<LaunchArgs*>(&a)};
+    return cudaLaunchCooperativeKernel((const void*)ring_kernel<DT, W>, grid, block, args, 0, stream);
+  }
+  ring_kernel<DT, W><<<grid, block, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_ring(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream) {
+  if (dtype == wire) {
+    switch (dtype) {
+      case DT_F32: return launch_ring_typed<DT_F32, DT_F32>(a, cooperative, stream);
+      case DT_F16: return launch_ring_typed<DT_F16, DT_F16>(a, cooperative, stream);
+      case DT_BF16: return launch_ring_typed<DT_BF16, DT_BF16>(a, cooperative, stream);
+      case DT_I32: return launch_ring_typed<DT_I32, DT_I32>(a, cooperative, stream);
+    }
+  } else if (dtype == DT_F32 && wire == DT_F16) {
+    return launch_ring_typed<DT_F32, DT_F16>(a, cooperative, stream);
+  } else if (dtype == DT_F32 && wire == DT_BF16) {
+    return launch_ring_typed<DT_F32, DT_BF16>(a, cooperative, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace torus

@@ -99,6 +99,9 @@ class _CommBase:
     def round_elems(self, wire: torch.dtype) -> int:
         return _lib.load().torus_comm_round_elems(self._comm, _dtype_code(wire))
 
+    def ring_round_elems(self, wire: torch.dtype) -> int:
+        return _lib.load().torus_comm_ring_round_elems(self._comm, _dtype_code(wire))
+
     def launches(self, count: int, dtype: torch.dtype, wire: torch.dtype | None = None) -> int:
         return _lib.load().torus_comm_launches(self._comm, count, _dtype_code(dtype),
                                                _dtype_code(wire or dtype))
@@ -178,6 +181,17 @@ class TorusComm(_CommBase):
         return t
 
 
+    def ring_all_reduce(self, t: torch.Tensor, op: str = "mean", wire: torch.dtype | None = None,
+                        stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """The flat-ring BASELINE (torus_ring_allreduce), same semantics, HOP rounding."""
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("ring all_reduce needs a contiguous CUDA tensor")
+        check(_lib.load().torus_ring_allreduce(
+            self._comm, ctypes.c_void_p(t.data_ptr()), t.numel(), _dtype_code(t.dtype),
+            _dtype_code(wire or t.dtype), OPS[op], _stream_ptr(stream)), "torus_ring_allreduce")
+        return t
+
+
 class VirtualTorus(_CommBase):
     """A whole X-by-Y grid emulated on one GPU (one cooperative launch per round); runs
     the product kernel with every virtual rank's peer pointers aimed at local slabs."""
@@ -203,4 +217,15 @@ class VirtualTorus(_CommBase):
         check(_lib.load().torus_vallreduce(
             self._comm, ptrs, t0.numel(), _dtype_code(t0.dtype), _dtype_code(wire or t0.dtype),
             OPS[op], _stream_ptr(stream)), "torus_vallreduce")
+        return tensors
+
+    def ring_all_reduce(self, tensors: Sequence[torch.Tensor], op: str = "mean",
+                        wire: torch.dtype | None = None,
+                        stream: torch.cuda.Stream | None = None) -> Sequence[torch.Tensor]:
+        """Flat-ring baseline over the virtual ranks (torus_vring_allreduce)."""
+        t0 = tensors[0]
+        ptrs = (ctypes.c_void_p * self.N)(*[t.data_ptr() for t in tensors])
+        check(_lib.load().torus_vring_allreduce(
+            self._comm, ptrs, t0.numel(), _dtype_code(t0.dtype), _dtype_code(wire or t0.dtype),
+            OPS[op], _stream_ptr(stream)), "torus_vring_allreduce")
         return tensors

@@ -66,18 +66,27 @@ def _worker(rank, world, port, cases, errfile):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         comms = {}
         for (X, Y, dtype, wire, op, D, dist_name) in cases:
-            if (X, Y) not in comms:
-                comms[(X, Y)] = TorusComm.init(X=X, Y=Y)
-            comm = comms[(X, Y)]
+            ring = X == 0  # (0, N, ...) marks the flat-ring baseline over all ranks
+            key = (world, 1) if ring else (X, Y)
+            if key not in comms:
+                comms[key] = TorusComm.init(X=key[0], Y=key[1])
+            comm = comms[key]
             ins = synthetic.make_all(dist_name, D, world, dtype, salt=D % 89)
             t = _to_dev(ins[rank], dtype, f"cuda:{rank}")
             torch.cuda.synchronize()
             dist.barrier()
-            comm.all_reduce(t, op=op, wire=TD[wire])
+            (comm.ring_all_reduce if ring else comm.all_reduce)(t, op=op, wire=TD[wire])
             torch.cuda.synchronize()
             assert comm.async_error() == 0, "watchdog"
             got = _from_dev(t, dtype)
             q = 16 // (2 if wire in ("f16", "bf16") else 4)
+            if ring:
+                ref = oracle.ring_allreduce(ins, dtype, wire=wire, op=op, policy="hop", q=q,
+                                            round_elems=comm.ring_round_elems(TD[wire]))[rank]
+                ok, nbad = _same(got, ref)
+                assert ok, f"rank {rank} ring {dtype}/{wire} {op} D={D}: {nbad} mismatches"
+                dist.barrier()
+                continue
             R = comm.round_elems(TD[wire])
             if D <= 300_000:
                 ref = oracle.torus_allreduce(ins, X, Y, dtype, wire=wire, op=op, q=q,
@@ -129,10 +138,10 @@ def _cases(grids, sizes=(1, 4099, 200_003), ops=("sum", "mean")):
 
 
 def test_two_gpus(tmp_path):
-    _run(2, _cases([(2, 1), (1, 2)]), tmp_path)
+    _run(2, _cases([(2, 1), (1, 2), (0, 2)]), tmp_path)
 
 
 def test_four_gpus(tmp_path):
-    cases = _cases([(2, 2), (4, 1), (1, 4)], ops=("mean",))
+    cases = _cases([(2, 2), (4, 1), (1, 4), (0, 4)], ops=("mean",))
     cases += [(2, 2, "f16", "f16", "mean", 25_557_032, "grad")]  # config 2 shape on 2x2
     _run(4, cases, tmp_path)

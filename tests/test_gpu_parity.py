@@ -250,3 +250,36 @@ def test_errors_are_reported():
         vt.destroy()
     with pytest.raises(TorusError, match="GRID"):
         VirtualTorus(5, 5, device=0)                   # > 16 virtual ranks
+
+
+@pytest.mark.parametrize("N", [2, 3, 4, 8])
+@pytest.mark.parametrize("dtype,wire", PAIRS)
+@pytest.mark.parametrize("op", ["sum", "mean"])
+def test_virtual_ring_baseline_bit_exact(vgrids, N, dtype, wire, op):
+    """The flat-ring BASELINE kernel (ref [14]) vs the oracle's ring with
+    the HOP policy (every message rounded to the wire type)."""
+    vt = vgrids(N, 1)
+    R = vt.ring_round_elems(TD[wire])
+    for D in (1, 1000, 4099, 100_003):
+        ins = synthetic.make_all("full" if dtype == "i32" else "normal", D, N, dtype, salt=D % 7)
+        ts = [_np_to_dev(a, dtype) for a in ins]
+        vt.ring_all_reduce(ts, op=op, wire=TD[wire])
+        torch.cuda.synchronize()
+        assert vt.async_error() == 0
+        ref = oracle.ring_allreduce(ins, dtype, wire=wire, op=op, policy="hop", q=q_of(wire),
+                                    round_elems=R)
+        for r in range(N):
+            assert_same(from_dev(ts[r], dtype), ref[r], f"ring N={N} {dtype}/{wire} {op} D={D} rank {r}")
+
+
+def test_ring_multi_round(vgrids):
+    vt = vgrids(4, 1, ws=1 << 20)
+    R = vt.ring_round_elems(torch.float16)
+    D = 2 * R + 999
+    ins = synthetic.make_all("normal", D, 4, "f16")
+    ts = [_np_to_dev(a, "f16") for a in ins]
+    vt.ring_all_reduce(ts, op="mean")
+    torch.cuda.synchronize()
+    ref = oracle.ring_allreduce(ins, "f16", op="mean", policy="hop", q=8, round_elems=R)
+    for r in range(4):
+        assert_same(from_dev(ts[r], "f16"), ref[r], f"ring rounds rank {r}")
