@@ -123,6 +123,21 @@ TORUS_API int torus_allreduce_ex(torus_comm_t comm, void* buf, size_t count, tor
 TORUS_API int torus_vallreduce(torus_comm_t comm, void* const* bufs, size_t count, torus_dtype_t dtype,
                      torus_dtype_t wire, torus_op_t op, torus_stream_t stream);
 
+/* Bucketed multi-tensor all-reduce (NEXT-1, BASELINE.json config 5: "layer-bucketed
+ * ResNet-50 gradients (161 tensors fused into buckets) fp16 with fused cast/scale").
+ * ptrs / counts: HOST arrays [ntensors] of device pointers and element counts.  The
+ * result equals torus_allreduce_ex on the concatenation of the tensors (same partition,
+ * fold order and rounding): a fused pack kernel casts dtype -> wire into the comm's
+ * staging buffer, the torus kernel reduces it (mean applied once), a fused unpack kernel
+ * casts back.  The staging buffer grows on the first call with a larger bucket (that
+ * call allocates and synchronizes; reserve it up front with torus_comm_reserve to keep
+ * every call capturable).  Concurrent buckets need one comm each, with CTA budgets that
+ * sum to at most the SM count (spin-waiting kernels of different comms must co-reside). */
+TORUS_API int torus_allreduce_multi(torus_comm_t comm, void* const* ptrs, const size_t* counts,
+                                    int ntensors, torus_dtype_t dtype, torus_dtype_t wire,
+                                    torus_op_t op, torus_stream_t stream);
+TORUS_API int torus_comm_reserve(torus_comm_t comm, size_t staging_bytes);
+
 /* Flat ring all-reduce over the rank ring 0 -> 1 -> ... -> N-1 -> 0 -- the BASELINE the
  * torus replaces ("Ring all-reduce scheme executes 2(N-1) GPU-to-GPU
  * operations", ref [14]).  N-1 reduce-scatter then N-1 all-gather steps, each a push

@@ -93,6 +93,8 @@ struct torus_comm {
   unsigned long long* d_trace = nullptr;  // TORUS_TRACE=1: [G][kTraceIters][kTraceEvents]
   uint32_t* d_done_local = nullptr;       // TMA kernel: [nlocal][G][8] stage tiles done
   uint32_t* d_sig_ack = nullptr;          // TMA kernel: [nlocal][G] signal-lane acks
+  void* d_staging = nullptr;              // multi-tensor staging buffer (wire type)
+  size_t staging_bytes = 0;
 };
 
 namespace {
@@ -195,6 +197,7 @@ void destroy_resources(torus_comm* c) {
   if (c->d_trace) cudaFree(c->d_trace);
   if (c->d_done_local) cudaFree(c->d_done_local);
   if (c->d_sig_ack) cudaFree(c->d_sig_ack);
+  if (c->d_staging) cudaFree(c->d_staging);
   if (c->h_err) cudaFreeHost(c->h_err);
   delete c;
 }
@@ -699,6 +702,77 @@ int torus_vring_allreduce(torus_comm_t c, void* const* bufs, size_t count, torus
 size_t torus_comm_ring_round_elems(torus_comm_t c, torus_dtype_t wire) {
   if (!c || !valid_dtype(wire)) return 0;
   return (size_t)ring_round_elems(c, wire);
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int torus_comm_reserve(torus_comm_t c, size_t staging_bytes) {
+  if (!c) return fail(TORUS_ERR_INVALID_ARG, "comm is NULL");
+  if (staging_bytes <= c->staging_bytes) return TORUS_OK;
+  CU(cudaSetDevice(c->device));
+  if (c->d_staging) {
+    CU(cudaDeviceSynchronize());
+    cudaFree(c->d_staging);
+    c->d_staging = nullptr;
+    c->staging_bytes = 0;
+  }
+  const size_t b = (staging_bytes + 65535) & ~(size_t)65535;
+  CU(cudaMalloc(&c->d_staging, b));
+  c->staging_bytes = b;
+  return TORUS_OK;
+}
+
+int torus_allreduce_multi(torus_comm_t c, void* const* ptrs, const size_t* counts, int ntensors,
+                          torus_dtype_t dtype, torus_dtype_t wire, torus_op_t op,
+                          torus_stream_t stream) {
+  if (!c || (ntensors > 0 && (!ptrs || !counts))) return fail(TORUS_ERR_INVALID_ARG, "null argument");
+  if (c->virt) return fail(TORUS_ERR_INVALID_ARG, "virtual comm: not supported for multi");
+  if (ntensors < 0) return fail(TORUS_ERR_INVALID_ARG, "ntensors < 0");
+  if (!valid_pair(dtype, wire)) return fail(TORUS_ERR_UNSUPPORTED, "dtype %d with wire %d", dtype, wire);
+  size_t total = 0;
+  const size_t esz = wire_size(dtype);
+  for (int i = 0; i < ntensors; ++i) {
+    if (counts[i] && !ptrs[i]) return fail(TORUS_ERR_INVALID_ARG, "tensor %d is NULL", i);
+    if (reinterpret_cast<uintptr_t>(ptrs[i]) % esz) return fail(TORUS_ERR_INVALID_ARG, "tensor %d misaligned", i);
+    total += counts[i];
+  }
+  if (total == 0) return TORUS_OK;
+  const size_t need = total * wire_size(wire) + 256;
+  if (need > c->staging_bytes) {
+    int rc = torus_comm_reserve(c, need);  // first use of a larger bucket allocates
+    if (rc) return rc;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  MultiTable tab;
+  size_t off = 0;
+  for (int i0 = 0; i0 < ntensors; i0 += kMultiMax) {  // pack: dtype -> wire (RNE)
+    const int n = std::min(kMultiMax, ntensors - i0);
+    for (int i = 0; i < n; ++i) {
+      tab.ptr[i] = ptrs[i0 + i];
+      tab.count[i] = counts[i0 + i];
+      tab.offset[i] = off;
+      off += counts[i0 + i];
+    }
+    cudaError_t e = launch_multi_copy(tab, n, dtype, wire, c->d_staging, true, s);
+    if (e != cudaSuccess) return cuda_fail(e, "multi pack");
+  }
+  int rc = torus_allreduce_ex(c, c->d_staging, total, wire, wire, op, stream);
+  if (rc) return rc;
+  off = 0;
+  for (int i0 = 0; i0 < ntensors; i0 += kMultiMax) {  // unpack: wire -> dtype (exact)
+    const int n = std::min(kMultiMax, ntensors - i0);
+    for (int i = 0; i < n; ++i) {
+      tab.ptr[i] = ptrs[i0 + i];
+      tab.count[i] = counts[i0 + i];
+      tab.offset[i] = off;
+      off += counts[i0 + i];
+    }
+    cudaError_t e = launch_multi_copy(tab, n, dtype, wire, c->d_staging, false, s);
+    if (e != cudaSuccess) return cuda_fail(e, "multi unpack");
+  }
+  return TORUS_OK;
 }
 
 }  // extern "C"

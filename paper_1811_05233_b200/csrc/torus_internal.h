@@ -126,6 +126,15 @@ inline size_t flags_bytes_for(int G) {
   return (b + 65535) & ~(size_t)65535;
 }
 
+// Multi-tensor table passed by value (kernel parameter space): up to kMultiMax tensors
+// per launch (161 ResNet-50 tensors fit in two).
+constexpr int kMultiMax = 96;
+struct MultiTable {
+  void* ptr[kMultiMax];
+  unsigned long long count[kMultiMax];
+  unsigned long long offset[kMultiMax];  // element offset in the staging buffer
+};
+
 // ---- launch wrappers implemented in torus_kernels.cu ----
 cudaError_t launch_torus(const LaunchArgs& a, int dtype, int wire, bool cooperative,
                          cudaStream_t stream);
@@ -135,6 +144,8 @@ cudaError_t launch_barrier(const RankDev* ranks, int nlocal, unsigned long long 
                            unsigned long long timeout_ns, cudaStream_t stream);
 int torus_kernel_max_ctas_per_sm(int dtype, int wire);
 cudaError_t launch_ring(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
+cudaError_t launch_multi_copy(const MultiTable& tab, int n, int dtype, int wire, void* staging,
+                              bool pack, cudaStream_t stream);
 cudaError_t launch_probe(const RankDev* ranks, unsigned long long data_off, unsigned long long bytes,
                          int mode, int iters, int ctas, unsigned long long* out, cudaStream_t stream);
 

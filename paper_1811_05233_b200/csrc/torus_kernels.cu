@@ -1740,3 +1740,67 @@ cudaError_t launch_ring(const LaunchArgs& a, int dtype, int wire, bool cooperati
 }
 
 }  // namespace torus
+
+// ------------------------------------------------------------------------------------
+// Multi-tensor pack / unpack (NEXT-1, BASELINE.json config 5): the bucket's tensors are
+// concatenated in order into a wire-typed staging buffer (cast fused, round to nearest
+// even) and scattered back (up-cast fused) -- exactly the all-reduce of the concatenated
+// buffer with dtype -> wire conversion on the first read and back on the last write.
+// The tensor table travels in the kernel parameters (no host->device copy per call).
+// ------------------------------------------------------------------------------------
+namespace torus {
+namespace {
+
+template <int DT, int W, bool PACK>
+__global__ void __launch_bounds__(256) multi_copy_kernel(const MultiTable tab, void* staging) {
+  using UT = typename Elem<DT>::T;
+  using WT = typename Elem<W>::T;
+  const int t = blockIdx.y;
+  const unsigned long long n = tab.count[t];
+  UT* user = reinterpret_cast<UT*>(tab.ptr[t]);
+  WT* st = reinterpret_cast<WT*>(staging) + tab.offset[t];
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    if constexpr (PACK) {
+      if constexpr (DT == W) st[i] = user[i];
+      else if constexpr (W == DT_F16) st[i] = __float2half_rn(user[i]);
+      else st[i] = __float2bfloat16_rn(user[i]);
+    } else {
+      if constexpr (DT == W) user[i] = st[i];
+      else user[i] = static_cast<float>(st[i]);  // exact
+    }
+  }
+}
+
+template <int DT, int W>
+cudaError_t launch_multi_typed(const MultiTable& tab, int n, void* staging, bool pack, cudaStream_t s) {
+  unsigned long long mx = 1;
+  for (int i = 0; i < n; ++i) mx = tab.count[i] > mx ? tab.count[i] : mx;
+  const unsigned gx = (unsigned)((mx + 255) / 256 < 296 ? (mx + 255) / 256 : 296);
+  const dim3 grid(gx, n);
+  if (pack) multi_copy_kernel<DT, W, true><<<grid, 256, 0, s>>>(tab, staging);
+  else multi_copy_kernel<DT, W, false><<<grid, 256, 0, s>>>(tab, staging);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_multi_copy(const MultiTable& tab, int n, int dtype, int wire, void* staging,
+                              bool pack, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  if (dtype == wire) {
+    switch (dtype) {
+      case DT_F32: return launch_multi_typed<DT_F32, DT_F32>(tab, n, staging, pack, stream);
+      case DT_F16: return launch_multi_typed<DT_F16, DT_F16>(tab, n, staging, pack, stream);
+      case DT_BF16: return launch_multi_typed<DT_BF16, DT_BF16>(tab, n, staging, pack, stream);
+      case DT_I32: return launch_multi_typed<DT_I32, DT_I32>(tab, n, staging, pack, stream);
+    }
+  } else if (dtype == DT_F32 && wire == DT_F16) {
+    return launch_multi_typed<DT_F32, DT_F16>(tab, n, staging, pack, stream);
+  } else if (dtype == DT_F32 && wire == DT_BF16) {
+    return launch_multi_typed<DT_F32, DT_BF16>(tab, n, staging, pack, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace torus

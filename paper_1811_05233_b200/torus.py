@@ -145,7 +145,7 @@ class TorusComm(_CommBase):
 
     @classmethod
     def init(cls, group=None, X: int = 0, Y: int = 0, ws_bytes: int = 0,
-             device: int | None = None) -> "TorusComm":
+             device: int | None = None, ctas: int = 0) -> "TorusComm":
         """Collective: every rank of `group` allocates and exports its slab, the 64-byte
         IPC handles are all-gathered in rank order, every rank opens its peers' slabs,
         and all ranks agree on success (no half-built communicator survives)."""
@@ -159,7 +159,18 @@ class TorusComm(_CommBase):
         check(L.torus_workspace_alloc(dev, ws_bytes, ctypes.byref(h)), "torus_workspace_alloc")
         arr = handles_array(exchange_blobs(bytes(h), world, group))
         comm = ctypes.c_void_p()
-        rc = L.torus_comm_init(rank, world, X, Y, arr, ctypes.byref(comm))
+        import os
+        old = os.environ.get("TORUS_CTAS")
+        if ctas:  # CTA budget (concurrent comms must fit on the SMs together)
+            os.environ["TORUS_CTAS"] = str(ctas)
+        try:
+            rc = L.torus_comm_init(rank, world, X, Y, arr, ctypes.byref(comm))
+        finally:
+            if ctas:
+                if old is None:
+                    del os.environ["TORUS_CTAS"]
+                else:
+                    os.environ["TORUS_CTAS"] = old
         msg = "" if rc == 0 else L.torus_last_error().decode(errors="replace")
         bad = agree_status(rc, msg, world, group)
         if bad:
@@ -180,6 +191,28 @@ class TorusComm(_CommBase):
             _dtype_code(wire or t.dtype), OPS[op], _stream_ptr(stream)), "torus_allreduce_ex")
         return t
 
+
+    def reserve(self, staging_bytes: int) -> None:
+        check(_lib.load().torus_comm_reserve(self._comm, staging_bytes), "torus_comm_reserve")
+
+    def all_reduce_multi(self, tensors: Sequence[torch.Tensor], op: str = "mean",
+                         wire: torch.dtype | None = None,
+                         stream: torch.cuda.Stream | None = None) -> Sequence[torch.Tensor]:
+        """Bucketed all-reduce of a list of same-dtype contiguous CUDA tensors (NEXT-1):
+        equal to all-reducing their concatenation, cast/scale fused."""
+        if not tensors:
+            return tensors
+        dt = tensors[0].dtype
+        for t in tensors:
+            if not t.is_cuda or not t.is_contiguous() or t.dtype != dt:
+                raise ValueError("all_reduce_multi needs contiguous CUDA tensors of one dtype")
+        n = len(tensors)
+        ptrs = (ctypes.c_void_p * n)(*[t.data_ptr() for t in tensors])
+        counts = (ctypes.c_size_t * n)(*[t.numel() for t in tensors])
+        check(_lib.load().torus_allreduce_multi(
+            self._comm, ptrs, counts, n, _dtype_code(dt), _dtype_code(wire or dt), OPS[op],
+            _stream_ptr(stream)), "torus_allreduce_multi")
+        return tensors
 
     def ring_all_reduce(self, t: torch.Tensor, op: str = "mean", wire: torch.dtype | None = None,
                         stream: torch.cuda.Stream | None = None) -> torch.Tensor:

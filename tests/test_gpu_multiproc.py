@@ -145,3 +145,56 @@ def test_four_gpus(tmp_path):
     cases = _cases([(2, 2), (4, 1), (1, 4), (0, 4)], ops=("mean",))
     cases += [(2, 2, "f16", "f16", "mean", 25_557_032, "grad")]  # config 2 shape on 2x2
     _run(4, cases, tmp_path)
+
+
+def _multi_worker(rank, world, port, errfile):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    try:
+        import torch.distributed as dist
+
+        import oracle
+        import synthetic
+        from paper_1811_05233_b200 import TorusComm
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        comm = TorusComm.init(X=world, Y=1)
+        # a ResNet-50-shaped bucket: the 40 smallest-to-mid layers (backprop order)
+        sizes = synthetic.resnet50_param_numels()[::-1][:40]
+        D = sum(sizes)
+        for wire in ("f16", "bf16"):
+            ins = synthetic.make_all("grad", D, world, "f32", salt=3)
+            full = torch.from_numpy(ins[rank].copy()).cuda()
+            parts = list(torch.split(full.clone(), sizes))
+            parts = [p.contiguous() for p in parts]
+            torch.cuda.synchronize()
+            dist.barrier()
+            comm.all_reduce_multi(parts, op="mean", wire=TD[wire])
+            torch.cuda.synchronize()
+            assert comm.async_error() == 0
+            got = torch.cat(parts).cpu().numpy()
+            ref = oracle.torus_allreduce(ins, world, 1, "f32", wire=wire, op="mean", q=8,
+                                         round_elems=comm.round_elems(TD[wire]))[rank]
+            ok, nbad = _same(got, ref)
+            assert ok, f"rank {rank} multi {wire}: {nbad} mismatches"
+            dist.barrier()
+        dist.barrier()
+        comm.destroy()
+        dist.destroy_process_group()
+    except Exception:
+        with open(errfile, "a") as f:
+            f.write(f"rank {rank}:\n{traceback.format_exc()}\n")
+        raise
+
+
+def test_multi_tensor_bucket_two_gpus(tmp_path):
+    """NEXT-1: the bucketed API equals the all-reduce of the concatenated bucket."""
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    errfile = str(tmp_path / "errors.txt")
+    try:
+        mp.spawn(_multi_worker, args=(2, _free_port(), errfile), nprocs=2, join=True)
+    except Exception as e:
+        raise AssertionError(open(errfile).read() if os.path.exists(errfile) else str(e)) from None

@@ -283,3 +283,23 @@ def test_ring_multi_round(vgrids):
     ref = oracle.ring_allreduce(ins, "f16", op="mean", policy="hop", q=8, round_elems=R)
     for r in range(4):
         assert_same(from_dev(ts[r], "f16"), ref[r], f"ring rounds rank {r}")
+
+
+def test_multi_tensor_single_rank():
+    """NEXT-1 at N = 1: pack (f32 -> f16/bf16 RNE) and unpack (exact) around the degenerate
+    cast pass equal the oracle on the concatenation."""
+    from paper_1811_05233_b200 import TorusComm
+    comm = TorusComm.init()
+    try:
+        sizes = synthetic.resnet50_param_numels()[:30]
+        D = sum(sizes)
+        x = synthetic.make("wide", D, 0, "f32")
+        for wire in ("f16", "bf16", "f32"):
+            parts = [p.contiguous() for p in torch.split(torch.from_numpy(x.copy()).cuda(), sizes)]
+            comm.all_reduce_multi(parts, op="mean", wire=TD[wire])
+            torch.cuda.synchronize()
+            got = torch.cat(parts).cpu().numpy()
+            ref = oracle.torus_allreduce([x], 1, 1, "f32", wire=wire, op="mean")[0]
+            assert_same(got, ref, f"multi N=1 {wire}")
+    finally:
+        comm.destroy()
