@@ -77,7 +77,6 @@ def main():
 
     def nccl_step():
         for bi, b in enumerate(bks):
-            torch.cat([grads[i] for i in b]).to(torch.float16, out=None)
             flat16[bi].copy_(torch.cat([grads[i] for i in b]))
             dist.all_reduce(flat16[bi], op=dist.ReduceOp.AVG)
             off = 0
