@@ -411,7 +411,11 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
     kinds[P++] = kD;
   }
   if (X > 1) kinds[P++] = kE;
-  const int iters = T + 2 * (P - 1);
+  // Stage distance: 2 (flags hide behind an iteration of data) when the call has several
+  // tiles; 1 for single-tile (small) calls, where latency is all there is -- each stage
+  // then waits on the previous one directly and the control warp raises before it polls.
+  const int SD = (T == 1) ? 1 : 2;
+  const int iters = T + SD * (P - 1);
 
   if (tid < kCtrlThreads) {
     // =============================== control warp ===============================
@@ -459,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
       bool ok = true;
       int e = 0;
       for (int p = 0; p < P; ++p) {
-        const int t = it - 2 * p;
+        const int t = it - SD * p;
         if (t < 0 || t >= T) continue;
         for_flags(kinds[p], t, true, [&](uint32_t* f, uint32_t v) {
           if ((e++ & 31) == lane && ok) ok = wait_flag_ge(f, v, deadline);
@@ -472,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
       asm volatile("fence.acq_rel.sys;" ::: "memory");
       int e = 0;
       for (int p = 0; p < P; ++p) {
-        const int t = it - 2 * p;
+        const int t = it - SD * p;
         if (t < 0 || t >= T) continue;
         for_flags(kinds[p], t, false, [&](uint32_t* f, uint32_t v) {
           if ((e++ & 31) == lane) st_relaxed_sys(f, v);
@@ -482,9 +486,13 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
     unsigned long long* const tr = (lane == 0 && lr == 0) ? a.trace : nullptr;
     for (int it = 0; it < iters; ++it) {
       stamp(tr, b, it, 0);
+      if (SD == 1 && it > 0) {            // latency mode: publish it-1 before waiting on it
+        bar_sync(kBarDone);
+        raise_iter(it - 1);
+      }
       const bool ok = poll_iter(it);      // inputs: raised by peers in iteration <= it-1
       stamp(tr, b, it, 1);
-      if (it > 0) bar_sync(kBarDone);     // workers finished iteration it-1
+      if (SD == 2 && it > 0) bar_sync(kBarDone);  // workers finished iteration it-1
       stamp(tr, b, it, 2);
       if (!ok) {
         if (lane == 0) {
@@ -497,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
       }
       bar_arrive(kBarReady);              // workers start iteration it ...
       stamp(tr, b, it, 3);
-      if (it > 0) raise_iter(it - 1);     // ... while the fence for it-1 drains
+      if (SD == 2 && it > 0) raise_iter(it - 1);  // ... while the fence for it-1 drains
       stamp(tr, b, it, 4);
     }
     bar_sync(kBarDone);
@@ -511,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) 
       stamp(tr, b, it, 5);
       if (*(volatile int*)&s_abort) return;
       for (int p = 0; p < P; ++p) {
-        const int t = it - 2 * p;
+        const int t = it - SD * p;
         if (t < 0 || t >= T) continue;
         const int k = kinds[p];
         if (k == kA) {
