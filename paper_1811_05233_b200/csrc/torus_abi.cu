@@ -355,7 +355,7 @@ int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t*
   c->own_slabs.push_back(own.ptr);
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
   { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
-  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", c->tma ? 512 : 3840));
+  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", 3840));
   int rc = TORUS_OK;
   std::vector<char*> bases(world, nullptr);
   if (cudaSetDevice(c->device) != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "cudaSetDevice");
@@ -410,7 +410,7 @@ int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_
   c->slab_size = (ws_bytes + 65535) & ~(size_t)65535;
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
   { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
-  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", c->tma ? 512 : 3840));
+  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", 3840));
   if (ctas > 0) setenv("TORUS_CTAS", std::to_string(ctas).c_str(), 1);
   c->G = pick_ctas(device, c->nlocal);
   c->layout = make_layout(c->slab_size, c->G);
@@ -576,15 +576,15 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   a.sig_ack = c->d_sig_ack;
   a.nsig = c->tma ? (c->nlocal * c->G + kThreads - 1) / kThreads : 0;
   if (c->tma) {
-    // ring buffers of one piece each: jobs in flight across the producer, the consumers
-    // and the 8 storer lanes; the largest job holds max(X,Y)+3 at once -- keep room for
-    // a few of those so the producer runs ahead
+    // ring buffers of one chunk each (tile pieces stream through in chunks): the largest
+    // job holds max(X,Y)+3 buffers at once -- keep room for a few so the producer runs
+    // ahead; shrink the chunk until that fits
     const int ratio = (int)(wire_size(dtype) / sw);
     const int need = 3 * (std::max(c->X, c->Y) + 3) + 4;
-    int tv = a.tile_vecs;
-    while (tv > 32 && kTmaSmemMax / (tma_buf_bytes(tv, ratio) + 24) < need) tv /= 2;
-    a.tile_vecs = tv;
-    a.nbufs = std::min(64, kTmaSmemMax / (tma_buf_bytes(tv, ratio) + 24));
+    int cv = std::min(a.tile_vecs, 1024);
+    while (cv > 32 && kTmaSmemMax / (tma_buf_bytes(cv, ratio) + 24) < need) cv /= 2;
+    a.chunk_vecs = cv;
+    a.nbufs = std::min(64, kTmaSmemMax / (tma_buf_bytes(cv, ratio) + 24));
     if (a.nbufs < need) return fail(TORUS_ERR_UNSUPPORTED, "grid %dx%d too large for the TMA ring", c->X, c->Y);
   }
   const unsigned long long Lc = R / c->X, Lcs = R / ((unsigned long long)c->X * c->Y);

@@ -78,6 +78,8 @@ struct LaunchArgs {
   uint32_t* done_local;          // [nlocal * G * 8]
   uint32_t* sig_ack;             // [nlocal * G]
   int nsig;                      // signal CTAs appended after the nlocal * G data CTAs
+  int chunk_vecs;                // TMA kernel: vectors per ring buffer (a tile piece is
+                                 // streamed through the ring in chunks of this size)
 };
 
 // TMA kernel shared memory: nbufs ring buffers of one piece each (tile_vecs 16-byte wire

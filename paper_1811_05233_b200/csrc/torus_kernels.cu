@@ -815,7 +815,8 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
   extern __shared__ __align__(1024) unsigned char smem[];
   const int NB = a.nbufs;
   const int TV = a.tile_vecs;
-  const unsigned PB = (unsigned)TV * VE * (ST > SW ? ST : SW);  // one piece, user or wire
+  const int CV = a.chunk_vecs;  // a tile piece moves through the ring in chunks of CV vectors
+  const unsigned PB = (unsigned)CV * VE * (ST > SW ? ST : SW);  // one chunk, user or wire
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NB * PB);
   uint64_t* empty = full + NB;
   uint64_t* consumed = empty + NB;
@@ -861,8 +862,19 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
   if (X > 1) kinds[P++] = kE;
   const int iters = T + 2 * (P - 1);
 
-  // Jobs of iteration `it` in a fixed order (identical in every role).
-  auto for_jobs = [&](int it, auto visit) {
+  // Jobs of iteration `it` in a fixed order (identical in every role): each tile piece
+  // is cut into chunks of CV vectors, one job per chunk.
+  auto for_jobs = [&](int it, auto visit0) {
+    auto visit = [&](Job& jb) {
+      const unsigned long long p0 = jb.p.p0, p1 = jb.p.p1;
+      for (unsigned long long c0 = p0; c0 < p1; c0 += CV) {
+        jb.p.p0 = c0;
+        jb.p.p1 = (c0 + CV < p1) ? c0 + CV : p1;
+        visit0(jb);
+      }
+      jb.p.p0 = p0;
+      jb.p.p1 = p1;
+    };
     for (int pp = 0; pp < P; ++pp) {
       const int t = it - 2 * pp;
       if (t < 0 || t >= T) continue;
@@ -1323,7 +1335,7 @@ cudaError_t launch_typed(const LaunchArgs& a, bool cooperative, cudaStream_t str
   const dim3 grid(a.nlocal * a.G), block(kThreads);
   if (a.nbufs > 0) {  // TMA-staged kernel: data CTAs + signal CTAs
     const dim3 grid(a.nlocal * a.G + a.nsig), block(kThreads);
-    const int smem = tma_smem_bytes(a.nbufs, a.tile_vecs, (int)(sizeof(typename Elem<DT>::T) * Wire<W>::VE / 16));
+    const int smem = tma_smem_bytes(a.nbufs, a.chunk_vecs, (int)(sizeof(typename Elem<DT>::T) * Wire<W>::VE / 16));
     static bool attr_set = false;
     if (!attr_set) {
       cudaError_t e = cudaFuncSetAttribute(torus_tma_kernel<DT, W>,
