@@ -75,7 +75,7 @@ struct torus_comm {
   int rank = 0, world = 1, X = 1, Y = 1;
   int device = 0;
   int G = 0;
-  int tile_vecs = 3840;     // 16-byte vectors per tile piece (env TORUS_TILE)
+  int tile_vecs = 0;        // vectors per tile piece (env TORUS_TILE); 0 = auto
   bool tma = false;         // env TORUS_KERNEL=tma selects the TMA-staged kernel
   int nlocal = 1;           // > 1: virtual ranks on one device
   bool virt = false;
@@ -355,7 +355,7 @@ int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t*
   c->own_slabs.push_back(own.ptr);
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
   { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
-  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", 3840));
+  c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // 0 = auto (T ~ 3 tiles per slice)
   int rc = TORUS_OK;
   std::vector<char*> bases(world, nullptr);
   if (cudaSetDevice(c->device) != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "cudaSetDevice");
@@ -410,7 +410,7 @@ int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_
   c->slab_size = (ws_bytes + 65535) & ~(size_t)65535;
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
   { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
-  c->tile_vecs = (int)std::max<size_t>(1, env_size("TORUS_TILE", 3840));
+  c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // 0 = auto (T ~ 3 tiles per slice)
   if (ctas > 0) setenv("TORUS_CTAS", std::to_string(ctas).c_str(), 1);
   c->G = pick_ctas(device, c->nlocal);
   c->layout = make_layout(c->slab_size, c->G);
@@ -570,6 +570,17 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   a.aligned = aligned ? 1 : 0;
   a.timeout_ns = c->timeout_ns;
   a.tile_vecs = c->tile_vecs;
+  if (a.tile_vecs <= 0) {
+    // auto: about kAutoTiles tiles per CTA slice of the largest sub-chunk (measured best
+    // at 2 and 4 GPUs); small calls get one tile (latency mode)
+    constexpr unsigned long long kAutoTiles = 3;
+    unsigned long long o, l0, s0;
+    qpart(std::min<unsigned long long>(R, count), c->X, (int)(kVecBytes / sw), 0, &o, &l0);
+    qpart(l0, c->Y, (int)(kVecBytes / sw), 0, &o, &s0);
+    const unsigned long long nv = (s0 * sw + kVecBytes - 1) / kVecBytes;
+    const unsigned long long slice = (nv + c->G - 1) / c->G;
+    a.tile_vecs = (int)std::max<unsigned long long>(256, (slice + kAutoTiles - 1) / kAutoTiles);
+  }
   a.trace = c->d_trace;
   a.nbufs = 0;
   a.done_local = c->d_done_local;
