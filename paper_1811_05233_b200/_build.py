@@ -31,18 +31,20 @@ def stale() -> bool:
     return any(p.stat().st_mtime > t for p in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
-    if force or stale():
-        tmp = LIB.with_name(f"libtorus.so.tmp{os.getpid()}")
-        cmd = [NVCC, *FLAGS, *map(str, SOURCES), "-o", str(tmp)]
+def build(force: bool = False, verbose: bool = False, out: pathlib.Path | None = None,
+          defines: tuple[str, ...] = ()) -> pathlib.Path:
+    lib = out or LIB
+    if force or out is not None or stale():
+        tmp = lib.with_name(f"{lib.name}.tmp{os.getpid()}")
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], *map(str, SOURCES), "-o", str(tmp)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
         (PKG / "build_ptxas.log").write_text(res.stderr)
         if verbose:
             print(res.stderr)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -10,7 +10,8 @@ import pathlib
 import threading
 
 _PKG = pathlib.Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libtorus.so"
+import os as _os
+LIB_PATH = pathlib.Path(_os.environ.get("TORUS_LIB_PATH", str(_PKG / "libtorus.so")))
 
 TORUS_OK = 0
 ERRORS = {

@@ -180,7 +180,7 @@ int pick_ctas(int device, int nlocal) {
   for (int d = 0; d < 4; ++d) per_sm = std::min(per_sm, torus_kernel_max_ctas_per_sm(d, d));
   if (per_sm < 1) per_sm = 1;
   const int resident = sms * per_sm;
-  int want = (int)env_size("TORUS_CTAS", nlocal > 1 ? 16 : sms);
+  int want = (int)env_size("TORUS_CTAS", nlocal > 1 ? 16 : sms * per_sm);
   want = std::max(1, want);
   // every CTA of every rank that waits on another must be co-resident
   // the TMA kernel appends one signal CTA on its own SM

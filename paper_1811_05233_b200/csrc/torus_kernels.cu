@@ -329,7 +329,12 @@ __device__ __forceinline__ Piece make_piece(unsigned long long n, int X, int Y, 
 }
 
 constexpr int kCtrlThreads = 32;                     // warp 0: flags, fences, signals
-constexpr int kWorkers = kThreads - kCtrlThreads;    // warps 1..15: data movement
+#ifndef TORUS_LDG_THREADS
+#define TORUS_LDG_THREADS 512
+#endif
+constexpr int kLdgThreads = TORUS_LDG_THREADS;       // threads per CTA of torus_kernel
+constexpr int kLdgCtasPerSm = 512 / TORUS_LDG_THREADS;
+constexpr int kWorkers = kLdgThreads - kCtrlThreads; // warps 1..: data movement
 constexpr int kUnroll = 4;                           // vectors per worker per pass (copies)
 constexpr int kUnrollFold = 2;                       // vectors per worker per pass (folds)
 
@@ -346,10 +351,10 @@ __device__ __forceinline__ void stamp(unsigned long long* tr, int b, int it, int
 constexpr int kBarReady = 1;  // control -> workers: inputs of iteration it are visible
 constexpr int kBarDone = 2;   // workers -> control: iteration it's data is written
 __device__ __forceinline__ void bar_sync(int id) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kThreads) : "memory");
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kLdgThreads) : "memory");
 }
 __device__ __forceinline__ void bar_arrive(int id) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kThreads) : "memory");
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kLdgThreads) : "memory");
 }
 
 // ------------------------------------------------------------------------------------
@@ -371,7 +376,7 @@ __device__ __forceinline__ void bar_arrive(int id) {
 // stalls on a cross-GPU round trip; the control warp polls the next stage's flags and
 // fences/raises the previous stage's flags while the workers move data.
 template <int DT, int W>
-__global__ void __launch_bounds__(kThreads, 1) torus_kernel(const LaunchArgs a) {
+__global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const LaunchArgs a) {
   using Acc = typename Wire<W>::Acc;
   constexpr int VE = Wire<W>::VE;
   constexpr int SW = kVecBytes / VE;  // bytes per wire element
@@ -1351,19 +1356,20 @@ cudaError_t launch_typed(const LaunchArgs& a, bool cooperative, cudaStream_t str
     torus_tma_kernel<DT, W><<<grid, block, smem, stream>>>(a);
     return cudaGetLastError();
   }
+  const dim3 lblock(kLdgThreads);
   if (cooperative) {
     void* args[] = {const_cast<LaunchArgs*>(&a)};
-    return cudaLaunchCooperativeKernel((const void*)torus_kernel<DT, W>, grid, block, args, 0,
+    return cudaLaunchCooperativeKernel((const void*)torus_kernel<DT, W>, grid, lblock, args, 0,
                                        stream);
   }
-  torus_kernel<DT, W><<<grid, block, 0, stream>>>(a);
+  torus_kernel<DT, W><<<grid, lblock, 0, stream>>>(a);
   return cudaGetLastError();
 }
 
 template <int DT, int W>
 int max_ctas_typed() {
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, torus_kernel<DT, W>, kThreads, 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, torus_kernel<DT, W>, kLdgThreads, 0) !=
       cudaSuccess)
     return 0;
   return nb;
