@@ -51,8 +51,8 @@ def parse():
     p.add_argument("--dtype", default=None, help="buffer dtype (default f16; f32 at N=1)")
     p.add_argument("--wire", default="f16")
     p.add_argument("--op", default="mean", choices=["sum", "mean"])
-    p.add_argument("--algo", default="torus", choices=["torus", "ring"],
-                   help="ring = the flat-ring baseline kernel (config 3 comparison)")
+    p.add_argument("--algo", default="torus", choices=["torus", "ring", "hier"],
+                   help="ring / hier = the flat-ring / hierarchical baseline kernels")
     p.add_argument("--no-nccl", action="store_true", help="skip the NCCL comparison")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
@@ -180,7 +180,7 @@ def run_torus(args):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    reduce_fn = comm.ring_all_reduce if args.algo == "ring" else comm.all_reduce
+    reduce_fn = {"ring": comm.ring_all_reduce, "hier": comm.hier_all_reduce}.get(args.algo, comm.all_reduce)
 
     def call():
         reduce_fn(buf, op=args.op, wire=TD[wire_s], stream=stream)
@@ -332,9 +332,9 @@ def run_torus(args):
         "config": {"workload": ("resnet50-grad-allreduce" if world > 1 else
                                 "resnet50-grad-castscale-degenerate (N=1)"),
                    "count": D, "buffer_dtype": dtype_s, "wire_dtype": wire_s, "op": args.op,
-                   "grid": f"{X}x{Y}" if args.algo == "torus" else f"ring{world}",
+                   "grid": f"ring{world}" if args.algo == "ring" else f"{X}x{Y}",
                    "algo": args.algo,
-                   "parallelism": f"torus{X}x{Y}" if args.algo == "torus" else f"ring{world}",
+                   "parallelism": (f"ring{world}" if args.algo == "ring" else f"{args.algo}{X}x{Y}"),
                    "ctas_per_rank": comm_ctas(),
                    "message_bytes": S, "l2": "flushed (256 MiB write) before every timed call",
                    "value_is": "busbw" if world > 1 else "algbw (busbw is 0 at N=1)"},

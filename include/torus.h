@@ -151,6 +151,20 @@ TORUS_API int torus_vring_allreduce(torus_comm_t comm, void* const* bufs, size_t
                                     torus_stream_t stream);
 TORUS_API size_t torus_comm_ring_round_elems(torus_comm_t comm, torus_dtype_t wire);
 
+/* Hierarchical all-reduce [6] -- the other baseline the paper compares against
+ * ("the hierarchical all-reduce also does the same amount of GPU-to-GPU
+ * operation as the 2D-Torus all-reduce, [but] the data size of the second step ... is X
+ * times" larger).  Per row of X ranks a chain reduce of the FULL buffer to column 0, a
+ * ring all-reduce of the full buffer among the Y leaders, a chain broadcast back (SPEC.md
+ * 234-242); HOP rounding; mean applied once.  Same conventions as torus_ring_allreduce;
+ * rounds of torus_comm_hier_round_elems() elements. */
+TORUS_API int torus_hier_allreduce(torus_comm_t comm, void* buf, size_t count, torus_dtype_t dtype,
+                                   torus_dtype_t wire, torus_op_t op, torus_stream_t stream);
+TORUS_API int torus_vhier_allreduce(torus_comm_t comm, void* const* bufs, size_t count,
+                                    torus_dtype_t dtype, torus_dtype_t wire, torus_op_t op,
+                                    torus_stream_t stream);
+TORUS_API size_t torus_comm_hier_round_elems(torus_comm_t comm, torus_dtype_t wire);
+
 /* ---------------------------------------------------------------------------------------
  * Queries, topology, host logic, errors
  * ------------------------------------------------------------------------------------- */

@@ -42,6 +42,9 @@ PROTOTYPES = {
     "torus_ring_allreduce": (_i, [_vp, _vp, _sz, _i, _i, _i, _vp]),
     "torus_vring_allreduce": (_i, [_vp, _c.POINTER(_vp), _sz, _i, _i, _i, _vp]),
     "torus_comm_ring_round_elems": (_sz, [_vp, _i]),
+    "torus_hier_allreduce": (_i, [_vp, _vp, _sz, _i, _i, _i, _vp]),
+    "torus_vhier_allreduce": (_i, [_vp, _c.POINTER(_vp), _sz, _i, _i, _i, _vp]),
+    "torus_comm_hier_round_elems": (_sz, [_vp, _i]),
     "torus_comm_get_async_error": (_i, [_vp]),
     "torus_comm_grid": (_i, [_vp, _c.POINTER(_i), _c.POINTER(_i)]),
     "torus_comm_rank": (_i, [_vp, _c.POINTER(_i), _c.POINTER(_i)]),

@@ -129,6 +129,17 @@ unsigned long long ring_round_elems(const torus_comm* c, int wire) {
   return k * q * N;
 }
 
+// Hierarchical baseline: chain slot [R] + broadcast slot [R] + 2(Y-1) ring slots [R/Y].
+unsigned long long hier_round_elems(const torus_comm* c, int wire) {
+  const unsigned long long sw = wire_size(wire), q = kVecBytes / sw;
+  const unsigned long long Y = (unsigned long long)c->Y;
+  if (c->world < 2 || c->slab_size <= c->layout.data_off) return 0;
+  const unsigned long long data_elems = (c->slab_size - c->layout.data_off) / sw;
+  // R = k*q*Y:  2*R + 2(Y-1)*R/Y = k*q*(2Y + 2(Y-1)) elements
+  const unsigned long long k = data_elems / (q * (2 * Y + 2 * (Y - 1)));
+  return k * q * Y;
+}
+
 int alloc_comm_common(torus_comm* c) {
   const size_t n_ep = (size_t)c->nlocal * c->G + c->nlocal;
   CU(cudaMalloc(&c->d_epochs, n_ep * sizeof(uint32_t)));
@@ -642,8 +653,8 @@ int torus_vallreduce(torus_comm_t c, void* const* bufs, size_t count, torus_dtyp
 
 namespace {
 
-int ring_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, int wire, int op,
-              cudaStream_t stream) {
+int baseline_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, int wire, int op,
+                  cudaStream_t stream, bool hier) {
   if (!c) return fail(TORUS_ERR_INVALID_ARG, "comm is NULL");
   if (!valid_pair(dtype, wire))
     return valid_dtype(dtype) && valid_dtype(wire)
@@ -668,8 +679,9 @@ int ring_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, int wir
     cudaError_t e = launch_castscale(bufs[0], count, dtype, wire, stream);
     return e == cudaSuccess ? TORUS_OK : cuda_fail(e, "castscale launch");
   }
-  const unsigned long long R = ring_round_elems(c, wire), sw = wire_size(wire);
-  if (R == 0) return fail(TORUS_ERR_INVALID_ARG, "workspace too small for the ring");
+  const unsigned long long R = hier ? hier_round_elems(c, wire) : ring_round_elems(c, wire);
+  const unsigned long long sw = wire_size(wire);
+  if (R == 0) return fail(TORUS_ERR_INVALID_ARG, "workspace too small for the baseline");
   LaunchArgs a;
   memset(&a, 0, sizeof a);
   a.ranks = c->d_ranks;
@@ -682,12 +694,18 @@ int ring_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, int wir
   a.aligned = aligned ? 1 : 0;
   a.timeout_ns = c->timeout_ns;
   a.hin_off = c->layout.data_off;
-  a.hin_stride = (R / (unsigned long long)c->world) * sw;  // one chunk slot
+  if (hier) {
+    a.hin_stride = R * sw;                                 // chain / broadcast slot
+    a.vin_stride = (R / (unsigned long long)c->Y) * sw;     // leader-ring slot
+  } else {
+    a.hin_stride = (R / (unsigned long long)c->world) * sw;  // one ring chunk slot
+  }
   for (unsigned long long r0 = 0; r0 < count; r0 += R) {
     a.n = std::min<unsigned long long>(R, count - r0);
     a.buf_off = r0;
-    cudaError_t e = launch_ring(a, dtype, wire, c->virt, stream);
-    if (e != cudaSuccess) return cuda_fail(e, "ring kernel launch");
+    cudaError_t e = hier ? launch_hier(a, dtype, wire, c->virt, stream)
+                         : launch_ring(a, dtype, wire, c->virt, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "baseline kernel launch");
   }
   return TORUS_OK;
 }
@@ -700,14 +718,33 @@ int torus_ring_allreduce(torus_comm_t c, void* buf, size_t count, torus_dtype_t 
                          torus_dtype_t wire, torus_op_t op, torus_stream_t stream) {
   if (c && c->virt) return fail(TORUS_ERR_INVALID_ARG, "virtual comm: use torus_vring_allreduce");
   void* bufs[1] = {buf};
-  return ring_impl(c, bufs, count, dtype, wire, op, static_cast<cudaStream_t>(stream));
+  return baseline_impl(c, bufs, count, dtype, wire, op, static_cast<cudaStream_t>(stream), false);
 }
 
 int torus_vring_allreduce(torus_comm_t c, void* const* bufs, size_t count, torus_dtype_t dtype,
                           torus_dtype_t wire, torus_op_t op, torus_stream_t stream) {
   if (!c || !bufs) return fail(TORUS_ERR_INVALID_ARG, "null argument");
   if (!c->virt) return fail(TORUS_ERR_INVALID_ARG, "not a virtual comm");
-  return ring_impl(c, bufs, count, dtype, wire, op, static_cast<cudaStream_t>(stream));
+  return baseline_impl(c, bufs, count, dtype, wire, op, static_cast<cudaStream_t>(stream), false);
+}
+
+int torus_hier_allreduce(torus_comm_t c, void* buf, size_t count, torus_dtype_t dtype,
+                         torus_dtype_t wire, torus_op_t op, torus_stream_t stream) {
+  if (c && c->virt) return fail(TORUS_ERR_INVALID_ARG, "virtual comm: use torus_vhier_allreduce");
+  void* bufs[1] = {buf};
+  return baseline_impl(c, bufs, count, dtype, wire, op, static_cast<cudaStream_t>(stream), true);
+}
+
+int torus_vhier_allreduce(torus_comm_t c, void* const* bufs, size_t count, torus_dtype_t dtype,
+                          torus_dtype_t wire, torus_op_t op, torus_stream_t stream) {
+  if (!c || !bufs) return fail(TORUS_ERR_INVALID_ARG, "null argument");
+  if (!c->virt) return fail(TORUS_ERR_INVALID_ARG, "not a virtual comm");
+  return baseline_impl(c, bufs, count, dtype, wire, op, static_cast<cudaStream_t>(stream), true);
+}
+
+size_t torus_comm_hier_round_elems(torus_comm_t c, torus_dtype_t wire) {
+  if (!c || !valid_dtype(wire)) return 0;
+  return (size_t)hier_round_elems(c, wire);
 }
 
 size_t torus_comm_ring_round_elems(torus_comm_t c, torus_dtype_t wire) {

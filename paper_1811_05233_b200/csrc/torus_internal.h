@@ -146,6 +146,7 @@ cudaError_t launch_barrier(const RankDev* ranks, int nlocal, unsigned long long 
                            unsigned long long timeout_ns, cudaStream_t stream);
 int torus_kernel_max_ctas_per_sm(int dtype, int wire);
 cudaError_t launch_ring(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
+cudaError_t launch_hier(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
 cudaError_t launch_multi_copy(const MultiTable& tab, int n, int dtype, int wire, void* staging,
                               bool pack, cudaStream_t stream);
 cudaError_t launch_probe(const RankDev* ranks, unsigned long long data_off, unsigned long long bytes,

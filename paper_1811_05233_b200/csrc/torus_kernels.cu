@@ -1830,3 +1830,199 @@ cudaError_t launch_multi_copy(const MultiTable& tab, int n, int dtype, int wire,
 }
 
 }  // namespace torus
+
+// ------------------------------------------------------------------------------------
+// Hierarchical all-reduce (baseline [6]; NEXT-3): per
+// row, a chain reduce of the FULL buffer to the column-0 leader; a ring all-reduce of the
+// full buffer among the Y leaders; a chain broadcast back along each row.  Every message
+// is rounded to the wire type (HOP).  Workspace (wire elements, round of n): chain slot
+// [n], broadcast slot [n], leader-ring slots 2(Y-1) x [n/Y].  Flags: H = chain step,
+// V / AG = leader-ring RS / AG step, R = broadcast step (source index = step).
+// ------------------------------------------------------------------------------------
+namespace torus {
+namespace {
+
+template <int DT, int W>
+__global__ void __launch_bounds__(512, 1) hier_kernel(const LaunchArgs a) {
+  using Acc = typename Wire<W>::Acc;
+  constexpr int VE = Wire<W>::VE;
+  constexpr int SW = kVecBytes / VE;
+  const int lr = blockIdx.x / a.G;
+  const int b = blockIdx.x - lr * a.G;
+  const RankDev* __restrict__ R = a.ranks + lr;
+  const int X = R->X, Y = R->Y, N = R->N, rho = R->rho, c = R->c, G = a.G, q = a.q, tid = threadIdx.x;
+  const unsigned long long n = a.n;
+  const bool aligned = a.aligned != 0;
+  void* const buf = a.buf[lr];
+  char* const myws = R->ws[R->rank];
+  char* const chain_slot = myws + a.hin_off;                 // [n]
+  char* const bcast_slot = chain_slot + a.hin_stride;        // [n]
+  char* const ring_base = bcast_slot + a.hin_stride;         // 2(Y-1) x [vin_stride]
+  const unsigned long long ring_slot = a.vin_stride;
+  auto rank_of = [&](int row, int col) { return row * X + col; };
+
+  __shared__ uint32_t s_e;
+  __shared__ int s_abort;
+  if (tid == 0) {
+    s_e = R->epoch[b] + 1u;
+    s_abort = 0;
+  }
+  __syncthreads();
+  const uint32_t e = s_e;
+  const unsigned long long deadline = gtimer() + a.timeout_ns;
+  auto flag = [&](char* ws, int kind, int step) -> uint32_t* {
+    return reinterpret_cast<uint32_t*>(ws) + ((size_t)(kind * kMaxDim + step) * G + b);
+  };
+  auto wait_in = [&](int kind, int step) -> bool {
+    if (tid == 0 && !wait_flag_ge(flag(myws, kind, step), e, deadline)) {
+      atomicExch_system(R->err, kErrTimeout);
+      s_abort = 1;
+    }
+    __syncthreads();
+    return s_abort == 0;
+  };
+  auto signal_to = [&](int peer, int kind, int step) {
+    __syncthreads();
+    if (tid == 0) st_release_sys(flag(R->ws[peer], kind, step), e);
+  };
+  // CTA b's slice of [0, len) in vectors
+  auto slice = [&](unsigned long long len, unsigned long long* va, unsigned long long* vz) {
+    const unsigned long long nv = (len + VE - 1) / VE;
+    *va = nv * (unsigned long long)b / G;
+    *vz = nv * (unsigned long long)(b + 1) / G;
+  };
+  // CTA b owns slice b of each of the Y leader-ring chunks in EVERY phase, so no phase
+  // reads another CTA's data (no grid-wide synchronization needed)
+  auto for_mine = [&](auto f) {
+    for (int k = 0; k < Y; ++k) {
+      unsigned long long co, cl, pa, pz;
+      qpart(n, Y, q, k, &co, &cl);
+      slice(cl, &pa, &pz);
+      for (unsigned long long v = pa + tid; v < pz; v += blockDim.x) {
+        const unsigned long long el = co + v * VE;
+        f(el, (int)min((unsigned long long)VE, co + cl - el));
+      }
+    }
+  };
+
+  // ---- phase 1: chain reduce to the leader (column X-1 -> ... -> 0) ----
+  // column c receives at step X-2-c from column c+1 and sends at step X-1-c to c-1
+  if (c < X - 1 && !wait_in(kFlagH, X - 2 - c)) return;
+  for_mine([&](unsigned long long el, int nrem) {
+    Acc acc[VE];
+    unpack<W>(load_user<DT, W>(buf, a.buf_off + el, nrem, aligned), acc);
+    if (c < X - 1) {  // partial = incoming message + my own contribution
+      Acc t[VE];
+      unpack<W>(ld_ws(chain_slot + el * SW), t);
+      acc_add<W>(t, acc);
+#pragma unroll
+      for (int i = 0; i < VE; ++i) acc[i] = t[i];
+    }
+    if (c > 0) {
+      st_ws(R->ws[rank_of(rho, c - 1)] + a.hin_off + el * SW, pack<W>(acc));
+    } else {  // leader: the row sum, rounded once (mean here if there is no vertical phase)
+      if (Y == 1 && a.op == 1) acc_mean<W>(acc, a.inv_n, N);
+      st_ws(chain_slot + el * SW, pack<W>(acc));  // the leader keeps its value in place
+    }
+  });
+  if (c > 0) signal_to(rank_of(rho, c - 1), kFlagH, X - 1 - c);
+  __syncthreads();
+
+  // ---- phase 2: ring all-reduce of the full buffer among the Y leaders ----
+  if (c == 0 && Y > 1) {
+    const int nextl = rank_of((rho + 1) % Y, 0);
+    auto rslot = [&](char* ws, int kind, int step) -> char* {
+      return ws + (a.hin_off + 2 * a.hin_stride) + ((size_t)kind * (Y - 1) + step) * ring_slot;
+    };
+    auto part = [&](int k, unsigned long long* co, unsigned long long* cl, unsigned long long* pa,
+                    unsigned long long* pz) {
+      qpart(n, Y, q, k, co, cl);
+      slice(*cl, pa, pz);
+    };
+    for (int s = 0; s <= Y - 1; ++s) {  // reduce-scatter over the leader ring
+      const int k = ((rho - s - 1) % Y + Y) % Y;
+      unsigned long long co, cl, pa, pz;
+      part(k, &co, &cl, &pa, &pz);
+      if (s > 0 && !wait_in(kFlagV, s - 1)) return;
+      for (unsigned long long v = pa + tid; v < pz; v += blockDim.x) {
+        const unsigned long long el = v * VE;
+        Acc acc[VE];
+        unpack<W>(ld_ws(chain_slot + (co + el) * SW), acc);
+        if (s > 0) {
+          Acc t[VE];
+          unpack<W>(ld_ws(rslot(myws, 0, s - 1) + el * SW), t);
+          acc_add<W>(t, acc);
+#pragma unroll
+          for (int i = 0; i < VE; ++i) acc[i] = t[i];
+        }
+        if (s < Y - 1) {
+          st_ws(rslot(R->ws[nextl], 0, s) + el * SW, pack<W>(acc));
+        } else {
+          if (a.op == 1) acc_mean<W>(acc, a.inv_n, N);
+          const uint4 out = pack<W>(acc);
+          st_ws(chain_slot + (co + el) * SW, out);           // final chunk, in place
+          st_ws(rslot(R->ws[nextl], 1, 0) + el * SW, out);   // all-gather step 0
+        }
+      }
+      if (s < Y - 1) signal_to(nextl, kFlagV, s);
+    }
+    signal_to(nextl, kFlagAG, 0);
+    for (int t = 1; t <= Y - 1; ++t) {  // all-gather over the leader ring
+      const int k = ((rho - t) % Y + Y) % Y;
+      unsigned long long co, cl, pa, pz;
+      part(k, &co, &cl, &pa, &pz);
+      if (!wait_in(kFlagAG, t - 1)) return;
+      for (unsigned long long v = pa + tid; v < pz; v += blockDim.x) {
+        const unsigned long long el = v * VE;
+        const uint4 w = ld_ws(rslot(myws, 1, t - 1) + el * SW);
+        st_ws(chain_slot + (co + el) * SW, w);
+        if (t < Y - 1) st_ws(rslot(R->ws[nextl], 1, t) + el * SW, w);
+      }
+      if (t < Y - 1) signal_to(nextl, kFlagAG, t);
+    }
+    __syncthreads();
+  }
+
+  // ---- phase 3: chain broadcast from the leader (column 0 -> 1 -> ... -> X-1) ----
+  const char* const src = (c == 0) ? chain_slot : bcast_slot;
+  if (c > 0 && !wait_in(kFlagR, c - 1)) return;
+  for_mine([&](unsigned long long el, int nrem) {
+    const uint4 w = ld_ws(src + el * SW);
+    store_user<DT, W>(buf, a.buf_off + el, nrem, w, aligned);
+    if (c < X - 1) st_ws(R->ws[rank_of(rho, c + 1)] + a.hin_off + a.hin_stride + el * SW, w);
+  });
+  if (c < X - 1) signal_to(rank_of(rho, c + 1), kFlagR, c);
+  __syncthreads();
+  if (tid == 0) R->epoch[b] = e;
+}
+
+template <int DT, int W>
+cudaError_t launch_hier_typed(const LaunchArgs& a, bool cooperative, cudaStream_t stream) {
+  const dim3 grid(a.nlocal * a.G), block(512);
+  if (cooperative) {
+    void* args[] = {const_cast<LaunchArgs*>(&a)};
+    return cudaLaunchCooperativeKernel((const void*)hier_kernel<DT, W>, grid, block, args, 0, stream);
+  }
+  hier_kernel<DT, W><<<grid, block, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_hier(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream) {
+  if (dtype == wire) {
+    switch (dtype) {
+      case DT_F32: return launch_hier_typed<DT_F32, DT_F32>(a, cooperative, stream);
+      case DT_F16: return launch_hier_typed<DT_F16, DT_F16>(a, cooperative, stream);
+      case DT_BF16: return launch_hier_typed<DT_BF16, DT_BF16>(a, cooperative, stream);
+      case DT_I32: return launch_hier_typed<DT_I32, DT_I32>(a, cooperative, stream);
+    }
+  } else if (dtype == DT_F32 && wire == DT_F16) {
+    return launch_hier_typed<DT_F32, DT_F16>(a, cooperative, stream);
+  } else if (dtype == DT_F32 && wire == DT_BF16) {
+    return launch_hier_typed<DT_F32, DT_BF16>(a, cooperative, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace torus

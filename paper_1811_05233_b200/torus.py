@@ -99,6 +99,9 @@ class _CommBase:
     def round_elems(self, wire: torch.dtype) -> int:
         return _lib.load().torus_comm_round_elems(self._comm, _dtype_code(wire))
 
+    def hier_round_elems(self, wire: torch.dtype) -> int:
+        return _lib.load().torus_comm_hier_round_elems(self._comm, _dtype_code(wire))
+
     def ring_round_elems(self, wire: torch.dtype) -> int:
         return _lib.load().torus_comm_ring_round_elems(self._comm, _dtype_code(wire))
 
@@ -225,6 +228,17 @@ class TorusComm(_CommBase):
         return t
 
 
+    def hier_all_reduce(self, t: torch.Tensor, op: str = "mean", wire: torch.dtype | None = None,
+                        stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """The hierarchical BASELINE [6] (torus_hier_allreduce), HOP rounding."""
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("hier all_reduce needs a contiguous CUDA tensor")
+        check(_lib.load().torus_hier_allreduce(
+            self._comm, ctypes.c_void_p(t.data_ptr()), t.numel(), _dtype_code(t.dtype),
+            _dtype_code(wire or t.dtype), OPS[op], _stream_ptr(stream)), "torus_hier_allreduce")
+        return t
+
+
 class VirtualTorus(_CommBase):
     """A whole X-by-Y grid emulated on one GPU (one cooperative launch per round); runs
     the product kernel with every virtual rank's peer pointers aimed at local slabs."""
@@ -261,4 +275,15 @@ class VirtualTorus(_CommBase):
         check(_lib.load().torus_vring_allreduce(
             self._comm, ptrs, t0.numel(), _dtype_code(t0.dtype), _dtype_code(wire or t0.dtype),
             OPS[op], _stream_ptr(stream)), "torus_vring_allreduce")
+        return tensors
+
+    def hier_all_reduce(self, tensors: Sequence[torch.Tensor], op: str = "mean",
+                        wire: torch.dtype | None = None,
+                        stream: torch.cuda.Stream | None = None) -> Sequence[torch.Tensor]:
+        """Hierarchical baseline over the virtual ranks (torus_vhier_allreduce)."""
+        t0 = tensors[0]
+        ptrs = (ctypes.c_void_p * self.N)(*[t.data_ptr() for t in tensors])
+        check(_lib.load().torus_vhier_allreduce(
+            self._comm, ptrs, t0.numel(), _dtype_code(t0.dtype), _dtype_code(wire or t0.dtype),
+            OPS[op], _stream_ptr(stream)), "torus_vhier_allreduce")
         return tensors

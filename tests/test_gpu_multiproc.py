@@ -67,7 +67,8 @@ def _worker(rank, world, port, cases, errfile):
         comms = {}
         for (X, Y, dtype, wire, op, D, dist_name) in cases:
             ring = X == 0  # (0, N, ...) marks the flat-ring baseline over all ranks
-            key = (world, 1) if ring else (X, Y)
+            hier = X < 0   # (-X, Y, ...) marks the hierarchical baseline on an X-by-Y grid
+            key = (world, 1) if ring else ((-X, Y) if hier else (X, Y))
             if key not in comms:
                 comms[key] = TorusComm.init(X=key[0], Y=key[1])
             comm = comms[key]
@@ -75,7 +76,8 @@ def _worker(rank, world, port, cases, errfile):
             t = _to_dev(ins[rank], dtype, f"cuda:{rank}")
             torch.cuda.synchronize()
             dist.barrier()
-            (comm.ring_all_reduce if ring else comm.all_reduce)(t, op=op, wire=TD[wire])
+            fn = comm.ring_all_reduce if ring else (comm.hier_all_reduce if hier else comm.all_reduce)
+            fn(t, op=op, wire=TD[wire])
             torch.cuda.synchronize()
             assert comm.async_error() == 0, "watchdog"
             got = _from_dev(t, dtype)
@@ -85,6 +87,12 @@ def _worker(rank, world, port, cases, errfile):
                                             round_elems=comm.ring_round_elems(TD[wire]))[rank]
                 ok, nbad = _same(got, ref)
                 assert ok, f"rank {rank} ring {dtype}/{wire} {op} D={D}: {nbad} mismatches"
+                dist.barrier()
+                continue
+            if hier:
+                ref = oracle.hier_allreduce(ins, -X, Y, dtype, wire=wire, op=op, policy="hop", q=q)[rank]
+                ok, nbad = _same(got, ref)
+                assert ok, f"rank {rank} hier {-X}x{Y} {dtype}/{wire} {op} D={D}: {nbad} mismatches"
                 dist.barrier()
                 continue
             R = comm.round_elems(TD[wire])
@@ -142,7 +150,7 @@ def test_two_gpus(tmp_path):
 
 
 def test_four_gpus(tmp_path):
-    cases = _cases([(2, 2), (4, 1), (1, 4), (0, 4)], ops=("mean",))
+    cases = _cases([(2, 2), (4, 1), (1, 4), (0, 4), (-2, 2)], ops=("mean",))
     cases += [(2, 2, "f16", "f16", "mean", 25_557_032, "grad")]  # config 2 shape on 2x2
     _run(4, cases, tmp_path)
 

@@ -303,3 +303,22 @@ def test_multi_tensor_single_rank():
             assert_same(got, ref, f"multi N=1 {wire}")
     finally:
         comm.destroy()
+
+
+@pytest.mark.parametrize("X,Y", [(2, 1), (1, 2), (2, 2), (2, 4), (4, 2), (3, 2)])
+@pytest.mark.parametrize("dtype,wire", PAIRS)
+@pytest.mark.parametrize("op", ["sum", "mean"])
+def test_virtual_hierarchical_baseline_bit_exact(vgrids, X, Y, dtype, wire, op):
+    """The hierarchical BASELINE kernel [6] vs the oracle's hierarchical all-reduce (HOP)."""
+    vt = vgrids(X, Y)
+    N = X * Y
+    assert vt.hier_round_elems(TD[wire]) > 100_003
+    for D in (1, 999, 4099, 100_003):
+        ins = synthetic.make_all("full" if dtype == "i32" else "normal", D, N, dtype, salt=D % 5)
+        ts = [_np_to_dev(a, dtype) for a in ins]
+        vt.hier_all_reduce(ts, op=op, wire=TD[wire])
+        torch.cuda.synchronize()
+        assert vt.async_error() == 0
+        ref = oracle.hier_allreduce(ins, X, Y, dtype, wire=wire, op=op, policy="hop", q=q_of(wire))
+        for r in range(N):
+            assert_same(from_dev(ts[r], dtype), ref[r], f"hier {X}x{Y} {dtype}/{wire} {op} D={D} rank {r}")
