@@ -165,6 +165,21 @@ TORUS_API int torus_vhier_allreduce(torus_comm_t comm, void* const* bufs, size_t
                                     torus_stream_t stream);
 TORUS_API size_t torus_comm_hier_round_elems(torus_comm_t comm, torus_dtype_t wire);
 
+/* NVLS variant (NEXT-4): all-reduce with NVLink-SHARP in-switch reduction over ALL ranks
+ * (multimem.ld_reduce with f32 accumulation + multimem.st on a multicast object), per GPU
+ * about (N+1)/N*S bytes each way instead of 2(N-1)/N*S.  The switch's summation order is
+ * unspecified: results match the oracle within the float tolerance, not bit for bit.
+ * Wires f16 / bf16 / f32 (no i32).  Setup is collective and takes two host exchanges:
+ *   prepare(bytes) -> blob[2] (rank 0: {pid, fd} of the exported multicast object)
+ *   all ranks: attach(blob of rank 0)  -- imports the fd (pidfd_getfd), adds the device
+ *   barrier; all ranks: bind()         -- binds the staging memory, maps the multicast VA
+ *   barrier; then torus_nvls_allreduce.  `bytes` = staging per rank (rounds above it). */
+TORUS_API int torus_nvls_prepare(torus_comm_t comm, size_t bytes, long long* blob /*[2]*/);
+TORUS_API int torus_nvls_attach(torus_comm_t comm, const long long* blob0 /*[2]*/);
+TORUS_API int torus_nvls_bind(torus_comm_t comm);
+TORUS_API int torus_nvls_allreduce(torus_comm_t comm, void* buf, size_t count, torus_dtype_t dtype,
+                                   torus_dtype_t wire, torus_op_t op, torus_stream_t stream);
+
 /* ---------------------------------------------------------------------------------------
  * Queries, topology, host logic, errors
  * ------------------------------------------------------------------------------------- */

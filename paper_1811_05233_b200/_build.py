@@ -9,7 +9,7 @@ import subprocess
 PKG = pathlib.Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-SOURCES = [CSRC / "torus_abi.cu", CSRC / "torus_kernels.cu"]
+SOURCES = [CSRC / "torus_abi.cu", CSRC / "torus_kernels.cu", CSRC / "torus_nvls.cu"]
 HEADERS = [CSRC / "torus_internal.h", ROOT / "include" / "torus.h"]
 LIB = PKG / "libtorus.so"
 

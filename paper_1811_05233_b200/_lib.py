@@ -45,6 +45,10 @@ PROTOTYPES = {
     "torus_hier_allreduce": (_i, [_vp, _vp, _sz, _i, _i, _i, _vp]),
     "torus_vhier_allreduce": (_i, [_vp, _c.POINTER(_vp), _sz, _i, _i, _i, _vp]),
     "torus_comm_hier_round_elems": (_sz, [_vp, _i]),
+    "torus_nvls_prepare": (_i, [_vp, _sz, _c.POINTER(_c.c_longlong)]),
+    "torus_nvls_attach": (_i, [_vp, _c.POINTER(_c.c_longlong)]),
+    "torus_nvls_bind": (_i, [_vp]),
+    "torus_nvls_allreduce": (_i, [_vp, _vp, _sz, _i, _i, _i, _vp]),
     "torus_comm_get_async_error": (_i, [_vp]),
     "torus_comm_grid": (_i, [_vp, _c.POINTER(_i), _c.POINTER(_i)]),
     "torus_comm_rank": (_i, [_vp, _c.POINTER(_i), _c.POINTER(_i)]),

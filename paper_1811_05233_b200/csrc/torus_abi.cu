@@ -95,6 +95,7 @@ struct torus_comm {
   uint32_t* d_sig_ack = nullptr;          // TMA kernel: [nlocal][G] signal-lane acks
   void* d_staging = nullptr;              // multi-tensor staging buffer (wire type)
   size_t staging_bytes = 0;
+  NvlsState nvls;                         // NVLS (multicast) variant, NEXT-4
 };
 
 namespace {
@@ -201,6 +202,7 @@ int pick_ctas(int device, int nlocal) {
 }
 
 void destroy_resources(torus_comm* c) {
+  nvls_release(&c->nvls);
   for (void* p : c->opened) cudaIpcCloseMemHandle(p);
   for (void* p : c->own_slabs) cudaFree(p);
   if (c->d_ranks) cudaFree(c->d_ranks);
@@ -819,6 +821,61 @@ int torus_allreduce_multi(torus_comm_t c, void* const* ptrs, const size_t* count
     }
     cudaError_t e = launch_multi_copy(tab, n, dtype, wire, c->d_staging, false, s);
     if (e != cudaSuccess) return cuda_fail(e, "multi unpack");
+  }
+  return TORUS_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int torus_nvls_prepare(torus_comm_t c, size_t bytes, long long* blob) {
+  if (!c || !blob || c->virt || c->world < 2) return fail(TORUS_ERR_INVALID_ARG, "nvls_prepare args");
+  if (c->nvls.mem) return fail(TORUS_ERR_INVALID_ARG, "NVLS already prepared");
+  CU(cudaSetDevice(c->device));
+  const int rc = nvls_prepare(c->device, c->rank, bytes, c->world, &c->nvls, blob);
+  if (rc) {
+    nvls_release(&c->nvls);
+    return fail(rc, "NVLS prepare (multicast object / physical memory)");
+  }
+  return TORUS_OK;
+}
+
+int torus_nvls_attach(torus_comm_t c, const long long* blob0) {
+  if (!c || !blob0 || !c->nvls.mem) return fail(TORUS_ERR_INVALID_ARG, "nvls_attach before prepare");
+  CU(cudaSetDevice(c->device));
+  const int rc = nvls_attach(&c->nvls, blob0);
+  return rc ? fail(rc, "NVLS attach (pidfd_getfd / import / add device)") : TORUS_OK;
+}
+
+int torus_nvls_bind(torus_comm_t c) {
+  if (!c || !c->nvls.have_mc) return fail(TORUS_ERR_INVALID_ARG, "nvls_bind before attach");
+  CU(cudaSetDevice(c->device));
+  const int rc = nvls_bind(&c->nvls);
+  return rc ? fail(rc, "NVLS bind / map") : TORUS_OK;
+}
+
+int torus_nvls_allreduce(torus_comm_t c, void* buf, size_t count, torus_dtype_t dtype,
+                         torus_dtype_t wire, torus_op_t op, torus_stream_t stream) {
+  if (!c) return fail(TORUS_ERR_INVALID_ARG, "comm is NULL");
+  if (!c->nvls.ready) return fail(TORUS_ERR_INVALID_ARG, "NVLS not initialised");
+  if (!valid_pair(dtype, wire) || wire == TORUS_I32)
+    return fail(TORUS_ERR_UNSUPPORTED, "NVLS: dtype %d with wire %d", dtype, wire);
+  if (op != TORUS_SUM && op != TORUS_MEAN) return fail(TORUS_ERR_INVALID_ARG, "bad op %d", op);
+  if (c->poisoned || *reinterpret_cast<volatile int*>(c->h_err)) {
+    c->poisoned = true;
+    return fail(TORUS_ERR_TIMEOUT, "communicator has an async error; destroy it");
+  }
+  if (count == 0) return TORUS_OK;
+  if (!buf || reinterpret_cast<uintptr_t>(buf) % wire_size(dtype))
+    return fail(TORUS_ERR_INVALID_ARG, "buffer NULL or misaligned");
+  const unsigned long long sw = wire_size(wire), q = kVecBytes / sw, N = (unsigned long long)c->world;
+  const unsigned long long R = (c->nvls.size / sw) / (q * N) * (q * N);
+  for (unsigned long long r0 = 0; r0 < count; r0 += R) {
+    const unsigned long long n = std::min<unsigned long long>(R, count - r0);
+    cudaError_t e = launch_nvls(c->d_ranks, &c->nvls, buf, n, r0, dtype, wire, op, 1.0f / (float)N, c->G,
+                                c->timeout_ns, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "nvls kernel launch");
   }
   return TORUS_OK;
 }

@@ -7,6 +7,7 @@
 #include <cstddef>
 #include <cstdint>
 
+#include <cuda.h>  // driver-API types only (NVLS); the library does not link libcuda
 #include <cuda_runtime.h>
 
 namespace torus {
@@ -136,6 +137,25 @@ struct MultiTable {
   unsigned long long count[kMultiMax];
   unsigned long long offset[kMultiMax];  // element offset in the staging buffer
 };
+
+// NVLS (multicast) state of one rank (torus_nvls.cu)
+struct NvlsState {
+  CUmemGenericAllocationHandle mem = 0;        // my physical staging memory
+  CUmemGenericAllocationHandle mc_handle = 0;  // the multicast object
+  CUdeviceptr uc = 0;                          // unicast view of my staging
+  CUdeviceptr mc = 0;                          // multicast view (everyone's staging)
+  size_t size = 0, gran = 0;
+  CUdevice dev = 0;
+  int export_fd = -1;
+  bool have_mc = false, ready = false;
+};
+int nvls_prepare(int device, int rank, size_t bytes, int world, NvlsState* st, long long blob[2]);
+int nvls_attach(NvlsState* st, const long long blob0[2]);
+int nvls_bind(NvlsState* st);
+void nvls_release(NvlsState* st);
+cudaError_t launch_nvls(const RankDev* ranks, const NvlsState* st, void* buf, unsigned long long n,
+                        unsigned long long buf_off, int dtype, int wire, int op, float inv_n, int G,
+                        unsigned long long timeout_ns, cudaStream_t s);
 
 // ---- launch wrappers implemented in torus_kernels.cu ----
 cudaError_t launch_torus(const LaunchArgs& a, int dtype, int wire, bool cooperative,

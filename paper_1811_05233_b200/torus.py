@@ -228,6 +228,37 @@ class TorusComm(_CommBase):
         return t
 
 
+    def nvls_init(self, nbytes: int, group=None) -> None:
+        """Collective NVLS setup (NEXT-4): multicast object over all ranks + staging."""
+        import torch.distributed as dist
+        L = _lib.load()
+        blob = (ctypes.c_longlong * 2)()
+        check(L.torus_nvls_prepare(self._comm, nbytes, blob), "torus_nvls_prepare")
+        blobs: list = [None] * self.world
+        dist.all_gather_object(blobs, (int(blob[0]), int(blob[1])), group=group)
+        b0 = (ctypes.c_longlong * 2)(*blobs[0])
+        rc = L.torus_nvls_attach(self._comm, b0)
+        st: list = [None] * self.world
+        dist.all_gather_object(st, rc, group=group)  # every device added before any bind
+        check(rc, "torus_nvls_attach")
+        if any(st):
+            raise RuntimeError(f"torus_nvls_attach failed on some rank: {st}")
+        rc = L.torus_nvls_bind(self._comm)
+        dist.all_gather_object(st, rc, group=group)
+        check(rc, "torus_nvls_bind")
+        if any(st):
+            raise RuntimeError(f"torus_nvls_bind failed on some rank: {st}")
+
+    def nvls_all_reduce(self, t: torch.Tensor, op: str = "mean", wire: torch.dtype | None = None,
+                        stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """In-switch-reduction all-reduce (NEXT-4); tolerance-level parity (switch order)."""
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("nvls all_reduce needs a contiguous CUDA tensor")
+        check(_lib.load().torus_nvls_allreduce(
+            self._comm, ctypes.c_void_p(t.data_ptr()), t.numel(), _dtype_code(t.dtype),
+            _dtype_code(wire or t.dtype), OPS[op], _stream_ptr(stream)), "torus_nvls_allreduce")
+        return t
+
     def hier_all_reduce(self, t: torch.Tensor, op: str = "mean", wire: torch.dtype | None = None,
                         stream: torch.cuda.Stream | None = None) -> torch.Tensor:
         """The hierarchical BASELINE [6] (torus_hier_allreduce), HOP rounding."""
