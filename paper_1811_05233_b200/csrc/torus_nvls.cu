@@ -252,23 +252,98 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
     *v0 = nv * (unsigned long long)b / G;
     *v1 = nv * (unsigned long long)(b + 1) / G;
   };
+  // 16-byte vector path when the user buffer (at this round's offset) is 16-byte aligned
+  using UT = typename NElem<DT>::T;
+  constexpr int UB = (int)sizeof(UT) * VE;  // user bytes per wire vector (16 or 32)
+  const bool vec = ((reinterpret_cast<uintptr_t>(a.buf) + a.buf_off * sizeof(UT)) & 15) == 0;
+  auto copy_in = [&](unsigned long long i0, unsigned long long i1) {  // elements [i0, i1)
+    unsigned long long i = i0;
+    if (vec) {
+      for (unsigned long long v = i0 / VE + tid; (v + 1) * VE <= i1; v += blockDim.x) {
+        const char* src = reinterpret_cast<const char*>(a.buf) + (a.buf_off + v * VE) * sizeof(UT);
+        uint4 w;
+        if constexpr (DT == W) {
+          w = __ldcs(reinterpret_cast<const uint4*>(src));
+        } else {
+          const float4 f0 = __ldcs(reinterpret_cast<const float4*>(src));
+          const float4 f1 = __ldcs(reinterpret_cast<const float4*>(src) + 1);
+          const float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+          uint32_t* o = &w.x;
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            if constexpr (W == 1) {
+              __half2 h = __floats2half2_rn(f[2 * k2], f[2 * k2 + 1]);
+              o[k2] = *reinterpret_cast<uint32_t*>(&h);
+            } else {
+              __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * k2], f[2 * k2 + 1]);
+              o[k2] = *reinterpret_cast<uint32_t*>(&h);
+            }
+          }
+        }
+        *reinterpret_cast<uint4*>(a.uc + v * VE * SW) = w;
+      }
+      i = i0 + (i1 - i0) / VE * VE;
+    }
+    for (unsigned long long j = i + tid; j < i1; j += blockDim.x) to_wire<DT, W>(a.buf, a.buf_off + j, a.uc + j * SW);
+  };
+  auto copy_out = [&](unsigned long long i0, unsigned long long i1) {
+    unsigned long long i = i0;
+    if (vec) {
+      for (unsigned long long v = i0 / VE + tid; (v + 1) * VE <= i1; v += blockDim.x) {
+        const uint4 w = *reinterpret_cast<const uint4*>(a.uc + v * VE * SW);
+        char* dst = reinterpret_cast<char*>(a.buf) + (a.buf_off + v * VE) * sizeof(UT);
+        if constexpr (DT == W) {
+          __stcs(reinterpret_cast<uint4*>(dst), w);
+        } else {
+          const uint32_t* o = &w.x;
+          float f[8];
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            if constexpr (W == 1) {
+              const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&o[k2]));
+              f[2 * k2] = t.x;
+              f[2 * k2 + 1] = t.y;
+            } else {
+              f[2 * k2] = __uint_as_float(o[k2] << 16);
+              f[2 * k2 + 1] = __uint_as_float(o[k2] & 0xffff0000u);
+            }
+          }
+          __stcs(reinterpret_cast<float4*>(dst), make_float4(f[0], f[1], f[2], f[3]));
+          __stcs(reinterpret_cast<float4*>(dst) + 1, make_float4(f[4], f[5], f[6], f[7]));
+        }
+      }
+      i = i0 + (i1 - i0) / VE * VE;
+    }
+    for (unsigned long long j = i + tid; j < i1; j += blockDim.x) from_wire<DT, W>(a.buf, a.buf_off + j, a.uc + j * SW);
+  };
+  (void)UB;
   // 1. my buffer -> my staging (all shards, my slices)
   for (int k = 0; k < N; ++k) {
     unsigned long long off, len, v0, v1;
     shard_slice(k, &off, &len, &v0, &v1);
-    for (unsigned long long i = off + v0 * VE + tid; i < off + min(len, v1 * VE); i += blockDim.x)
-      to_wire<DT, W>(a.buf, a.buf_off + i, a.uc + i * SW);
+    copy_in(off + v0 * VE, off + min(len, v1 * VE));
   }
   if (!barrier(kFlagH)) return;
   // 3. my shard: in-switch sum over all GPUs, mean, multicast back to everyone
   {
+    constexpr int U = 4;  // in-switch reductions in flight per thread
     unsigned long long off, len, v0, v1;
     shard_slice(me, &off, &len, &v0, &v1);
-    for (unsigned long long v = v0 + tid; v < v1; v += blockDim.x) {
-      const unsigned long long byte = (off + v * VE) * SW;
-      uint4 r = Mm<W>::ld_reduce(a.mc + byte);
-      if (a.op == 1) Mm<W>::scale(r, a.inv_n);
-      Mm<W>::st(a.mc + byte, r);
+    for (unsigned long long vb = v0 + tid; vb < v1; vb += U * blockDim.x) {
+      uint4 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned long long v = vb + (unsigned long long)u * blockDim.x;
+        if (v < v1) r[u] = Mm<W>::ld_reduce(a.mc + (off + v * VE) * SW);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned long long v = vb + (unsigned long long)u * blockDim.x;
+        if (v < v1) {
+          if (a.op == 1) Mm<W>::scale(r[u], a.inv_n);
+          Mm<W>::st(a.mc + (off + v * VE) * SW, r[u]);
+        }
+      }
     }
   }
   if (!barrier(kFlagR)) return;
@@ -276,8 +351,7 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
   for (int k = 0; k < N; ++k) {
     unsigned long long off, len, v0, v1;
     shard_slice(k, &off, &len, &v0, &v1);
-    for (unsigned long long i = off + v0 * VE + tid; i < off + min(len, v1 * VE); i += blockDim.x)
-      from_wire<DT, W>(a.buf, a.buf_off + i, a.uc + i * SW);
+    copy_out(off + v0 * VE, off + min(len, v1 * VE));
   }
   __syncthreads();
   if (tid == 0) R->epoch[b] = e;
