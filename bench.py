@@ -51,8 +51,8 @@ def parse():
     p.add_argument("--dtype", default=None, help="buffer dtype (default f16; f32 at N=1)")
     p.add_argument("--wire", default="f16")
     p.add_argument("--op", default="mean", choices=["sum", "mean"])
-    p.add_argument("--algo", default="torus", choices=["torus", "ring", "hier"],
-                   help="ring / hier = the flat-ring / hierarchical baseline kernels")
+    p.add_argument("--algo", default="torus", choices=["torus", "ring", "hier", "nvls"],
+                   help="ring / hier = baseline kernels; nvls = in-switch-reduction variant")
     p.add_argument("--no-nccl", action="store_true", help="skip the NCCL comparison")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
@@ -180,7 +180,10 @@ def run_torus(args):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    reduce_fn = {"ring": comm.ring_all_reduce, "hier": comm.hier_all_reduce}.get(args.algo, comm.all_reduce)
+    if args.algo == "nvls":
+        comm.nvls_init(D * DT_BYTES[wire_s] + (4 << 20))
+    reduce_fn = {"ring": comm.ring_all_reduce, "hier": comm.hier_all_reduce,
+                 "nvls": comm.nvls_all_reduce}.get(args.algo, comm.all_reduce)
 
     def call():
         reduce_fn(buf, op=args.op, wire=TD[wire_s], stream=stream)

@@ -206,3 +206,56 @@ def test_multi_tensor_bucket_two_gpus(tmp_path):
         mp.spawn(_multi_worker, args=(2, _free_port(), errfile), nprocs=2, join=True)
     except Exception as e:
         raise AssertionError(open(errfile).read() if os.path.exists(errfile) else str(e)) from None
+
+
+def _nvls_worker(rank, world, port, errfile):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    try:
+        import torch.distributed as dist
+
+        import oracle
+        import synthetic
+        from paper_1811_05233_b200 import TorusComm
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        comm = TorusComm.init(X=world, Y=1)
+        comm.nvls_init(8 << 20)
+        for dtype, wire, tol in (("f16", "f16", 1e-2), ("bf16", "bf16", 1e-2), ("f32", "f32", 1e-6),
+                                 ("f32", "f16", 1e-2)):
+            D = 1_000_003
+            ins = synthetic.make_all("normal", D, world, dtype, salt=11)
+            t = _to_dev(ins[rank], dtype, f"cuda:{rank}")
+            torch.cuda.synchronize()
+            dist.barrier()
+            comm.nvls_all_reduce(t, op="mean", wire=TD[wire])  # 4 rounds of the 8 MiB staging
+            torch.cuda.synchronize()
+            assert comm.async_error() == 0
+            got = synthetic.as_float64(_from_dev(t, dtype), dtype)
+            ref = oracle.brute_sum_f64(ins, dtype, "mean")
+            mag = sum(np.abs(synthetic.as_float64(a, dtype)) for a in ins) / world
+            err = np.abs(got - ref) / (mag + 1e-30)
+            assert (err <= tol).all(), f"rank {rank} nvls {dtype}/{wire}: max err {err.max()}"
+            dist.barrier()
+        dist.barrier()
+        comm.destroy()
+        dist.destroy_process_group()
+    except Exception:
+        with open(errfile, "a") as f:
+            f.write(f"rank {rank}:\n{traceback.format_exc()}\n")
+        raise
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_nvls_variant_tolerance(tmp_path, world):
+    """NEXT-4: in-switch reduction; the switch's order is unspecified, so the check is the
+    north-star tolerance vs the f64 sum (1e-2 f16/bf16, 1e-6 f32, normalized by sum|x|)."""
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    errfile = str(tmp_path / "errors.txt")
+    try:
+        mp.spawn(_nvls_worker, args=(world, _free_port(), errfile), nprocs=world, join=True)
+    except Exception as e:
+        raise AssertionError(open(errfile).read() if os.path.exists(errfile) else str(e)) from None
