@@ -48,11 +48,12 @@ def main():
         for it in range(iters):
             r = rel[:, it, :]
             m = lambda x: round(float(x.mean()), 2)
+            prev6 = rel[:, it - 1, 6] if it > 0 else rel[:, it, 5]
             print(json.dumps({
-                "it": it, "poll_start": m(r[:, 0]), "poll": m(r[:, 1] - r[:, 0]),
-                "cons_start": m(r[:, 5]), "cons_busy": m(r[:, 6] - r[:, 5]),
-                "storer_done": m(r[:, 7]), "done_after_cons": m(r[:, 7] - r[:, 6]),
-                "raiser_sees_done": m(r[:, 2] - r[:, 7]), "fence": m(r[:, 3] - r[:, 2]), "flag_stores": m(r[:, 4] - r[:, 3])}))
+                "it": it, "ctl_start": m(r[:, 0]), "poll": m(r[:, 1] - r[:, 0]),
+                "done_wait": m(r[:, 2] - r[:, 1]), "raise": m(r[:, 4] - r[:, 3]),
+                "wk_start": m(r[:, 5]), "wk_idle": m(r[:, 5] - prev6), "wk_busy": m(r[:, 6] - r[:, 5]),
+                "wk_busy_max": round(float((r[:, 6] - r[:, 5]).max()), 2)}))
     comm.destroy()
     dist.destroy_process_group()
 
