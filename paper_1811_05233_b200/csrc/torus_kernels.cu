@@ -26,6 +26,9 @@
 // every rank owns the same slice of every sub-chunk; cross-GPU ordering uses one
 // st.release.sys / ld.acquire.sys epoch flag per (phase, source rank, CTA).
 // No tensor cores: the path is a bandwidth-bound reduction (BASELINE.json north_star).
+#include <cstdio>
+#include <cstdlib>
+
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -1284,24 +1287,23 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
 }
 
 // N = 1: buf = from_wire(to_wire(buf)); the mean scale is x * 1.0 (identity).
-// HBM-bound: 8 B per element.  Each thread keeps kCastUnroll 32-byte vectors in flight
-// (4 x LDG.E.128 before the first store) over a grid of 4 CTAs per SM.
-constexpr int kCastUnroll = 4;
-template <int W>
-__global__ void __launch_bounds__(256) castscale_kernel(float* buf, unsigned long long n) {
+// HBM-bound: 8 B per element.  Each thread keeps U 32-byte vectors in flight (2U x
+// LDG.E.128 before the first store); the grid is CPS CTAs per SM of BLK threads.
+template <int W, int U, int BLK>
+__global__ void __launch_bounds__(BLK) castscale_kernel(float* buf, unsigned long long n) {
   const unsigned long long nv = (n + 7) / 8;
   const bool aligned = (reinterpret_cast<uintptr_t>(buf) & 15) == 0;
-  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-  for (unsigned long long v0 = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; v0 < nv;
-       v0 += stride * kCastUnroll) {
-    uint4 w[kCastUnroll];
+  const unsigned long long stride = (unsigned long long)gridDim.x * BLK;
+  for (unsigned long long v0 = blockIdx.x * (unsigned long long)BLK + threadIdx.x; v0 < nv;
+       v0 += stride * U) {
+    uint4 w[U];
 #pragma unroll
-    for (int u = 0; u < kCastUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const unsigned long long v = v0 + u * stride;
       if (v < nv) w[u] = load_user<DT_F32, W>(buf, v * 8, (int)min(8ull, n - v * 8), aligned);
     }
 #pragma unroll
-    for (int u = 0; u < kCastUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       const unsigned long long v = v0 + u * stride;
       if (v < nv) store_user<DT_F32, W>(buf, v * 8, (int)min(8ull, n - v * 8), w[u], aligned);
     }
@@ -1410,22 +1412,37 @@ int torus_kernel_max_ctas_per_sm(int dtype, int wire) {
   return 0;
 }
 
-cudaError_t launch_castscale(void* buf, unsigned long long n, int dtype, int wire,
-                             cudaStream_t stream) {
-  if (dtype != DT_F32) return cudaErrorInvalidValue;
+// castscale variant (env TORUS_CS = "<unroll>x<block>x<ctas per SM>", default 4x256x4)
+template <int W, int U, int BLK>
+cudaError_t launch_cs(float* buf, unsigned long long n, int cps, cudaStream_t stream) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const unsigned long long nv = (n + 7) / 8;
-  const unsigned long long want = (nv + 256ull * kCastUnroll - 1) / (256ull * kCastUnroll);
-  int blocks = (int)(want < (unsigned long long)sms * 4 ? want : (unsigned long long)sms * 4);
-  if (blocks < 1) blocks = 1;
-  if (wire == DT_F16)
-    castscale_kernel<DT_F16><<<blocks, 256, 0, stream>>>(reinterpret_cast<float*>(buf), n);
-  else if (wire == DT_BF16)
-    castscale_kernel<DT_BF16><<<blocks, 256, 0, stream>>>(reinterpret_cast<float*>(buf), n);
-  else
-    return cudaErrorInvalidValue;
+  const unsigned long long want = (nv + (unsigned long long)BLK * U - 1) / ((unsigned long long)BLK * U);
+  const unsigned long long cap = (unsigned long long)sms * cps;
+  const int blocks = (int)(want < 1 ? 1 : (want < cap ? want : cap));
+  castscale_kernel<W, U, BLK><<<blocks, BLK, 0, stream>>>(buf, n);
   return cudaGetLastError();
+}
+
+template <int W>
+cudaError_t launch_cs_variant(float* buf, unsigned long long n, cudaStream_t stream) {
+  int u = 4, blk = 256, cps = 4;
+  if (const char* v = getenv("TORUS_CS")) sscanf(v, "%dx%dx%d", &u, &blk, &cps);
+  if (u == 8 && blk == 256) return launch_cs<W, 8, 256>(buf, n, cps, stream);
+  if (u == 2 && blk == 256) return launch_cs<W, 2, 256>(buf, n, cps, stream);
+  if (u == 4 && blk == 512) return launch_cs<W, 4, 512>(buf, n, cps, stream);
+  if (u == 8 && blk == 512) return launch_cs<W, 8, 512>(buf, n, cps, stream);
+  if (u == 4 && blk == 128) return launch_cs<W, 4, 128>(buf, n, cps, stream);
+  return launch_cs<W, 4, 256>(buf, n, cps, stream);
+}
+
+cudaError_t launch_castscale(void* buf, unsigned long long n, int dtype, int wire,
+                             cudaStream_t stream) {
+  if (dtype != DT_F32) return cudaErrorInvalidValue;
+  if (wire == DT_F16) return launch_cs_variant<DT_F16>(reinterpret_cast<float*>(buf), n, stream);
+  if (wire == DT_BF16) return launch_cs_variant<DT_BF16>(reinterpret_cast<float*>(buf), n, stream);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_barrier(const RankDev* ranks, int nlocal, unsigned long long bar_off,
