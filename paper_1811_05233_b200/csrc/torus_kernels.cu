@@ -1,31 +1,20 @@
 // torus_kernels.cu -- sm_100a kernels of the 2D-Torus all-reduce (Sec. 2.2).
 //
-// One fused kernel per round runs the paper's three steps for one rank (or, in the
-// single-GPU emulation, for every virtual rank of the grid in one cooperative launch):
-//
-//   phase 1  horizontal reduce-scatter  ("Firstly, reduce-scatter is performed
-//            horizontally").  PUSH: each rank casts its buffer to the wire
-//            type on the first read (FP16 communication) and stores the
-//            share of every row peer's chunk straight into that peer's h_in slot over
-//            NVLink.  The chunk owner folds the X shares in the ring's order (SURVEY C5:
-//            w[c+1] + ... + w[c], f32 accumulation) and stores the rounded result into
-//            the v_in slot of the rank that owns each sub-chunk in its column (this is
-//            the send half of phase 2, fused).
-//   phase 2  vertical all-reduce on the 1/X shard ("Then, all-reduce is performed
-//            vertically").  Reduce-scatter: the sub-chunk owner folds the Y rows' values
-//            (rows rho+1 ... rho), applies the 1/N mean scale, rounds once,
-//            and PUSHES the result into its own and every column peer's chunk slot
-//            (the all-gather half, fused).
-//   phase 3  horizontal all-gather ("Finally, all-gather is performed horizontally").
-//            PULL: each rank reads every row peer's completed chunk over NVLink and
-//            writes its user buffer with the wire->dtype cast fused.
-//
-// Every element crosses NVLink exactly once per hop the algorithm needs; the
-// per-rank NVLink volume is (X-1)/X*S + 2(Y-1)/Y*S/X + (X-1)/X*S = 2(N-1)/N*S.
-// All data movement is 128-bit (LDG/STG.E.128), coalesced, CTA-sliced so that CTA b of
-// every rank owns the same slice of every sub-chunk; cross-GPU ordering uses one
-// st.release.sys / ld.acquire.sys epoch flag per (phase, source rank, CTA).
-// No tensor cores: the path is a bandwidth-bound reduction (BASELINE.json north_star).
+//   torus_kernel      (default) one fused launch per round: the paper's three steps as a
+//                     5-stage tile wavefront (A push / B row fold / C column fold + mean /
+//                     D column all-gather / E row all-gather), control warp + 15 data
+//                     warps, 128-bit LDG/STG over NVLink, one system fence per iteration
+//   torus_tma_kernel  (TORUS_KERNEL=tma) the same protocol with TMA bulk copies, a
+//                     producer / consumer / storer / poller / publisher split and a signal
+//                     CTA that fences from a quiet SM (parity-green, latency-bound today)
+//   castscale_kernel  the N = 1 degenerate case (fused cast round trip)
+//   ring_kernel, hier_kernel   the flat-ring and hierarchical baselines
+//   probe kernels     NVLink / fence calibration (torus_probe)
+//   multi_copy_kernel bucketed pack / unpack (NEXT-1)
+// Phases in the paper's words: "Firstly, reduce-scatter is performed horizontally. Then,
+// all-reduce is performed vertically. Finally, all-gather is performed horizontally."
+// Fold order, partition and rounding points follow the oracle, so every
+// dtype is bit-exact.  No tensor cores: a bandwidth-bound reduction, not a contraction.
 #include <cstdio>
 #include <cstdlib>
 
