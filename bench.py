@@ -378,9 +378,11 @@ def emit(line, args):
 # ----------------------------------------------------------------------------------------
 # the oracle (CPU) legs: cpu_baseline and --impl reference
 # ----------------------------------------------------------------------------------------
-def oracle_sample_size(X, Y):
-    # ~ a few seconds of single-threaded oracle work per call
-    return 1 << 22 if X * Y == 1 else (1 << 20)
+def oracle_sample_size(X, Y, steps=1):
+    # bounded single-threaded oracle work: ~0.1-0.3 s per step (1M elements at 2x4),
+    # smaller samples for long --steps runs so the reference arm ends within minutes
+    base = (1 << 22) if X * Y == 1 else (1 << 20)
+    return base if steps <= 200 else base // 4
 
 
 def time_oracle(X, Y, dtype_s, wire_s, op, D):
@@ -419,7 +421,7 @@ def run_reference(args):
             else DEFAULT_GRID.get(world, (world, 1)))
     dtype_s = args.dtype or ("f32" if world == 1 else "f16")
     wire_s = args.wire if dtype_s == "f32" else dtype_s
-    D = min(args.count, oracle_sample_size(X, Y))
+    D = min(args.count, oracle_sample_size(X, Y, args.steps))
     for _ in range(max(args.warmup, 1) if D < (1 << 21) else 1):
         time_oracle(X, Y, dtype_s, wire_s, args.op, D)
     ts = [time_oracle(X, Y, dtype_s, wire_s, args.op, D) for _ in range(args.steps)]
