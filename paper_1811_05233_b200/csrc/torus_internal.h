@@ -81,6 +81,7 @@ struct LaunchArgs {
   int nsig;                      // signal CTAs appended after the nlocal * G data CTAs
   int chunk_vecs;                // TMA kernel: vectors per ring buffer (a tile piece is
                                  // streamed through the ring in chunks of this size)
+  int fence_early;               // default kernel: fence before releasing the next iteration
 };
 
 // TMA kernel shared memory: nbufs ring buffers of one piece each (tile_vecs 16-byte wire

@@ -469,8 +469,8 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
       return __all_sync(0xffffffffu, ok);
     };
     // one system-scope fence for all the flags an iteration raises
-    auto raise_iter = [&](int it) {
-      asm volatile("fence.acq_rel.sys;" ::: "memory");
+    auto raise_iter = [&](int it, bool fence = true) {
+      if (fence) asm volatile("fence.acq_rel.sys;" ::: "memory");
       int e = 0;
       for (int p = 0; p < P; ++p) {
         const int t = it - SD * p;
@@ -500,9 +500,16 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
         bar_arrive(kBarReady);
         return;
       }
-      bar_arrive(kBarReady);              // workers start iteration it ...
-      stamp(tr, b, it, 3);
-      if (SD == 2 && it > 0) raise_iter(it - 1);  // ... while the fence for it-1 drains
+      if (SD == 2 && it > 0 && a.fence_early) {  // fence on it-1's stores only, then go
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        bar_arrive(kBarReady);
+        stamp(tr, b, it, 3);
+        raise_iter(it - 1, false);
+      } else {
+        bar_arrive(kBarReady);              // workers start iteration it ...
+        stamp(tr, b, it, 3);
+        if (SD == 2 && it > 0) raise_iter(it - 1);  // ... while the fence for it-1 drains
+      }
       stamp(tr, b, it, 4);
     }
     bar_sync(kBarDone);
