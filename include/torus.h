@@ -106,7 +106,11 @@ TORUS_API int torus_comm_destroy(torus_comm_t comm);
  * count == 0: TORUS_OK, nothing enqueued.  buf must be element-aligned; 16-byte
  * alignment selects the 128-bit vector path.  The caller keeps buf valid until the
  * stream work completes.  Errors: INVALID_ARG / UNSUPPORTED before anything is
- * enqueued; CUDA if a launch fails; TIMEOUT is reported asynchronously. */
+ * enqueued; CUDA if a launch fails; TIMEOUT is reported asynchronously.
+ * Messages of at most torus_comm_ll_max_bytes() wire bytes take the one-shot
+ * small-message kernel (every rank broadcasts, then folds locally in the same torus
+ * order: the result is bit-identical to the multi-phase path); larger ones the
+ * multi-phase kernel, in rounds of torus_comm_round_elems() elements. */
 TORUS_API int torus_allreduce(torus_comm_t comm, void* buf, size_t count, torus_dtype_t dtype,
                     torus_op_t op, torus_stream_t stream);
 
@@ -195,6 +199,13 @@ TORUS_API int torus_comm_ctas(torus_comm_t comm);                  /* CTAs per r
 /* Elements per round for a wire type: calls longer than this run as consecutive rounds
  * (one kernel launch each), each partitioned independently.  0 on error. */
 TORUS_API size_t torus_comm_round_elems(torus_comm_t comm, torus_dtype_t wire);
+
+/* Small-message threshold: calls with count * sizeof(wire) <= this many bytes run the
+ * one-shot kernel (NEXT-2; the latency term of PAPER.md:68).  Set at
+ * init from env TORUS_LL_MAX_BYTES (default 512 KiB; 0 disables) -- it must be the same
+ * on every rank, like the grid.  0 if disabled or comm is NULL.  The region it needs,
+ * 4 * N * threshold bytes, comes out of the slab (never more than a quarter of it). */
+TORUS_API size_t torus_comm_ll_max_bytes(torus_comm_t comm);
 
 /* Kernel launches one torus_allreduce_ex call with these arguments enqueues (0 for
  * count == 0 or a no-op N == 1 call).  Returns -1 on invalid arguments. */

@@ -51,6 +51,8 @@ size_t env_size(const char* name, size_t dflt) {
 }
 
 constexpr size_t kDefaultSlab = 320ull << 20;
+constexpr int kLLThreadsHost = 256;  // ll_kernel block size (torus_kernels.cu)
+constexpr size_t kDefaultLLMax = 512ull << 10;  // one-shot kernel up to 512 KiB of wire per rank
 
 struct Slab {
   int device;
@@ -100,14 +102,24 @@ struct torus_comm {
 
 namespace {
 
-SlabLayout make_layout(size_t slab_size, int G) {
+// ll_max: largest message (wire bytes per rank) for the one-shot small-message kernel;
+// its region is dropped when it would take more than a quarter of the slab.
+SlabLayout make_layout(size_t slab_size, int G, int N, size_t ll_max) {
   SlabLayout L;
   L.flags_bytes = flags_bytes_for(G);
   L.bar_off = L.flags_bytes;
-  L.data_off = L.bar_off + 65536;
+  L.ll_off = L.bar_off + 65536;
+  size_t slot = 2 * ((ll_max + 15) & ~(size_t)15);  // two LL lines per 16-byte vector
+  size_t region = (N >= 2 && ll_max) ? 2 * (size_t)N * slot : 0;
+  region = (region + 65535) & ~(size_t)65535;
+  if (region > slab_size / 4) region = slot = 0;
+  L.ll_slot = region ? slot : 0;
+  L.data_off = L.ll_off + region;
   L.size = slab_size;
   return L;
 }
+
+size_t ll_max_env() { return env_size("TORUS_LL_MAX_BYTES", kDefaultLLMax); }
 
 // Round capacity for a wire type (elements): R = k * q * X * Y with
 // h_in (X>1: X slots of R/X) + v_in (Y slots of R/(XY)) + chunk (R/X) in the data region.
@@ -142,7 +154,7 @@ unsigned long long hier_round_elems(const torus_comm* c, int wire) {
 }
 
 int alloc_comm_common(torus_comm* c) {
-  const size_t n_ep = (size_t)c->nlocal * c->G + c->nlocal;
+  const size_t n_ep = (size_t)c->nlocal * c->G + 3 * (size_t)c->nlocal;  // + barrier, ll[2]
   CU(cudaMalloc(&c->d_epochs, n_ep * sizeof(uint32_t)));
   CU(cudaMemset(c->d_epochs, 0, n_ep * sizeof(uint32_t)));
   CU(cudaHostAlloc(&c->h_err, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
@@ -180,6 +192,7 @@ int upload_ranks(torus_comm* c, const std::vector<char*>& bases) {
     r.epoch = c->d_epochs + (size_t)l * c->G;
     r.bar_epoch = c->d_epochs + (size_t)c->nlocal * c->G + l;
     r.err = c->d_err;
+    r.ll_ctr = c->d_epochs + (size_t)c->nlocal * (c->G + 1) + 2 * (size_t)l;
   }
   CU(cudaMemcpy(c->d_ranks, rd.data(), sizeof(RankDev) * c->nlocal, cudaMemcpyHostToDevice));
   return TORUS_OK;
@@ -374,7 +387,7 @@ int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t*
   if (cudaSetDevice(c->device) != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "cudaSetDevice");
   if (!rc) {
     c->G = pick_ctas(c->device, 1);
-    c->layout = make_layout(c->slab_size, c->G);
+    c->layout = make_layout(c->slab_size, c->G, world, ll_max_env());
     if (round_elems(c, TORUS_F32) == 0) rc = fail(TORUS_ERR_INVALID_ARG, "workspace too small");
   }
   for (int p = 0; !rc && p < world; ++p) {
@@ -426,7 +439,7 @@ int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_
   c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // 0 = auto (T ~ 3 tiles per slice)
   if (ctas > 0) setenv("TORUS_CTAS", std::to_string(ctas).c_str(), 1);
   c->G = pick_ctas(device, c->nlocal);
-  c->layout = make_layout(c->slab_size, c->G);
+  c->layout = make_layout(c->slab_size, c->G, c->world, ll_max_env());
   int rc = TORUS_OK;
   if (round_elems(c, TORUS_F32) == 0) rc = fail(TORUS_ERR_INVALID_ARG, "workspace too small");
   std::vector<char*> bases(c->world, nullptr);
@@ -529,6 +542,10 @@ size_t torus_comm_round_elems(torus_comm_t c, torus_dtype_t wire) {
   return (size_t)round_elems(c, wire);
 }
 
+size_t torus_comm_ll_max_bytes(torus_comm_t c) {
+  return c ? c->layout.ll_slot / 2 : 0;
+}
+
 int torus_comm_launches(torus_comm_t c, size_t count, torus_dtype_t dtype, torus_dtype_t wire) {
   if (!c || !valid_pair(dtype, wire)) return -1;
   if (count == 0) return 0;
@@ -573,6 +590,29 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   const unsigned long long sw = wire_size(wire);
   LaunchArgs a;
   memset(&a, 0, sizeof a);
+  if (count * sw <= c->layout.ll_slot / 2 && count <= R) {
+    // small message: one-shot broadcast + local fold in the torus order (NEXT-2)
+    a.ranks = c->d_ranks;
+    for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];
+    a.nlocal = c->nlocal;
+    a.q = (int)(kVecBytes / sw);
+    a.op = op;
+    a.inv_n = 1.0f / (float)(c->X * c->Y);
+    a.aligned = aligned ? 1 : 0;
+    a.timeout_ns = c->timeout_ns;
+    a.n = count;
+    a.buf_off = 0;
+    a.ll_off = c->layout.ll_off;
+    a.ll_slot = c->layout.ll_slot;
+    const unsigned long long nvec = (count * sw + kVecBytes - 1) / kVecBytes;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    // every CTA waits on peers' CTAs: keep the grid co-resident (2 per SM always fits)
+    const int cap = std::max(1, (int)env_size("TORUS_LL_CTAS", 2 * sms) / c->nlocal);
+    a.G = (int)std::min<unsigned long long>(cap, (nvec + kLLThreadsHost - 1) / kLLThreadsHost);
+    cudaError_t e = launch_ll(a, dtype, wire, c->virt, stream);
+    return e == cudaSuccess ? TORUS_OK : cuda_fail(e, "one-shot kernel launch");
+  }
   a.ranks = c->d_ranks;
   for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];
   a.nlocal = c->nlocal;

@@ -36,9 +36,13 @@ enum FlagKind : int {
 //        h_in[X][Lc]   (X > 1 only) shares of MY chunk pushed by each row peer
 //        v_in[Y][Lcs]  phase-1 results of MY sub-chunk pushed by each column peer
 //        chunk[Lc]     MY chunk, complete after phase 2 (pulled by row peers in phase 3)
+//   [ll_off, +2*N*ll_slot)    small-message one-shot region (ll_kernel): [parity][src]
+//                             slots of ll_slot bytes (0 when the LL path is disabled)
 struct SlabLayout {
   size_t flags_bytes;
   size_t bar_off;
+  size_t ll_off;
+  size_t ll_slot;
   size_t data_off;
   size_t size;
 };
@@ -52,6 +56,7 @@ struct RankDev {
   uint32_t* epoch;               // [G] local per-CTA call counters (device memory)
   uint32_t* bar_epoch;           // [1] barrier counter
   int* err;                      // host-mapped async error word
+  uint32_t* ll_ctr;              // [2] one-shot kernel: epoch, CTAs done in the current call
 };
 
 // Per-launch (per-round) arguments, passed by value.
@@ -82,6 +87,7 @@ struct LaunchArgs {
   int chunk_vecs;                // TMA kernel: vectors per ring buffer (a tile piece is
                                  // streamed through the ring in chunks of this size)
   int fence_early;               // default kernel: fence before releasing the next iteration
+  unsigned long long ll_off, ll_slot;  // one-shot kernel region (SlabLayout)
 };
 
 // TMA kernel shared memory: nbufs ring buffers of one piece each (tile_vecs 16-byte wire
@@ -168,6 +174,7 @@ cudaError_t launch_barrier(const RankDev* ranks, int nlocal, unsigned long long 
 int torus_kernel_max_ctas_per_sm(int dtype, int wire);
 cudaError_t launch_ring(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
 cudaError_t launch_hier(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
+cudaError_t launch_ll(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
 cudaError_t launch_multi_copy(const MultiTable& tab, int n, int dtype, int wire, void* staging,
                               bool pack, cudaStream_t stream);
 cudaError_t launch_probe(const RankDev* ranks, unsigned long long data_off, unsigned long long bytes,

@@ -109,6 +109,10 @@ class _CommBase:
         return _lib.load().torus_comm_launches(self._comm, count, _dtype_code(dtype),
                                                _dtype_code(wire or dtype))
 
+    def ll_max_bytes(self) -> int:
+        """Small-message threshold in wire bytes (torus_comm_ll_max_bytes; 0 = off)."""
+        return int(_lib.load().torus_comm_ll_max_bytes(self._comm))
+
     def probe(self, mode: int, nbytes: int = 0, iters: int = 0, ctas: int = 0,
               stream: torch.cuda.Stream | None = None) -> int:
         """Calibration probe (torus_probe); returns ns for mode 2, else 0 (time it yourself)."""

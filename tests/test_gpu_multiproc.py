@@ -118,16 +118,30 @@ def _worker(rank, world, port, cases, errfile):
         raise
 
 
-def _run(world, cases, tmp_path):
+def _run(world, cases, tmp_path, ll_max=None):
+    """ll_max: TORUS_LL_MAX_BYTES for the spawned ranks (None = library default)."""
     import torch.multiprocessing as mp
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     errfile = str(tmp_path / "errors.txt")
+    old = os.environ.get("TORUS_LL_MAX_BYTES")
+    if ll_max is not None:
+        os.environ["TORUS_LL_MAX_BYTES"] = str(ll_max)
     try:
         mp.spawn(_worker, args=(world, _free_port(), cases, errfile), nprocs=world, join=True)
     except Exception as e:
         msg = open(errfile).read() if os.path.exists(errfile) else str(e)
         raise AssertionError(msg) from None
+    finally:
+        if old is None:
+            os.environ.pop("TORUS_LL_MAX_BYTES", None)
+        else:
+            os.environ["TORUS_LL_MAX_BYTES"] = old
+
+
+# one-shot small-message kernel off (multi-phase kernel at every size) / forced on for
+# every size below 1 MiB of wire per rank (NEXT-2)
+LL_MODES = pytest.mark.parametrize("ll_max", [0, 1 << 20], ids=["multiphase", "oneshot"])
 
 
 PAIRS = [("f32", "f32"), ("f16", "f16"), ("bf16", "bf16"), ("i32", "i32"), ("f32", "f16"),
@@ -145,14 +159,16 @@ def _cases(grids, sizes=(1, 4099, 200_003), ops=("sum", "mean")):
     return out
 
 
-def test_two_gpus(tmp_path):
-    _run(2, _cases([(2, 1), (1, 2), (0, 2)]), tmp_path)
+@LL_MODES
+def test_two_gpus(tmp_path, ll_max):
+    _run(2, _cases([(2, 1), (1, 2), (0, 2)]), tmp_path, ll_max)
 
 
-def test_four_gpus(tmp_path):
+@LL_MODES
+def test_four_gpus(tmp_path, ll_max):
     cases = _cases([(2, 2), (4, 1), (1, 4), (0, 4), (-2, 2)], ops=("mean",))
     cases += [(2, 2, "f16", "f16", "mean", 25_557_032, "grad")]  # config 2 shape on 2x2
-    _run(4, cases, tmp_path)
+    _run(4, cases, tmp_path, ll_max)
 
 
 def _multi_worker(rank, world, port, errfile):

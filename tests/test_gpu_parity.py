@@ -64,22 +64,34 @@ def run_virtual(vt, ins, dtype, wire, op):
     return [from_dev(t, dtype) for t in ts]
 
 
-KERNELS = ["ldg", "tma"]  # the default LDG/STG kernel and the TMA-staged one
+# the default LDG/STG multi-phase kernel, the TMA-staged one, and the one-shot
+# small-message kernel (NEXT-2) forced for every size these tests use
+KERNELS = ["ldg", "tma", "ll"]
+LL_FORCED = 1 << 20  # 1 MiB of wire per rank: covers D = 200,003 f32
 
 
-def make_vt(X, Y, ws=0, kernel="ldg"):
-    """The kernel is chosen from TORUS_KERNEL when the communicator is built."""
+def make_vt(X, Y, ws=0, kernel="ldg", ll=None):
+    """The kernel is chosen from TORUS_KERNEL / TORUS_LL_MAX_BYTES when the communicator
+    is built; the multi-phase variants run with the one-shot path off (ll=0)."""
     import os
     from paper_1811_05233_b200 import VirtualTorus
-    old = os.environ.get("TORUS_KERNEL")
-    os.environ["TORUS_KERNEL"] = kernel
+    env = {"TORUS_KERNEL": "tma" if kernel == "tma" else "ldg",
+           "TORUS_LL_MAX_BYTES": str(ll if ll is not None else (LL_FORCED if kernel == "ll" else 0))}
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
-        return VirtualTorus(X, Y, device=0, ws_bytes=ws)
+        vt = VirtualTorus(X, Y, device=0, ws_bytes=ws)
     finally:
-        if old is None:
-            del os.environ["TORUS_KERNEL"]
-        else:
-            os.environ["TORUS_KERNEL"] = old
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
+    if kernel == "ll" and not ws:
+        assert vt.ll_max_bytes() == LL_FORCED
+    elif ll is None:
+        assert vt.ll_max_bytes() == 0
+    return vt
 
 
 @pytest.fixture(scope="module")
@@ -114,7 +126,7 @@ def test_virtual_grid_bit_exact(vgrids, X, Y, dtype, wire, op, kernel):
             assert_same(got[r], ref[r], f"{X}x{Y} {dtype}/{wire} {op} D={D} rank {r}")
 
 
-@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("kernel", ["ldg", "tma"])
 @pytest.mark.parametrize("X,Y", [(2, 2), (2, 4), (1, 4)])
 @pytest.mark.parametrize("dtype,wire", [("f16", "f16"), ("f32", "bf16"), ("i32", "i32")])
 def test_multi_round(vgrids, X, Y, dtype, wire, kernel):
@@ -201,7 +213,7 @@ def test_single_rank_cast_scale():
         vt.destroy()
 
 
-@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("kernel", ["ldg", "tma"])
 def test_full_size_resnet50_sampled(kernel):
     """BASELINE config 2 at full size, in the bench's launch configuration (2x4 grid,
     fp16, mean, default slab -> one round): sampled outputs vs the oracle's closed form,
@@ -232,6 +244,27 @@ def test_full_size_resnet50_sampled(kernel):
         exact = sum(a[idx].astype(np.float64) for a in ins) / 8
         mag = sum(np.abs(a[idx].astype(np.float64)) for a in ins) / 8
         assert (np.abs(got.astype(np.float64) - exact) <= 1e-2 * mag + 1e-7).all()
+    finally:
+        vt.destroy()
+
+
+@pytest.mark.parametrize("X,Y", [(2, 2), (2, 4), (4, 1)])
+def test_small_and_large_calls_interleaved(X, Y):
+    """Default threshold: calls alternate between the one-shot kernel (<= 512 KiB of wire)
+    and the multi-phase kernel; both epochs (LL parity, per-CTA flags) must stay in step,
+    and every result equals the oracle's torus fold bit for bit."""
+    vt = make_vt(X, Y, ll=512 << 10)
+    try:
+        assert vt.ll_max_bytes() == 512 << 10
+        N, R = X * Y, vt.round_elems(torch.float16)
+        sizes = (5, 262_144, 262_145, 1000, 300_000, 8, 9, 131_071, 3)  # f16: 512 KiB = 262,144
+        for it, D in enumerate(sizes):
+            ins = synthetic.make_all("normal", D, N, "f16", salt=50 + it)
+            got = run_virtual(vt, ins, "f16", "f16", "mean" if it % 2 else "sum")
+            ref = oracle.torus_allreduce(ins, X, Y, "f16", op="mean" if it % 2 else "sum", q=8,
+                                         round_elems=R)
+            for r in range(N):
+                assert_same(got[r], ref[r], f"interleaved call {it} D={D} rank {r}")
     finally:
         vt.destroy()
 

@@ -29,6 +29,11 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     X, Y = (map(int, args.grid.split("x")) if args.grid else {2: (1, 2), 4: (2, 2), 8: (2, 4)}[world])
     comm = TorusComm.init(X=X, Y=Y)
+    comm_mp = None
+    if "torus_mp" in args.impls:  # multi-phase kernel at every size (one-shot path off)
+        os.environ["TORUS_LL_MAX_BYTES"] = "0"
+        comm_mp = TorusComm.init(X=X, Y=Y)
+        del os.environ["TORUS_LL_MAX_BYTES"]
     dt = TD[args.dtype]
     esz = torch.tensor([], dtype=dt).element_size()
     bus = 2.0 * (world - 1) / world
@@ -40,6 +45,8 @@ def main():
         for impl in impls:
             if impl == "torus":
                 fn = lambda: comm.all_reduce(x, op="mean")  # noqa: E731
+            elif impl == "torus_mp":
+                fn = lambda: comm_mp.all_reduce(x, op="mean")  # noqa: E731
             elif impl == "ring":
                 fn = lambda: comm.ring_all_reduce(x, op="mean")  # noqa: E731
             else:
