@@ -52,7 +52,6 @@ size_t env_size(const char* name, size_t dflt) {
 
 constexpr size_t kDefaultSlab = 320ull << 20;
 constexpr int kLLThreadsHost = 256;  // ll_kernel block size (torus_kernels.cu)
-constexpr size_t kDefaultLLMax = 512ull << 10;  // one-shot kernel up to 512 KiB of wire per rank
 
 struct Slab {
   int device;
@@ -119,7 +118,16 @@ SlabLayout make_layout(size_t slab_size, int G, int N, size_t ll_max) {
   return L;
 }
 
-size_t ll_max_env() { return env_size("TORUS_LL_MAX_BYTES", kDefaultLLMax); }
+// Default threshold: the one-shot kernel moves 2(N-1) * S bytes per rank (LL lines, one
+// copy per peer) against the multi-phase kernel's 2(N-1)/N * S plus four dependent
+// hand-offs.  Measured on B200 (profiles/r01_ll_*): it is at least as fast as the
+// multi-phase kernel up to 8 MB at N = 2 and N = 4, so the default is
+// min(8 MiB, 12 MiB / (N-1)) -- 8 MiB at N=2, 4 MiB at N=4, ~1.7 MiB at N=8 (a slab
+// region of at most 64 MiB).
+size_t ll_max_env(int N) {
+  const size_t dflt = N < 2 ? 0 : std::min<size_t>(8ull << 20, ((12ull << 20) / (N - 1)) & ~(size_t)15);
+  return env_size("TORUS_LL_MAX_BYTES", dflt);
+}
 
 // Round capacity for a wire type (elements): R = k * q * X * Y with
 // h_in (X>1: X slots of R/X) + v_in (Y slots of R/(XY)) + chunk (R/X) in the data region.
@@ -387,7 +395,7 @@ int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t*
   if (cudaSetDevice(c->device) != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "cudaSetDevice");
   if (!rc) {
     c->G = pick_ctas(c->device, 1);
-    c->layout = make_layout(c->slab_size, c->G, world, ll_max_env());
+    c->layout = make_layout(c->slab_size, c->G, world, ll_max_env(world));
     if (round_elems(c, TORUS_F32) == 0) rc = fail(TORUS_ERR_INVALID_ARG, "workspace too small");
   }
   for (int p = 0; !rc && p < world; ++p) {
@@ -439,7 +447,7 @@ int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_
   c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // 0 = auto (T ~ 3 tiles per slice)
   if (ctas > 0) setenv("TORUS_CTAS", std::to_string(ctas).c_str(), 1);
   c->G = pick_ctas(device, c->nlocal);
-  c->layout = make_layout(c->slab_size, c->G, c->world, ll_max_env());
+  c->layout = make_layout(c->slab_size, c->G, c->world, ll_max_env(c->world));
   int rc = TORUS_OK;
   if (round_elems(c, TORUS_F32) == 0) rc = fail(TORUS_ERR_INVALID_ARG, "workspace too small");
   std::vector<char*> bases(c->world, nullptr);

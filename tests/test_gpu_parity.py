@@ -250,8 +250,8 @@ def test_full_size_resnet50_sampled(kernel):
 
 @pytest.mark.parametrize("X,Y", [(2, 2), (2, 4), (4, 1)])
 def test_small_and_large_calls_interleaved(X, Y):
-    """Default threshold: calls alternate between the one-shot kernel (<= 512 KiB of wire)
-    and the multi-phase kernel; both epochs (LL parity, per-CTA flags) must stay in step,
+    """With a 512 KiB threshold, calls alternate between the one-shot kernel and the
+    multi-phase kernel; both epochs (LL parity, per-CTA flags) must stay in step,
     and every result equals the oracle's torus fold bit for bit."""
     vt = make_vt(X, Y, ll=512 << 10)
     try:
@@ -265,6 +265,21 @@ def test_small_and_large_calls_interleaved(X, Y):
                                          round_elems=R)
             for r in range(N):
                 assert_same(got[r], ref[r], f"interleaved call {it} D={D} rank {r}")
+    finally:
+        vt.destroy()
+
+
+@pytest.mark.parametrize("X,Y", [(2, 1), (2, 2), (2, 4)])
+def test_default_ll_threshold(X, Y):
+    """Default one-shot threshold min(8 MiB, 12 MiB / (N-1)), 16-byte multiple."""
+    import os
+    if "TORUS_LL_MAX_BYTES" in os.environ:
+        pytest.skip("threshold overridden in the environment")
+    from paper_1811_05233_b200 import VirtualTorus
+    vt = VirtualTorus(X, Y, device=0)
+    try:
+        N = X * Y
+        assert vt.ll_max_bytes() == min(8 << 20, ((12 << 20) // (N - 1)) & ~15)
     finally:
         vt.destroy()
 

@@ -23,17 +23,34 @@ def main():
     ap.add_argument("--min-bytes", type=int, default=4096)
     ap.add_argument("--max-bytes", type=int, default=1 << 30)
     ap.add_argument("--impls", default="torus,ring,nccl")
+    ap.add_argument("--ll-max", type=int, default=4 << 20)
     args = ap.parse_args()
     world, rank, local = (int(os.environ[k]) for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     X, Y = (map(int, args.grid.split("x")) if args.grid else {2: (1, 2), 4: (2, 2), 8: (2, 4)}[world])
     comm = TorusComm.init(X=X, Y=Y)
-    comm_mp = None
-    if "torus_mp" in args.impls:  # multi-phase kernel at every size (one-shot path off)
-        os.environ["TORUS_LL_MAX_BYTES"] = "0"
-        comm_mp = TorusComm.init(X=X, Y=Y)
-        del os.environ["TORUS_LL_MAX_BYTES"]
+    # extra arms: "torus_mp" = multi-phase kernel at every size (one-shot path off);
+    # "torus_mpc<G>" = the same with G CTAs; "torus_ll" = one-shot path forced (--ll-max)
+    extra = {}
+    for impl in args.impls.split(","):
+        env = {}
+        if impl.startswith("torus_mp"):
+            env["TORUS_LL_MAX_BYTES"] = "0"
+            if impl.startswith("torus_mpc"):
+                env["TORUS_CTAS"] = impl[len("torus_mpc"):]
+        elif impl == "torus_ll":
+            env["TORUS_LL_MAX_BYTES"] = str(args.ll_max)
+        else:
+            continue
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        extra[impl] = TorusComm.init(X=X, Y=Y)
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     dt = TD[args.dtype]
     esz = torch.tensor([], dtype=dt).element_size()
     bus = 2.0 * (world - 1) / world
@@ -45,8 +62,8 @@ def main():
         for impl in impls:
             if impl == "torus":
                 fn = lambda: comm.all_reduce(x, op="mean")  # noqa: E731
-            elif impl == "torus_mp":
-                fn = lambda: comm_mp.all_reduce(x, op="mean")  # noqa: E731
+            elif impl in extra:
+                fn = lambda c=extra[impl]: c.all_reduce(x, op="mean")  # noqa: E731
             elif impl == "ring":
                 fn = lambda: comm.ring_all_reduce(x, op="mean")  # noqa: E731
             else:
