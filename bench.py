@@ -12,7 +12,8 @@ gradient buffer (25,557,032 elements, synthetic N(0,1)*2^-7 values, per-rank see
 value = busbw (GB/s) = S * 2(N-1)/N / t, t = max over ranks of the per-call device time
 (CUDA events on the launching stream); at N == 1 busbw is 0 by definition and value is
 the algbw S/t of the degenerate pass (S = fp16 message bytes).  L2 is flushed (256 MiB
-write) before every timed call, outside the events.  Rank 0 prints ONE JSON line.
+write, then a 256 MiB read that leaves it clean) before every timed call, outside the
+events.  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -179,6 +180,14 @@ def run_torus(args):
     buf = x0.clone()
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    clean = torch.zeros(64 << 20, dtype=torch.int32, device=dev)  # 256 MiB, read only
+
+    def evict(s):
+        """Untimed L2 eviction between timed calls: write 256 MiB (> 126 MB L2), then read
+        another 256 MiB so the flush's dirty lines are written back here, not inside the
+        timed call."""
+        flush.fill_(s & 0xFF)
+        clean.max()
 
     if args.algo == "nvls":
         comm.nvls_init(D * DT_BYTES[wire_s] + (4 << 20))
@@ -230,7 +239,7 @@ def run_torus(args):
     torch.cuda.synchronize()
     barrier(world)
     for s in range(args.steps):
-        flush.fill_(s & 0xFF)                   # evict L2 (256 MiB > 126 MB), untimed
+        evict(s)                                # L2 evicted and clean, untimed
         ev[s][0].record(stream)
         call()
         ev[s][1].record(stream)
@@ -258,7 +267,7 @@ def run_torus(args):
                for _ in range(args.steps)]
         ns = torch.cuda.current_stream()
         for s in range(args.steps):
-            flush.fill_(s & 0xFF)
+            evict(s)
             evn[s][0].record(ns)
             dist.all_reduce(buf, op=op)
             evn[s][1].record(ns)
@@ -339,7 +348,7 @@ def run_torus(args):
                    "algo": args.algo,
                    "parallelism": (f"ring{world}" if args.algo == "ring" else f"{args.algo}{X}x{Y}"),
                    "ctas_per_rank": comm_ctas(),
-                   "message_bytes": S, "l2": "flushed (256 MiB write) before every timed call",
+                   "message_bytes": S, "l2": "flushed before every timed call (256 MiB write, then 256 MiB read so no dirty flush lines are written back inside the timed call)",
                    "value_is": "busbw" if world > 1 else "algbw (busbw is 0 at N=1)"},
         "algbw": algbw, "busbw": busbw, "us_per_call": t * 1e6, "us_per_call_min": t_min * 1e6,
         "frac_nvlink_900": busbw / NVLINK_NOMINAL if world > 1 else None,
