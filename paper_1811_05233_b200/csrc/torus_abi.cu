@@ -631,6 +631,7 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   a.aligned = aligned ? 1 : 0;
   a.timeout_ns = c->timeout_ns;
   a.fence_early = (int)env_size("TORUS_FENCE_EARLY", 0);
+  a.poll_sleep = (unsigned)env_size("TORUS_POLL_SLEEP", 64);
   a.tile_vecs = c->tile_vecs;
   if (a.tile_vecs <= 0) {
     // auto: about kAutoTiles tiles per CTA slice of the largest sub-chunk (measured best

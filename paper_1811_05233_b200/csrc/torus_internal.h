@@ -88,6 +88,7 @@ struct LaunchArgs {
                                  // streamed through the ring in chunks of this size)
   int fence_early;               // default kernel: fence before releasing the next iteration
   unsigned long long ll_off, ll_slot;  // one-shot kernel region (SlabLayout)
+  unsigned poll_sleep;           // default kernel: ns of back-off between flag polls
 };
 
 // TMA kernel shared memory: nbufs ring buffers of one piece each (tile_vecs 16-byte wire

@@ -74,10 +74,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // Wait until *f >= v (wrap-safe).  Spin with relaxed loads and a short sleep -- a hot
 // loop of ld.acquire.sys (each one an L1 invalidate) slows every fence on the SM -- and
 // take the acquire once the value is there.  Returns false once `deadline` passes.
-__device__ __forceinline__ bool wait_flag_ge(const uint32_t* f, uint32_t v, unsigned long long deadline) {
+__device__ __forceinline__ bool wait_flag_ge(const uint32_t* f, uint32_t v, unsigned long long deadline,
+                                             unsigned sleep_ns = 64) {
   unsigned spin = 0;
   while ((int32_t)(ld_relaxed_sys(f) - v) < 0) {
-    __nanosleep(64);
+    if (sleep_ns) __nanosleep(sleep_ns);
     if ((++spin & 63u) == 0 && gtimer() > deadline) return false;
   }
   (void)ld_acquire_sys(f);
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
         const int t = it - SD * p;
         if (t < 0 || t >= T) continue;
         for_flags(kinds[p], t, true, [&](uint32_t* f, uint32_t v) {
-          if ((e++ & 31) == lane && ok) ok = wait_flag_ge(f, v, deadline);
+          if ((e++ & 31) == lane && ok) ok = wait_flag_ge(f, v, deadline, a.poll_sleep);
         });
       }
       return __all_sync(0xffffffffu, ok);
