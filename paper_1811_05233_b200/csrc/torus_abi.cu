@@ -97,8 +97,6 @@ struct torus_comm {
   void* d_staging = nullptr;              // multi-tensor staging buffer (wire type)
   size_t staging_bytes = 0;
   NvlsState nvls;                         // NVLS (multicast) variant, NEXT-4
-  int sched = 0;                          // env TORUS_SCHED=df: dataflow control loop
-  int auto_tiles = 3;                     // env TORUS_AUTO_TILES: tiles per CTA slice
 };
 
 namespace {
@@ -392,8 +390,6 @@ int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t*
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
   { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
   c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // 0 = auto (T ~ 3 tiles per slice)
-  { const char* sc = getenv("TORUS_SCHED"); c->sched = (sc && strcmp(sc, "df") == 0) ? 1 : 0; }
-  c->auto_tiles = std::max(1, (int)env_size("TORUS_AUTO_TILES", 3));
   int rc = TORUS_OK;
   std::vector<char*> bases(world, nullptr);
   if (cudaSetDevice(c->device) != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "cudaSetDevice");
@@ -449,8 +445,6 @@ int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
   { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
   c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // 0 = auto (T ~ 3 tiles per slice)
-  { const char* sc = getenv("TORUS_SCHED"); c->sched = (sc && strcmp(sc, "df") == 0) ? 1 : 0; }
-  c->auto_tiles = std::max(1, (int)env_size("TORUS_AUTO_TILES", 3));
   if (ctas > 0) setenv("TORUS_CTAS", std::to_string(ctas).c_str(), 1);
   c->G = pick_ctas(device, c->nlocal);
   c->layout = make_layout(c->slab_size, c->G, c->world, ll_max_env(c->world));
@@ -638,12 +632,11 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   a.timeout_ns = c->timeout_ns;
   a.fence_early = (int)env_size("TORUS_FENCE_EARLY", 0);
   a.poll_sleep = (unsigned)env_size("TORUS_POLL_SLEEP", 64);
-  a.sched = c->sched;
   a.tile_vecs = c->tile_vecs;
   if (a.tile_vecs <= 0) {
     // auto: about kAutoTiles tiles per CTA slice of the largest sub-chunk (measured best
     // at 2 and 4 GPUs); small calls get one tile (latency mode)
-    const unsigned long long kAutoTiles = c->auto_tiles;
+    constexpr unsigned long long kAutoTiles = 3;
     unsigned long long o, l0, s0;
     qpart(std::min<unsigned long long>(R, count), c->X, (int)(kVecBytes / sw), 0, &o, &l0);
     qpart(l0, c->Y, (int)(kVecBytes / sw), 0, &o, &s0);

@@ -89,7 +89,6 @@ struct LaunchArgs {
   int fence_early;               // default kernel: fence before releasing the next iteration
   unsigned long long ll_off, ll_slot;  // one-shot kernel region (SlabLayout)
   unsigned poll_sleep;           // default kernel: ns of back-off between flag polls
-  int sched;                     // default kernel: 0 lockstep wavefront, 1 dataflow
 };
 
 // TMA kernel shared memory: nbufs ring buffers of one piece each (tile_vecs 16-byte wire

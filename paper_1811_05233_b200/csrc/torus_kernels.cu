@@ -390,7 +390,6 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
 
   __shared__ uint32_t s_seq;
   __shared__ int s_abort;
-  __shared__ int s_job[2];  // dataflow scheduler: (stage kind, tile) posted to the workers
   if (tid == 0) {
     s_seq = R->epoch[b];
     s_abort = 0;
@@ -483,83 +482,6 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
       }
     };
     unsigned long long* const tr = (lane == 0 && lr == 0) ? a.trace : nullptr;
-    if (a.sched == 1) {
-      // ---- dataflow: post the next (stage, tile) job as soon as its inputs are visible
-      // (peer flags raised for that tile + my own previous stage done on it), preferring
-      // the latest stage; release the workers on it BEFORE fencing and raising the job
-      // that just finished, so the fence overlaps the next job's data movement.
-      int posted[kStages], done[kStages];
-      for (int p = 0; p < kStages; ++p) posted[p] = done[p] = 0;
-      auto ready = [&](int p, int t) -> bool {
-        bool ok = true;
-        int e = 0;
-        for_flags(kinds[p], t, true, [&](uint32_t* f, uint32_t v) {
-          if ((e++ & 31) == lane) ok = ok && (int32_t)(ld_relaxed_sys(f) - v) >= 0;
-        });
-        return __all_sync(0xffffffffu, ok);
-      };
-      auto acquire = [&](int p, int t) {
-        int e = 0;
-        for_flags(kinds[p], t, true, [&](uint32_t* f, uint32_t v) {
-          if ((e++ & 31) == lane) (void)ld_acquire_sys(f);
-        });
-      };
-      const int total = P * T;
-      int completed = 0, busy_p = -1, raise_p = -1, raise_t = 0;
-      unsigned spin = 0;
-      for (;;) {
-        if (busy_p < 0) {
-          int jp = -1;
-          for (int p = P - 1; p >= 0 && jp < 0; --p) {
-            const int t = posted[p];
-            if (t >= T || (p > 0 && done[p - 1] <= t)) continue;
-            if (ready(p, t)) jp = p;
-          }
-          if (jp >= 0) {
-            acquire(jp, posted[jp]);
-            if (lane == 0) {
-              s_job[0] = kinds[jp];
-              s_job[1] = posted[jp];
-            }
-            __syncwarp();
-            bar_arrive(kBarReady);
-            busy_p = jp;
-            ++posted[jp];
-          }
-        }
-        if (raise_p >= 0) {
-          asm volatile("fence.acq_rel.sys;" ::: "memory");
-          int e = 0;
-          for_flags(kinds[raise_p], raise_t, false, [&](uint32_t* f, uint32_t v) {
-            if ((e++ & 31) == lane) st_relaxed_sys(f, v);
-          });
-          raise_p = -1;
-          continue;
-        }
-        if (busy_p >= 0) {
-          bar_sync(kBarDone);
-          raise_p = busy_p;
-          raise_t = done[busy_p]++;
-          busy_p = -1;
-          ++completed;
-          continue;
-        }
-        if (completed == total) break;
-        if ((++spin & 63u) == 0 && gtimer() > deadline) {
-          if (lane == 0) {
-            atomicExch_system(R->err, kErrTimeout);
-            s_abort = 1;
-            s_job[0] = -1;
-          }
-          __syncwarp();
-          bar_arrive(kBarReady);
-          return;
-        }
-      }
-      if (lane == 0) s_job[0] = -1;  // release the workers from their job loop
-      __syncwarp();
-      bar_arrive(kBarReady);
-    } else {
     for (int it = 0; it < iters; ++it) {
       stamp(tr, b, it, 0);
       if (SD == 1 && it > 0) {            // latency mode: publish it-1 before waiting on it
@@ -593,12 +515,18 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
     }
     bar_sync(kBarDone);
     raise_iter(iters - 1);
-    }
   } else {
     // =============================== worker warps ===============================
     const int w = tid - kCtrlThreads;
     unsigned long long* const tr = (w == 0 && lr == 0) ? a.trace : nullptr;
-    auto run = [&](const int k, const int t) {
+    for (int it = 0; it < iters; ++it) {
+      bar_sync(kBarReady);
+      stamp(tr, b, it, 5);
+      if (*(volatile int*)&s_abort) return;
+      for (int p = 0; p < P; ++p) {
+        const int t = it - SD * p;
+        if (t < 0 || t >= T) continue;
+        const int k = kinds[p];
         if (k == kA) {
           // ---- phase 1 push ----
           for (int jj = 1; jj < X; ++jj) {
@@ -767,28 +695,9 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
             }
           }
         }
-    };
-    if (a.sched == 1) {
-      for (;;) {
-        bar_sync(kBarReady);
-        const int jk = *(volatile int*)&s_job[0], jt = *(volatile int*)&s_job[1];
-        if (jk < 0) break;
-        run(jk, jt);
-        bar_arrive(kBarDone);
       }
-    } else {
-      for (int it = 0; it < iters; ++it) {
-        bar_sync(kBarReady);
-        stamp(tr, b, it, 5);
-        if (*(volatile int*)&s_abort) return;
-        for (int p = 0; p < P; ++p) {
-          const int t = it - SD * p;
-          if (t < 0 || t >= T) continue;
-          run(kinds[p], t);
-        }
-        stamp(tr, b, it, 6);
-        bar_arrive(kBarDone);
-      }
+      stamp(tr, b, it, 6);
+      bar_arrive(kBarDone);
     }
   }
   __syncthreads();

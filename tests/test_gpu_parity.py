@@ -66,7 +66,7 @@ def run_virtual(vt, ins, dtype, wire, op):
 
 # the default LDG/STG multi-phase kernel, the TMA-staged one, and the one-shot
 # small-message kernel (NEXT-2) forced for every size these tests use
-KERNELS = ["ldg", "tma", "ll", "df"]  # df: the default kernel under the dataflow scheduler
+KERNELS = ["ldg", "tma", "ll"]
 LL_FORCED = 1 << 20  # 1 MiB of wire per rank: covers D = 200,003 f32
 
 
@@ -76,7 +76,6 @@ def make_vt(X, Y, ws=0, kernel="ldg", ll=None):
     import os
     from paper_1811_05233_b200 import VirtualTorus
     env = {"TORUS_KERNEL": "tma" if kernel == "tma" else "ldg",
-           "TORUS_SCHED": "df" if kernel == "df" else "lockstep",
            "TORUS_LL_MAX_BYTES": str(ll if ll is not None else (LL_FORCED if kernel == "ll" else 0))}
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
@@ -127,7 +126,7 @@ def test_virtual_grid_bit_exact(vgrids, X, Y, dtype, wire, op, kernel):
             assert_same(got[r], ref[r], f"{X}x{Y} {dtype}/{wire} {op} D={D} rank {r}")
 
 
-@pytest.mark.parametrize("kernel", ["ldg", "tma", "df"])
+@pytest.mark.parametrize("kernel", ["ldg", "tma"])
 @pytest.mark.parametrize("X,Y", [(2, 2), (2, 4), (1, 4)])
 @pytest.mark.parametrize("dtype,wire", [("f16", "f16"), ("f32", "bf16"), ("i32", "i32")])
 def test_multi_round(vgrids, X, Y, dtype, wire, kernel):
@@ -214,7 +213,7 @@ def test_single_rank_cast_scale():
         vt.destroy()
 
 
-@pytest.mark.parametrize("kernel", ["ldg", "tma", "df"])
+@pytest.mark.parametrize("kernel", ["ldg", "tma"])
 def test_full_size_resnet50_sampled(kernel):
     """BASELINE config 2 at full size, in the bench's launch configuration (2x4 grid,
     fp16, mean, default slab -> one round): sampled outputs vs the oracle's closed form,
