@@ -328,8 +328,14 @@ constexpr int kCtrlThreads = 32;                     // warp 0: flags, fences, s
 constexpr int kLdgThreads = TORUS_LDG_THREADS;       // threads per CTA of torus_kernel
 constexpr int kLdgCtasPerSm = 512 / TORUS_LDG_THREADS;
 constexpr int kWorkers = kLdgThreads - kCtrlThreads; // warps 1..: data movement
-constexpr int kUnroll = 4;                           // vectors per worker per pass (copies)
-constexpr int kUnrollFold = 2;                       // vectors per worker per pass (folds)
+#ifndef TORUS_UNROLL
+#define TORUS_UNROLL 2
+#endif
+#ifndef TORUS_UNROLL_FOLD
+#define TORUS_UNROLL_FOLD 2
+#endif
+constexpr int kUnroll = TORUS_UNROLL;                // vectors per worker per pass (copies)
+constexpr int kUnrollFold = TORUS_UNROLL_FOLD;       // vectors per worker per pass (folds)
 
 // Stages of the wavefront (iteration `it` runs A on tile it, B on it-1, ... E on it-4).
 enum Stage { kA = 0, kB = 1, kC = 2, kD = 3, kE = 4, kStages = 5 };
