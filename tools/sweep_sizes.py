@@ -31,7 +31,7 @@ def main():
     X, Y = (map(int, args.grid.split("x")) if args.grid else {2: (1, 2), 4: (2, 2), 8: (2, 4)}[world])
     comm = TorusComm.init(X=X, Y=Y)
     # extra arms: "torus_mp" = multi-phase kernel at every size (one-shot path off);
-    # "torus_mpc<G>" = the same with G CTAs; "torus_ll" = one-shot path forced (--ll-max)
+    # "torus_mpc<G>" = the same with G CTAs; "torus_mpt<V>" = with V-vector tiles; "torus_ll" = one-shot path forced (--ll-max)
     extra = {}
     for impl in args.impls.split(","):
         env = {}
@@ -39,6 +39,8 @@ def main():
             env["TORUS_LL_MAX_BYTES"] = "0"
             if impl.startswith("torus_mpc"):
                 env["TORUS_CTAS"] = impl[len("torus_mpc"):]
+            elif impl.startswith("torus_mpt"):  # fixed tile (vectors); huge = one tile
+                env["TORUS_TILE"] = impl[len("torus_mpt"):]
         elif impl == "torus_ll":
             env["TORUS_LL_MAX_BYTES"] = str(args.ll_max)
         else:
