@@ -120,12 +120,12 @@ SlabLayout make_layout(size_t slab_size, int G, int N, size_t ll_max) {
 
 // Default threshold: the one-shot kernel moves 2(N-1) * S bytes per rank (LL lines, one
 // copy per peer) against the multi-phase kernel's 2(N-1)/N * S plus four dependent
-// hand-offs.  Measured on B200 (profiles/r01_ll_*): it is at least as fast as the
-// multi-phase kernel up to 8 MB at N = 2 and N = 4, so the default is
-// min(8 MiB, 12 MiB / (N-1)) -- 8 MiB at N=2, 4 MiB at N=4, ~1.7 MiB at N=8 (a slab
-// region of at most 64 MiB).
+// hand-offs.  Measured on B200 (profiles/r01_ll_*, r01_single_tile_sizes.jsonl): it beats
+// the multi-phase kernel (single-tile mode) up to ~6.5 MB at N = 2 and ~3.6 MB at N = 4,
+// so the default is min(6 MiB, 12 MiB / (N-1)) -- 6 MiB at N=2, 4 MiB at N=4, ~1.7 MiB
+// at N=8 (a slab region of at most 64 MiB).
 size_t ll_max_env(int N) {
-  const size_t dflt = N < 2 ? 0 : std::min<size_t>(8ull << 20, ((12ull << 20) / (N - 1)) & ~(size_t)15);
+  const size_t dflt = N < 2 ? 0 : std::min<size_t>(6ull << 20, ((12ull << 20) / (N - 1)) & ~(size_t)15);
   return env_size("TORUS_LL_MAX_BYTES", dflt);
 }
 
@@ -642,7 +642,12 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
     qpart(l0, c->Y, (int)(kVecBytes / sw), 0, &o, &s0);
     const unsigned long long nv = (s0 * sw + kVecBytes - 1) / kVecBytes;
     const unsigned long long slice = (nv + c->G - 1) / c->G;
-    a.tile_vecs = (int)std::max<unsigned long long>(256, (slice + kAutoTiles - 1) / kAutoTiles);
+    // up to kOneTile vectors per CTA slice the call is one tile (stage distance 1): five
+    // latency-bound iterations beat ~11 pipelined ones (measured, r01_single_tile_sizes)
+    const unsigned long long one_tile = env_size("TORUS_ONE_TILE_MAX", 4096);
+    a.tile_vecs = slice <= one_tile
+                      ? (int)std::max<unsigned long long>(1, slice)
+                      : (int)std::max<unsigned long long>(256, (slice + kAutoTiles - 1) / kAutoTiles);
   }
   a.trace = c->d_trace;
   a.nbufs = 0;

@@ -66,7 +66,9 @@ def run_virtual(vt, ins, dtype, wire, op):
 
 # the default LDG/STG multi-phase kernel, the TMA-staged one, and the one-shot
 # small-message kernel (NEXT-2) forced for every size these tests use
-KERNELS = ["ldg", "tma", "ll"]
+# ldgt: the default kernel with 256-vector tiles, so small calls run the multi-tile
+# wavefront (stage distance 2) that the auto rule keeps for large slices
+KERNELS = ["ldg", "ldgt", "tma", "ll"]
 LL_FORCED = 1 << 20  # 1 MiB of wire per rank: covers D = 200,003 f32
 
 
@@ -76,6 +78,7 @@ def make_vt(X, Y, ws=0, kernel="ldg", ll=None):
     import os
     from paper_1811_05233_b200 import VirtualTorus
     env = {"TORUS_KERNEL": "tma" if kernel == "tma" else "ldg",
+           "TORUS_TILE": "256" if kernel == "ldgt" else "0",
            "TORUS_LL_MAX_BYTES": str(ll if ll is not None else (LL_FORCED if kernel == "ll" else 0))}
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
@@ -126,7 +129,7 @@ def test_virtual_grid_bit_exact(vgrids, X, Y, dtype, wire, op, kernel):
             assert_same(got[r], ref[r], f"{X}x{Y} {dtype}/{wire} {op} D={D} rank {r}")
 
 
-@pytest.mark.parametrize("kernel", ["ldg", "tma"])
+@pytest.mark.parametrize("kernel", ["ldg", "ldgt", "tma"])
 @pytest.mark.parametrize("X,Y", [(2, 2), (2, 4), (1, 4)])
 @pytest.mark.parametrize("dtype,wire", [("f16", "f16"), ("f32", "bf16"), ("i32", "i32")])
 def test_multi_round(vgrids, X, Y, dtype, wire, kernel):
@@ -271,7 +274,7 @@ def test_small_and_large_calls_interleaved(X, Y):
 
 @pytest.mark.parametrize("X,Y", [(2, 1), (2, 2), (2, 4)])
 def test_default_ll_threshold(X, Y):
-    """Default one-shot threshold min(8 MiB, 12 MiB / (N-1)), 16-byte multiple."""
+    """Default one-shot threshold min(6 MiB, 12 MiB / (N-1)), 16-byte multiple."""
     import os
     if "TORUS_LL_MAX_BYTES" in os.environ:
         pytest.skip("threshold overridden in the environment")
@@ -279,7 +282,7 @@ def test_default_ll_threshold(X, Y):
     vt = VirtualTorus(X, Y, device=0)
     try:
         N = X * Y
-        assert vt.ll_max_bytes() == min(8 << 20, ((12 << 20) // (N - 1)) & ~15)
+        assert vt.ll_max_bytes() == min(6 << 20, ((12 << 20) // (N - 1)) & ~15)
     finally:
         vt.destroy()
 
