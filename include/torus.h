@@ -202,7 +202,7 @@ TORUS_API size_t torus_comm_round_elems(torus_comm_t comm, torus_dtype_t wire);
 
 /* Small-message threshold: calls with count * sizeof(wire) <= this many bytes run the
  * one-shot kernel (NEXT-2; the latency term of PAPER.md:68).  Set at
- * init from env TORUS_LL_MAX_BYTES (default min(6 MiB, 12 MiB / (N-1)); 0 disables) --
+ * init from env TORUS_LL_MAX_BYTES (default min(6 MiB, 10 MiB / (N-1)); 0 disables) --
  * it must be the same on every rank, like the grid.  0 if disabled or comm is NULL.  The
  * region it needs, 4 * N * threshold bytes, comes out of the slab (the path is disabled
  * if that would exceed a quarter of it). */

@@ -122,10 +122,10 @@ SlabLayout make_layout(size_t slab_size, int G, int N, size_t ll_max) {
 // copy per peer) against the multi-phase kernel's 2(N-1)/N * S plus four dependent
 // hand-offs.  Measured on B200 (profiles/r01_ll_*, r01_single_tile_sizes.jsonl): it beats
 // the multi-phase kernel (single-tile mode) up to ~6.5 MB at N = 2 and ~3.6 MB at N = 4,
-// so the default is min(6 MiB, 12 MiB / (N-1)) -- 6 MiB at N=2, 4 MiB at N=4, ~1.7 MiB
-// at N=8 (a slab region of at most 64 MiB).
+// so the default is min(6 MiB, 10 MiB / (N-1)) -- 6 MiB at N=2, 3.3 MiB at N=4, 1.4 MiB
+// at N=8 (a slab region of at most 53 MiB).
 size_t ll_max_env(int N) {
-  const size_t dflt = N < 2 ? 0 : std::min<size_t>(6ull << 20, ((12ull << 20) / (N - 1)) & ~(size_t)15);
+  const size_t dflt = N < 2 ? 0 : std::min<size_t>(6ull << 20, ((10ull << 20) / (N - 1)) & ~(size_t)15);
   return env_size("TORUS_LL_MAX_BYTES", dflt);
 }
 

@@ -274,7 +274,7 @@ def test_small_and_large_calls_interleaved(X, Y):
 
 @pytest.mark.parametrize("X,Y", [(2, 1), (2, 2), (2, 4)])
 def test_default_ll_threshold(X, Y):
-    """Default one-shot threshold min(6 MiB, 12 MiB / (N-1)), 16-byte multiple."""
+    """Default one-shot threshold min(6 MiB, 10 MiB / (N-1)), 16-byte multiple."""
     import os
     if "TORUS_LL_MAX_BYTES" in os.environ:
         pytest.skip("threshold overridden in the environment")
@@ -282,7 +282,7 @@ def test_default_ll_threshold(X, Y):
     vt = VirtualTorus(X, Y, device=0)
     try:
         N = X * Y
-        assert vt.ll_max_bytes() == min(6 << 20, ((12 << 20) // (N - 1)) & ~15)
+        assert vt.ll_max_bytes() == min(6 << 20, ((10 << 20) // (N - 1)) & ~15)
     finally:
         vt.destroy()
 
