@@ -645,9 +645,13 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
     // up to kOneTile vectors per CTA slice the call is one tile (stage distance 1): five
     // latency-bound iterations beat ~11 pipelined ones (measured, r01_single_tile_sizes)
     const unsigned long long one_tile = env_size("TORUS_ONE_TILE_MAX", 4096);
-    a.tile_vecs = slice <= one_tile
-                      ? (int)std::max<unsigned long long>(1, slice)
-                      : (int)std::max<unsigned long long>(256, (slice + kAutoTiles - 1) / kAutoTiles);
+    const unsigned long long mid = std::max<size_t>(1, env_size("TORUS_MID_TILES", 1));
+    if (slice <= one_tile) {
+      a.tile_vecs = (int)std::max<unsigned long long>(1, (slice + mid - 1) / mid);
+      a.sd1 = 1;
+    } else {
+      a.tile_vecs = (int)std::max<unsigned long long>(256, (slice + kAutoTiles - 1) / kAutoTiles);
+    }
   }
   a.trace = c->d_trace;
   a.nbufs = 0;

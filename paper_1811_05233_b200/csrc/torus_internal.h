@@ -89,6 +89,7 @@ struct LaunchArgs {
   int fence_early;               // default kernel: fence before releasing the next iteration
   unsigned long long ll_off, ll_slot;  // one-shot kernel region (SlabLayout)
   unsigned poll_sleep;           // default kernel: ns of back-off between flag polls
+  int sd1;                       // default kernel: stage distance 1 even with T > 1
 };
 
 // TMA kernel shared memory: nbufs ring buffers of one piece each (tile_vecs 16-byte wire

@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
   // Stage distance: 2 (flags hide behind an iteration of data) when the call has several
   // tiles; 1 for single-tile (small) calls, where latency is all there is -- each stage
   // then waits on the previous one directly and the control warp raises before it polls.
-  const int SD = (T == 1) ? 1 : 2;
+  const int SD = (T == 1 || a.sd1) ? 1 : 2;
   const int iters = T + SD * (P - 1);
 
   if (tid < kCtrlThreads) {

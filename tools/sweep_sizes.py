@@ -41,6 +41,9 @@ def main():
                 env["TORUS_CTAS"] = impl[len("torus_mpc"):]
             elif impl.startswith("torus_mpt"):  # fixed tile (vectors); huge = one tile
                 env["TORUS_TILE"] = impl[len("torus_mpt"):]
+            elif impl.startswith("torus_mpm"):  # "torus_mpm<tiles>o<one_tile_max>"
+                m, o = impl[len("torus_mpm"):].split("o")
+                env["TORUS_MID_TILES"], env["TORUS_ONE_TILE_MAX"] = m, o
         elif impl == "torus_ll":
             env["TORUS_LL_MAX_BYTES"] = str(args.ll_max)
         else:
