@@ -97,22 +97,27 @@ struct torus_comm {
   void* d_staging = nullptr;              // multi-tensor staging buffer (wire type)
   size_t staging_bytes = 0;
   NvlsState nvls;                         // NVLS (multicast) variant, NEXT-4
+  size_t ll2_max = 0;                     // two-shot LL up to this many wire bytes (N >= 3)
 };
 
 namespace {
 
 // ll_max: largest message (wire bytes per rank) for the one-shot small-message kernel;
 // its region is dropped when it would take more than a quarter of the slab.
-SlabLayout make_layout(size_t slab_size, int G, int N, size_t ll_max) {
+// ll2_max: largest message for the two-shot variant (N >= 3); per parity it needs 2N
+// slots of two LL lines per vector of the largest sub-chunk, ~4 * ll2_max bytes.
+SlabLayout make_layout(size_t slab_size, int G, int N, size_t ll_max, size_t ll2_max) {
   SlabLayout L;
   L.flags_bytes = flags_bytes_for(G);
   L.bar_off = L.flags_bytes;
   L.ll_off = L.bar_off + 65536;
   size_t slot = 2 * ((ll_max + 15) & ~(size_t)15);  // two LL lines per 16-byte vector
   size_t region = (N >= 2 && ll_max) ? 2 * (size_t)N * slot : 0;
+  if (N >= 3 && ll2_max) region = std::max(region, 8 * ll2_max + 64 * (size_t)N * 32);
   region = (region + 65535) & ~(size_t)65535;
   if (region > slab_size / 4) region = slot = 0;
   L.ll_slot = region ? slot : 0;
+  L.ll_region = region;
   L.data_off = L.ll_off + region;
   L.size = slab_size;
   return L;
@@ -390,12 +395,13 @@ int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t*
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
   { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
   c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // 0 = auto (T ~ 3 tiles per slice)
+  c->ll2_max = env_size("TORUS_LL2_MAX_BYTES", 0);
   int rc = TORUS_OK;
   std::vector<char*> bases(world, nullptr);
   if (cudaSetDevice(c->device) != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "cudaSetDevice");
   if (!rc) {
     c->G = pick_ctas(c->device, 1);
-    c->layout = make_layout(c->slab_size, c->G, world, ll_max_env(world));
+    c->layout = make_layout(c->slab_size, c->G, world, ll_max_env(world), c->ll2_max);
     if (round_elems(c, TORUS_F32) == 0) rc = fail(TORUS_ERR_INVALID_ARG, "workspace too small");
   }
   for (int p = 0; !rc && p < world; ++p) {
@@ -445,9 +451,10 @@ int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
   { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
   c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // 0 = auto (T ~ 3 tiles per slice)
+  c->ll2_max = env_size("TORUS_LL2_MAX_BYTES", 0);
   if (ctas > 0) setenv("TORUS_CTAS", std::to_string(ctas).c_str(), 1);
   c->G = pick_ctas(device, c->nlocal);
-  c->layout = make_layout(c->slab_size, c->G, c->world, ll_max_env(c->world));
+  c->layout = make_layout(c->slab_size, c->G, c->world, ll_max_env(c->world), c->ll2_max);
   int rc = TORUS_OK;
   if (round_elems(c, TORUS_F32) == 0) rc = fail(TORUS_ERR_INVALID_ARG, "workspace too small");
   std::vector<char*> bases(c->world, nullptr);
@@ -612,6 +619,8 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
     a.buf_off = 0;
     a.ll_off = c->layout.ll_off;
     a.ll_slot = c->layout.ll_slot;
+    a.ll_half = c->layout.ll_region / 2;
+    a.ll_two_shot = 0;
     const unsigned long long nvec = (count * sw + kVecBytes - 1) / kVecBytes;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -620,6 +629,37 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
     a.G = (int)std::min<unsigned long long>(cap, (nvec + kLLThreadsHost - 1) / kLLThreadsHost);
     cudaError_t e = launch_ll(a, dtype, wire, c->virt, stream);
     return e == cudaSuccess ? TORUS_OK : cuda_fail(e, "one-shot kernel launch");
+  }
+  if (c->world >= 3 && c->layout.ll_region && count * sw <= c->ll2_max && count <= R) {
+    // mid-size message: two-shot LL (scatter to the torus owners, fold, broadcast back)
+    const int q = (int)(kVecBytes / sw);
+    unsigned long long o, l0, s0;
+    qpart(count, c->X, q, 0, &o, &l0);
+    qpart(l0, c->Y, q, 0, &o, &s0);
+    const unsigned long long slot = 2 * ((s0 * sw + kVecBytes - 1) / kVecBytes) * kVecBytes;
+    if (2ull * c->world * slot <= c->layout.ll_region / 2) {
+      a.ranks = c->d_ranks;
+      for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];
+      a.nlocal = c->nlocal;
+      a.q = q;
+      a.op = op;
+      a.inv_n = 1.0f / (float)(c->X * c->Y);
+      a.aligned = aligned ? 1 : 0;
+      a.timeout_ns = c->timeout_ns;
+      a.n = count;
+      a.buf_off = 0;
+      a.ll_off = c->layout.ll_off;
+      a.ll_slot = slot;
+      a.ll_half = c->layout.ll_region / 2;
+      a.ll_two_shot = 1;
+      const unsigned long long nvec = (count * sw + kVecBytes - 1) / kVecBytes;
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+      const int cap = std::max(1, (int)env_size("TORUS_LL_CTAS", 2 * sms) / c->nlocal);
+      a.G = (int)std::min<unsigned long long>(cap, (nvec + kLLThreadsHost - 1) / kLLThreadsHost);
+      cudaError_t e = launch_ll(a, dtype, wire, c->virt, stream);
+      return e == cudaSuccess ? TORUS_OK : cuda_fail(e, "two-shot kernel launch");
+    }
   }
   a.ranks = c->d_ranks;
   for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];

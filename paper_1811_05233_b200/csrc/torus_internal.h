@@ -43,6 +43,7 @@ struct SlabLayout {
   size_t bar_off;
   size_t ll_off;
   size_t ll_slot;
+  size_t ll_region;   // bytes of the LL region (two parity halves)
   size_t data_off;
   size_t size;
 };
@@ -88,6 +89,8 @@ struct LaunchArgs {
                                  // streamed through the ring in chunks of this size)
   int fence_early;               // default kernel: fence before releasing the next iteration
   unsigned long long ll_off, ll_slot;  // one-shot kernel region (SlabLayout)
+  unsigned long long ll_half;    // bytes per parity half of the LL region
+  int ll_two_shot;               // 1: ll2_kernel (two-shot) instead of ll_kernel
   unsigned poll_sleep;           // default kernel: ns of back-off between flag polls
   int sd1;                       // default kernel: stage distance 1 even with T > 1
 };

@@ -119,29 +119,35 @@ def _worker(rank, world, port, cases, errfile):
 
 
 def _run(world, cases, tmp_path, ll_max=None):
-    """ll_max: TORUS_LL_MAX_BYTES for the spawned ranks (None = library default)."""
+    """ll_max: (TORUS_LL_MAX_BYTES, TORUS_LL2_MAX_BYTES) for the spawned ranks (None =
+    library defaults)."""
     import torch.multiprocessing as mp
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     errfile = str(tmp_path / "errors.txt")
-    old = os.environ.get("TORUS_LL_MAX_BYTES")
+    keys = ("TORUS_LL_MAX_BYTES", "TORUS_LL2_MAX_BYTES")
+    old = {k: os.environ.get(k) for k in keys}
     if ll_max is not None:
-        os.environ["TORUS_LL_MAX_BYTES"] = str(ll_max)
+        for k, v in zip(keys, ll_max):
+            os.environ[k] = str(v)
     try:
         mp.spawn(_worker, args=(world, _free_port(), cases, errfile), nprocs=world, join=True)
     except Exception as e:
         msg = open(errfile).read() if os.path.exists(errfile) else str(e)
         raise AssertionError(msg) from None
     finally:
-        if old is None:
-            os.environ.pop("TORUS_LL_MAX_BYTES", None)
-        else:
-            os.environ["TORUS_LL_MAX_BYTES"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
 
-# one-shot small-message kernel off (multi-phase kernel at every size) / forced on for
-# every size below 1 MiB of wire per rank (NEXT-2)
-LL_MODES = pytest.mark.parametrize("ll_max", [0, 1 << 20], ids=["multiphase", "oneshot"])
+# LL paths off (multi-phase kernel at every size) / one-shot forced for every size below
+# 1 MiB of wire per rank (NEXT-2) / two-shot forced below 1 MiB (N >= 3)
+LL_MODES = pytest.mark.parametrize("ll_max", [(0, 0), (1 << 20, 0)], ids=["multiphase", "oneshot"])
+LL_MODES_4 = pytest.mark.parametrize("ll_max", [(0, 0), (1 << 20, 0), (0, 1 << 20)],
+                                     ids=["multiphase", "oneshot", "twoshot"])
 
 
 PAIRS = [("f32", "f32"), ("f16", "f16"), ("bf16", "bf16"), ("i32", "i32"), ("f32", "f16"),
@@ -164,7 +170,7 @@ def test_two_gpus(tmp_path, ll_max):
     _run(2, _cases([(2, 1), (1, 2), (0, 2)]), tmp_path, ll_max)
 
 
-@LL_MODES
+@LL_MODES_4
 def test_four_gpus(tmp_path, ll_max):
     cases = _cases([(2, 2), (4, 1), (1, 4), (0, 4), (-2, 2)], ops=("mean",))
     cases += [(2, 2, "f16", "f16", "mean", 25_557_032, "grad")]  # config 2 shape on 2x2

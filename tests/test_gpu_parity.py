@@ -68,7 +68,8 @@ def run_virtual(vt, ins, dtype, wire, op):
 # small-message kernel (NEXT-2) forced for every size these tests use
 # ldgt: the default kernel with 256-vector tiles, so small calls run the multi-tile
 # wavefront (stage distance 2) that the auto rule keeps for large slices
-KERNELS = ["ldg", "ldgt", "tma", "ll"]
+# ll2: the two-shot LL kernel forced (grids with N >= 3; N = 2 falls back to multi-phase)
+KERNELS = ["ldg", "ldgt", "tma", "ll", "ll2"]
 LL_FORCED = 1 << 20  # 1 MiB of wire per rank: covers D = 200,003 f32
 
 
@@ -79,7 +80,8 @@ def make_vt(X, Y, ws=0, kernel="ldg", ll=None):
     from paper_1811_05233_b200 import VirtualTorus
     env = {"TORUS_KERNEL": "tma" if kernel == "tma" else "ldg",
            "TORUS_TILE": "256" if kernel == "ldgt" else "0",
-           "TORUS_LL_MAX_BYTES": str(ll if ll is not None else (LL_FORCED if kernel == "ll" else 0))}
+           "TORUS_LL_MAX_BYTES": str(ll if ll is not None else (LL_FORCED if kernel == "ll" else 0)),
+           "TORUS_LL2_MAX_BYTES": str(LL_FORCED if kernel == "ll2" else 0)}
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
