@@ -37,6 +37,7 @@ def main():
         env = {}
         if impl.startswith("torus_mp"):
             env["TORUS_LL_MAX_BYTES"] = "0"
+            env["TORUS_LL2_MAX_BYTES"] = "0"
             if impl.startswith("torus_mpc"):
                 env["TORUS_CTAS"] = impl[len("torus_mpc"):]
             elif impl.startswith("torus_mpt"):  # fixed tile (vectors); huge = one tile
