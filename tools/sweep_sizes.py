@@ -47,6 +47,10 @@ def main():
                 env["TORUS_MID_TILES"], env["TORUS_ONE_TILE_MAX"] = m, o
         elif impl == "torus_ll":
             env["TORUS_LL_MAX_BYTES"] = str(args.ll_max)
+            env["TORUS_LL2_MAX_BYTES"] = "0"
+        elif impl == "torus_ll2":  # two-shot forced up to --ll-max
+            env["TORUS_LL_MAX_BYTES"] = "0"
+            env["TORUS_LL2_MAX_BYTES"] = str(args.ll_max)
         else:
             continue
         old = {k: os.environ.get(k) for k in env}
