@@ -109,7 +109,8 @@ TORUS_API int torus_comm_destroy(torus_comm_t comm);
  * enqueued; CUDA if a launch fails; TIMEOUT is reported asynchronously.
  * Messages of at most torus_comm_ll_max_bytes() wire bytes take the one-shot
  * small-message kernel (every rank broadcasts, then folds locally in the same torus
- * order: the result is bit-identical to the multi-phase path); larger ones the
+ * order: the result is bit-identical to the multi-phase path); up to
+ * torus_comm_ll2_max_bytes() the two-shot kernel (N >= 3); larger ones the
  * multi-phase kernel, in rounds of torus_comm_round_elems() elements. */
 TORUS_API int torus_allreduce(torus_comm_t comm, void* buf, size_t count, torus_dtype_t dtype,
                     torus_op_t op, torus_stream_t stream);
@@ -202,11 +203,19 @@ TORUS_API size_t torus_comm_round_elems(torus_comm_t comm, torus_dtype_t wire);
 
 /* Small-message threshold: calls with count * sizeof(wire) <= this many bytes run the
  * one-shot kernel (NEXT-2; the latency term of PAPER.md:68).  Set at
- * init from env TORUS_LL_MAX_BYTES (default min(6 MiB, 10 MiB / (N-1)); 0 disables) --
- * it must be the same on every rank, like the grid.  0 if disabled or comm is NULL.  The
- * region it needs, 4 * N * threshold bytes, comes out of the slab (the path is disabled
- * if that would exceed a quarter of it). */
+ * init from env TORUS_LL_MAX_BYTES (default 6 MiB at N = 2, 1.5 MiB / (N-1) at N >= 3;
+ * 0 disables) -- it must be the same on every rank, like the grid.  0 if disabled or
+ * comm is NULL.  The region it needs, 4 * N * threshold bytes, comes out of the slab
+ * (both LL paths are disabled if their region would exceed a quarter of it). */
 TORUS_API size_t torus_comm_ll_max_bytes(torus_comm_t comm);
+
+/* Mid-size threshold (N >= 3): calls above the one-shot threshold and up to this many
+ * wire bytes run the two-shot kernel -- each rank sends every sub-chunk C_{c,s} to its
+ * torus owner (s, c), the owner folds it in the torus order and broadcasts it back;
+ * bit-identical to the multi-phase path.  Env TORUS_LL2_MAX_BYTES (default 8 MiB at
+ * N >= 3; 0 disables; same on every rank); needs ~8x that many bytes of slab region.
+ * 0 if disabled, N < 3 or comm is NULL. */
+TORUS_API size_t torus_comm_ll2_max_bytes(torus_comm_t comm);
 
 /* Kernel launches one torus_allreduce_ex call with these arguments enqueues (0 for
  * count == 0 or a no-op N == 1 call).  Returns -1 on invalid arguments. */

@@ -56,6 +56,7 @@ PROTOTYPES = {
     "torus_comm_round_elems": (_sz, [_vp, _i]),
     "torus_comm_launches": (_i, [_vp, _sz, _i, _i]),
     "torus_comm_ll_max_bytes": (_sz, [_vp]),
+    "torus_comm_ll2_max_bytes": (_sz, [_vp]),
     "torus_comm_trace": (_i, [_vp, _c.POINTER(_ull), _sz]),
     "torus_probe": (_i, [_vp, _i, _sz, _i, _i, _c.POINTER(_ull), _vp]),
     "torus_pick_grid": (_i, [_i, _c.POINTER(_i), _c.POINTER(_i), _c.POINTER(_i)]),

@@ -127,12 +127,17 @@ SlabLayout make_layout(size_t slab_size, int G, int N, size_t ll_max, size_t ll2
 // copy per peer) against the multi-phase kernel's 2(N-1)/N * S plus four dependent
 // hand-offs.  Measured on B200 (profiles/r01_ll_*, r01_single_tile_sizes.jsonl): it beats
 // the multi-phase kernel (single-tile mode) up to ~6.5 MB at N = 2 and ~3.6 MB at N = 4,
-// so the default is min(6 MiB, 10 MiB / (N-1)) -- 6 MiB at N=2, 3.3 MiB at N=4, 1.4 MiB
-// at N=8 (a slab region of at most 53 MiB).
+// so at N = 2 the default is 6 MiB (a 48 MiB slab region).
+// With N >= 3 the two-shot variant takes over above 1.5 MiB / (N-1) (512 KiB at N=4,
+// where both take ~14 us) and runs up to 8 MiB (profiles/r01_ll2_*: 13-33 us from 256 KB
+// to 4 MB at 2x2 vs NCCL's 21-43); at N = 2 it would move the same bytes as the one-shot.
 size_t ll_max_env(int N) {
-  const size_t dflt = N < 2 ? 0 : std::min<size_t>(6ull << 20, ((10ull << 20) / (N - 1)) & ~(size_t)15);
+  size_t dflt = 0;
+  if (N == 2) dflt = 6ull << 20;
+  else if (N >= 3) dflt = ((3ull << 19) / (N - 1)) & ~(size_t)15;
   return env_size("TORUS_LL_MAX_BYTES", dflt);
 }
+size_t ll2_max_env(int N) { return env_size("TORUS_LL2_MAX_BYTES", N >= 3 ? (8ull << 20) : 0); }
 
 // Round capacity for a wire type (elements): R = k * q * X * Y with
 // h_in (X>1: X slots of R/X) + v_in (Y slots of R/(XY)) + chunk (R/X) in the data region.
@@ -395,7 +400,7 @@ int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t*
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
   { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
   c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // 0 = auto (T ~ 3 tiles per slice)
-  c->ll2_max = env_size("TORUS_LL2_MAX_BYTES", 0);
+  c->ll2_max = ll2_max_env(c->world);
   int rc = TORUS_OK;
   std::vector<char*> bases(world, nullptr);
   if (cudaSetDevice(c->device) != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "cudaSetDevice");
@@ -451,7 +456,7 @@ int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
   { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
   c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // 0 = auto (T ~ 3 tiles per slice)
-  c->ll2_max = env_size("TORUS_LL2_MAX_BYTES", 0);
+  c->ll2_max = ll2_max_env(c->world);
   if (ctas > 0) setenv("TORUS_CTAS", std::to_string(ctas).c_str(), 1);
   c->G = pick_ctas(device, c->nlocal);
   c->layout = make_layout(c->slab_size, c->G, c->world, ll_max_env(c->world), c->ll2_max);
@@ -559,6 +564,10 @@ size_t torus_comm_round_elems(torus_comm_t c, torus_dtype_t wire) {
 
 size_t torus_comm_ll_max_bytes(torus_comm_t c) {
   return c ? c->layout.ll_slot / 2 : 0;
+}
+
+size_t torus_comm_ll2_max_bytes(torus_comm_t c) {
+  return (c && c->world >= 3 && c->layout.ll_region) ? c->ll2_max : 0;
 }
 
 int torus_comm_launches(torus_comm_t c, size_t count, torus_dtype_t dtype, torus_dtype_t wire) {

@@ -113,6 +113,10 @@ class _CommBase:
         """Small-message threshold in wire bytes (torus_comm_ll_max_bytes; 0 = off)."""
         return int(_lib.load().torus_comm_ll_max_bytes(self._comm))
 
+    def ll2_max_bytes(self) -> int:
+        """Two-shot (mid-size) threshold in wire bytes (torus_comm_ll2_max_bytes; 0 = off)."""
+        return int(_lib.load().torus_comm_ll2_max_bytes(self._comm))
+
     def probe(self, mode: int, nbytes: int = 0, iters: int = 0, ctas: int = 0,
               stream: torch.cuda.Stream | None = None) -> int:
         """Calibration probe (torus_probe); returns ns for mode 2, else 0 (time it yourself)."""

@@ -69,6 +69,7 @@ def test_null_and_bad_arguments_rejected_without_gpu():
     assert L.torus_comm_round_elems(None, 1) == 0
     assert L.torus_comm_launches(None, 10, 1, 1) == -1
     assert L.torus_comm_ll_max_bytes(None) == 0
+    assert L.torus_comm_ll2_max_bytes(None) == 0
     assert L.torus_comm_ctas(None) == -1
     h = (_lib.torus_ipc_handle_t * 2)()
     c = ctypes.c_void_p()
