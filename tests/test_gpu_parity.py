@@ -377,3 +377,45 @@ def test_virtual_hierarchical_baseline_bit_exact(vgrids, X, Y, dtype, wire, op):
         ref = oracle.hier_allreduce(ins, X, Y, dtype, wire=wire, op=op, policy="hop", q=q_of(wire))
         for r in range(N):
             assert_same(from_dev(ts[r], dtype), ref[r], f"hier {X}x{Y} {dtype}/{wire} {op} D={D} rank {r}")
+
+
+def test_cuda_graph_capture_and_replay():
+    """The call path is CUDA-graph capturable (include/torus.h): no host sync, no
+    allocation, epochs device-resident.  Capture one call of each path -- one-shot,
+    two-shot, multi-phase -- on a virtual 2x2 grid, then replay the graph with fresh
+    inputs; every replay must equal the oracle (the epochs advance on the device)."""
+    X, Y, N = 2, 2, 4
+    from paper_1811_05233_b200 import VirtualTorus
+    vt = VirtualTorus(X, Y, device=0)
+    try:
+        R = vt.round_elems(torch.float16)
+        sizes = (1000, 1_000_000, 5_000_000)  # 2 KB one-shot, 2 MB two-shot, 10 MB multi-phase
+        assert 2 * sizes[0] <= vt.ll_max_bytes() < 2 * sizes[1] <= vt.ll2_max_bytes() < 2 * sizes[2]
+        bufs = [[torch.zeros(D, dtype=torch.float16, device="cuda") for _ in range(N)] for D in sizes]
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):  # warm-up outside the capture
+            for ts in bufs:
+                vt.all_reduce(ts, op="mean", stream=s)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for ts in bufs:
+                vt.all_reduce(ts, op="mean", stream=s)
+        for rep in range(2):
+            ins = [synthetic.make_all("normal", D, N, "f16", salt=70 + 3 * rep + k)
+                   for k, D in enumerate(sizes)]
+            for ts, arrs in zip(bufs, ins):
+                for t, a in zip(ts, arrs):
+                    t.copy_(torch.from_numpy(a))
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            assert vt.async_error() == 0
+            for ts, arrs, D in zip(bufs, ins, sizes):
+                ref = oracle.torus_allreduce(arrs, X, Y, "f16", op="mean", q=8, round_elems=R)
+                for r in range(N):
+                    assert_same(from_dev(ts[r], "f16"), ref[r], f"graph replay {rep} D={D} rank {r}")
+    finally:
+        vt.destroy()
