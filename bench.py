@@ -142,6 +142,62 @@ class Clocks:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+class NvlinkCounters:
+    """NVML NVLink data counters of this rank's GPU (KiB, cumulative, summed over links):
+    NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX (user payload, no protocol overhead) and
+    _RAW_TX / _RAW_RX (payload + protocol).  Read around a block of calls they give the
+    NVLink bytes per call measured by the hardware, without a profiler."""
+    FIELDS = {"data_tx": 138, "data_rx": 139, "raw_tx": 140, "raw_rx": 141}
+
+    def __init__(self, local):
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            bus = None
+            import torch
+            props = torch.cuda.get_device_properties(local)
+            bus = getattr(props, "pci_bus_id", None)
+            if bus is not None:
+                for i in range(pynvml.nvmlDeviceGetCount()):
+                    hh = pynvml.nvmlDeviceGetHandleByIndex(i)
+                    if pynvml.nvmlDeviceGetPciInfo(hh).bus == bus:
+                        self.h = hh
+            if self.h is None:
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+                idx = int(vis.split(",")[local]) if vis else local
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nvml = pynvml
+            self.links = 18
+        except Exception:  # no NVML: counters unavailable
+            self.h = None
+
+    def read(self):
+        if self.h is None:
+            return None
+        out = {}
+        any_ok = False
+        try:
+            for name, fid in self.FIELDS.items():
+                vals = self.nvml.nvmlDeviceGetFieldValues(self.h, [(fid, l) for l in range(self.links)])
+                tot = 0
+                for v in vals:
+                    if v.nvmlReturn == 0:
+                        tot += int(v.value.ullVal)
+                        any_ok = True
+                out[name] = tot * 1024  # KiB -> bytes
+        except Exception:
+            return None
+        # NOT_SUPPORTED on every link (e.g. this pool's containers: profiles/r02_nvml_probe.txt)
+        return out if any_ok else None
+
+    @staticmethod
+    def per_call(a, b, calls):
+        if a is None or b is None or calls <= 0:
+            return None
+        return {k: (b[k] - a[k]) / calls for k in a}
+
+
 # ----------------------------------------------------------------------------------------
 # the torus arm
 # ----------------------------------------------------------------------------------------
@@ -255,6 +311,19 @@ def run_torus(args):
     if comm.async_error():
         raise SystemExit("device watchdog fired during timing")
 
+    # ---- NVLink bytes per call, measured by the hardware (NVML counters, untimed) ----
+    nvl_torus = nvl_nccl = None
+    nvl = NvlinkCounters(local) if world > 1 else None
+    if nvl is not None and nvl.h is not None:
+        torch.cuda.synchronize()
+        barrier(world)
+        c0 = nvl.read()
+        for _ in range(args.steps):
+            call()
+        torch.cuda.synchronize()
+        c1 = nvl.read()
+        nvl_torus = gather_counters(NvlinkCounters.per_call(c0, c1, args.steps), world)
+
     # ---- NCCL comparator on the same tensor (like for like: AVG for mean) ----
     nccl = None
     if world > 1 and not args.no_nccl:
@@ -273,7 +342,17 @@ def run_torus(args):
             evn[s][1].record(ns)
         torch.cuda.synchronize()
         tn = gather_max(sum(a.elapsed_time(b) for a, b in evn) * 1e-3 / args.steps, world)
+        if nvl is not None and nvl.h is not None:
+            torch.cuda.synchronize()
+            barrier(world)
+            c0 = nvl.read()
+            for _ in range(args.steps):
+                dist.all_reduce(buf, op=op)
+            torch.cuda.synchronize()
+            c1 = nvl.read()
+            nvl_nccl = gather_counters(NvlinkCounters.per_call(c0, c1, args.steps), world)
         nccl = {"busbw": S / tn / 1e9 * bus, "algbw": S / tn / 1e9, "us": tn * 1e6,
+                "nvlink_bytes_per_call": nvl_nccl,
                 "version": ".".join(map(str, torch.cuda.nccl.version())),
                 "nvls_env": os.environ.get("NCCL_NVLS_ENABLE", "default")}
         buf.copy_(x0)
@@ -307,15 +386,16 @@ def run_torus(args):
     launches = comm.launches(D, TD[dtype_s], TD[wire_s])
     # ---- roofline of the dominant (only) kernel ----
     if world > 1:
-        alg_bytes = bus * S                        # NVLink bytes per rank per launch
-        achieved = alg_bytes / (t / launches) / 1e9
+        alg_bytes = bus * S                        # NVLink bytes per rank per call
+        achieved = alg_bytes / t / 1e9             # t is per call (all rounds)
         roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_MEASURED,
                 "unit": "GB/s", "frac": achieved / NVLINK_MEASURED,
                 "frac_of_nominal_900": achieved / NVLINK_NOMINAL,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction "
                                "(MEASURED_PEAKS.json has no NVLink entry)",
-                "traffic": None, "kernel": "torus_kernel",
-                "algorithmic_bytes_per_launch": alg_bytes}
+                "traffic": load_traffic(f"torus_{X}x{Y}"), "kernel": kernel_name(comm, D, TD, dtype_s, wire_s),
+                "algorithmic_bytes_per_call": alg_bytes,
+                "nvlink_bytes_per_call": nvl_torus}
     else:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
             os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -326,7 +406,7 @@ def run_torus(args):
                 "frac": achieved / hbm,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
                 "traffic": load_traffic("castscale"), "kernel": "castscale_kernel",
-                "algorithmic_bytes_per_launch": alg_bytes}
+                "algorithmic_bytes_per_call": alg_bytes}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -360,6 +440,25 @@ def run_torus(args):
 
 
 _CTAS = [None]
+
+
+def gather_counters(d, world):
+    """max over ranks of each NVML counter delta (None if any rank lacks NVML)"""
+    if world == 1 or d is None:
+        return d
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, d)
+    if any(o is None for o in out):
+        return None
+    return {k: max(o[k] for o in out) for k in d} | {"ranks": out}
+
+
+def kernel_name(comm, D, TD, dtype_s, wire_s):
+    try:
+        return comm.route(D, TD[dtype_s], TD[wire_s])
+    except Exception:
+        return "torus_kernel"
 
 
 def comm_ctas():

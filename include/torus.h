@@ -89,9 +89,29 @@ TORUS_API int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc
  * CTAs are co-resident); ws_bytes per rank (0 = default). */
 TORUS_API int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_comm_t* out);
 
-/* Collective teardown: a device barrier among all ranks (so no peer still reads this
- * rank's slab), then unmap peers, free the slab.  NULL is a no-op. */
+/* Collective teardown: waits for every collective this comm enqueued on any stream
+ * (device synchronize), then a device barrier among all ranks (so no peer still reads
+ * this rank's slab), then unmap peers, free the slab.  NULL is a no-op. */
 TORUS_API int torus_comm_destroy(torus_comm_t comm);
+
+/* Non-collective teardown for a comm whose peers never finished init (or are gone):
+ * drains this rank's own work, frees its resources, no barrier.  NULL is a no-op. */
+TORUS_API int torus_comm_abort(torus_comm_t comm);
+
+/* Configuration fingerprint: writes up to n words that must be EQUAL on every
+ * rank for the flag protocol to line up -- grid, CTA count, slab layout, routing
+ * thresholds, kernel choice and tiling knobs (all read from the environment once, at
+ * init).  Returns the number of meaningful words (<= n) or a negative error.  The Python
+ * binding all-gathers it right after init and fails with TORUS_ERR_MISMATCH if ranks
+ * differ.  words: host array [n]. */
+TORUS_API int torus_comm_config(torus_comm_t comm, unsigned long long* words, int n);
+
+/* Which kernel a torus_allreduce_ex call with these arguments runs ("torus_pull_kernel",
+ * "torus_kernel", "ll_kernel", "ll2_kernel", "castscale_kernel", "none"); a static
+ * string.  The routing is a pure function of (count, dtype, wire) and the comm's
+ * configuration, so it is the same on every rank. */
+TORUS_API const char* torus_comm_route(torus_comm_t comm, size_t count, torus_dtype_t dtype,
+                                       torus_dtype_t wire);
 
 /* ---------------------------------------------------------------------------------------
  * The all-reduce

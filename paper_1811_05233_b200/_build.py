@@ -9,8 +9,9 @@ import subprocess
 PKG = pathlib.Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-SOURCES = [CSRC / "torus_abi.cu", CSRC / "torus_kernels.cu", CSRC / "torus_nvls.cu"]
-HEADERS = [CSRC / "torus_internal.h", ROOT / "include" / "torus.h"]
+SOURCES = [CSRC / "torus_abi.cu", CSRC / "torus_kernels.cu", CSRC / "torus_pull.cu",
+           CSRC / "torus_nvls.cu"]
+HEADERS = [CSRC / "torus_internal.h", CSRC / "torus_device.cuh", ROOT / "include" / "torus.h"]
 LIB = PKG / "libtorus.so"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -35,14 +36,35 @@ def build(force: bool = False, verbose: bool = False, out: pathlib.Path | None =
           defines: tuple[str, ...] = ()) -> pathlib.Path:
     lib = out or LIB
     if force or out is not None or stale():
+        # one nvcc per translation unit, in parallel, then one link
         tmp = lib.with_name(f"{lib.name}.tmp{os.getpid()}")
-        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], *map(str, SOURCES), "-o", str(tmp)]
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
-        (PKG / "build_ptxas.log").write_text(res.stderr)
+        objs = [tmp.with_name(f"{p.stem}.{os.getpid()}.o") for p in SOURCES]
+        compile_flags = [f for f in FLAGS if f not in ("-shared", "-cudart", "static")]
+        procs = [subprocess.Popen([NVCC, *compile_flags, *[f"-D{d}" for d in defines], "-c", str(src),
+                                   "-o", str(o)], stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                  text=True) for src, o in zip(SOURCES, objs)]
+        logs = []
+        failed = None
+        for p in procs:
+            out_s, err_s = p.communicate()
+            logs.append(err_s)
+            if p.returncode != 0:
+                failed = (p.returncode, err_s)
+        if failed is None:
+            res = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                                  "-cudart", "static", *map(str, objs), "-o", str(tmp)],
+                                 capture_output=True, text=True)
+            if res.returncode != 0:
+                failed = (res.returncode, res.stderr)
+        for o in objs:
+            if o.exists():
+                o.unlink()
+        if failed is not None:
+            raise RuntimeError(f"nvcc failed ({failed[0]}):\n{failed[1][-4000:]}")
+        log = "\n".join(logs)
+        (PKG / "build_ptxas.log").write_text(log)
         if verbose:
-            print(res.stderr)
+            print(log)
         os.replace(tmp, lib)
     return lib
 

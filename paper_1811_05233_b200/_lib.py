@@ -34,6 +34,9 @@ PROTOTYPES = {
     "torus_comm_init": (_i, [_i, _i, _i, _i, _c.POINTER(torus_ipc_handle_t), _c.POINTER(_vp)]),
     "torus_vcomm_init": (_i, [_i, _i, _i, _i, _sz, _c.POINTER(_vp)]),
     "torus_comm_destroy": (_i, [_vp]),
+    "torus_comm_abort": (_i, [_vp]),
+    "torus_comm_config": (_i, [_vp, _c.POINTER(_ull), _i]),
+    "torus_comm_route": (_c.c_char_p, [_vp, _sz, _i, _i]),
     "torus_allreduce": (_i, [_vp, _vp, _sz, _i, _i, _vp]),
     "torus_allreduce_ex": (_i, [_vp, _vp, _sz, _i, _i, _i, _vp]),
     "torus_vallreduce": (_i, [_vp, _c.POINTER(_vp), _sz, _i, _i, _i, _vp]),

@@ -98,9 +98,32 @@ struct torus_comm {
   size_t staging_bytes = 0;
   NvlsState nvls;                         // NVLS (multicast) variant, NEXT-4
   size_t ll2_max = 0;                     // two-shot LL up to this many wire bytes (N >= 3)
+  // ---- knobs, read ONCE at init (they must agree across ranks: torus_comm_config) ----
+  int mode = 0;                           // kModePull (default) / kModePush / kModeTma
+  unsigned long long one_tile_max = 4096; // push kernel: single-tile threshold (vectors)
+  unsigned long long mid_tiles = 1;       // push kernel: tiles per slice below it
+  int fence_early = 0;                    // push kernel experiment
+  unsigned poll_sleep = 64;               // push kernel poll back-off (ns)
+  int pull_tv = 0;                        // pull kernel: vectors per tile (0 = auto)
+  int pull_slots = 0;                     // pull kernel: shared-memory ring slots (0 = auto)
+  int pull_ctas = 0;                      // pull kernel: CTA budget per rank (0 = all resident)
+  float pull_w[5] = {0.5f, 1.f, 1.f, 1.f, 1.f};  // pull kernel: CTA weight per kind
+  uint32_t* d_pull_ctr = nullptr;         // [nlocal][2] pull call epochs
+  int last_data_kernel = 0;               // kernel that last used the shared data region
+  int ctas_req = 0;                       // CTA count requested at init (0 = auto)
 };
 
 namespace {
+
+enum { kModePull = 0, kModePush = 1, kModeTma = 2 };
+// kernels that share the slab's data region (a switch between them needs a barrier)
+enum { kDataNone = 0, kDataPull = 1, kDataPush = 2, kDataRing = 3, kDataHier = 4 };
+
+size_t pull_flag_bytes(size_t slab_size) {
+  size_t b = std::min<size_t>(kPullFlagBytes, slab_size / 16);
+  b = std::max<size_t>(b, 65536);
+  return (b + 65535) & ~(size_t)65535;
+}
 
 // ll_max: largest message (wire bytes per rank) for the one-shot small-message kernel;
 // its region is dropped when it would take more than a quarter of the slab.
@@ -118,7 +141,8 @@ SlabLayout make_layout(size_t slab_size, int G, int N, size_t ll_max, size_t ll2
   if (region > slab_size / 4) region = slot = 0;
   L.ll_slot = region ? slot : 0;
   L.ll_region = region;
-  L.data_off = L.ll_off + region;
+  L.pull_flag_off = L.ll_off + region;
+  L.data_off = L.pull_flag_off + pull_flag_bytes(slab_size);
   L.size = slab_size;
   return L;
 }
@@ -143,11 +167,38 @@ size_t ll2_max_env(int N) { return env_size("TORUS_LL2_MAX_BYTES", N >= 3 ? (8ul
 // h_in (X>1: X slots of R/X) + v_in (Y slots of R/(XY)) + chunk (R/X) in the data region.
 unsigned long long round_elems(const torus_comm* c, int wire) {
   const unsigned long long sw = wire_size(wire), q = kVecBytes / sw;
-  if (c->slab_size <= c->layout.data_off) return 0;
-  const unsigned long long data_elems = (c->slab_size - c->layout.data_off) / sw;
-  const unsigned long long per_k = q * (unsigned long long)c->Y * ((c->X > 1 ? c->X : 0) + 2);
+  if (c->slab_size <= c->layout.data_off + 4096) return 0;
+  const unsigned long long data_elems = (c->slab_size - c->layout.data_off - 4096) / sw;
+  const unsigned long long X = (unsigned long long)c->X, Y = (unsigned long long)c->Y;
+  // R = k * q * X * Y elements.
+  // push kernel: h_in (X > 1: X slots of R/X) + v_in (Y slots of R/(XY)) + chunk (R/X)
+  // pull kernel, per call parity: win (R) + P1 (R/X, if X > 1 and Y > 1) + chunk (R/X)
+  unsigned long long per_k;
+  if (c->mode == kModePull) per_k = 2 * q * (X * Y + ((X > 1 && Y > 1) ? 2 : 1) * Y);
+  else per_k = q * Y * ((X > 1 ? X : 0) + 2);
   const unsigned long long k = data_elems / per_k;
-  return k * q * (unsigned long long)c->X * (unsigned long long)c->Y;
+  return k * q * X * Y;
+}
+
+// Pull-kernel slab regions for a round capacity R (identical on every rank).
+struct PullLayout {
+  unsigned long long win[2], p1[2], chunk[2];
+};
+PullLayout pull_layout(const torus_comm* c, unsigned long long R, unsigned long long sw) {
+  const unsigned long long X = (unsigned long long)c->X, Y = (unsigned long long)c->Y;
+  auto up = [](unsigned long long b) { return (b + 255) & ~255ull; };
+  const unsigned long long win = up(R * sw + 64), lc = up((R / X) * sw + 64);
+  PullLayout p;
+  unsigned long long off = c->layout.data_off;
+  for (int par = 0; par < 2; ++par) {
+    p.win[par] = off;
+    off += win;
+    p.p1[par] = off;
+    if (X > 1 && Y > 1) off += lc;
+    p.chunk[par] = off;
+    off += lc;
+  }
+  return p;
 }
 
 // Flat ring baseline: 2(N-1) slots of one chunk (R/N elements) per round.
@@ -172,7 +223,7 @@ unsigned long long hier_round_elems(const torus_comm* c, int wire) {
 }
 
 int alloc_comm_common(torus_comm* c) {
-  const size_t n_ep = (size_t)c->nlocal * c->G + 3 * (size_t)c->nlocal;  // + barrier, ll[2]
+  const size_t n_ep = (size_t)c->nlocal * c->G + 5 * (size_t)c->nlocal;  // + barrier, ll[2], pull[2]
   CU(cudaMalloc(&c->d_epochs, n_ep * sizeof(uint32_t)));
   CU(cudaMemset(c->d_epochs, 0, n_ep * sizeof(uint32_t)));
   CU(cudaHostAlloc(&c->h_err, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
@@ -211,25 +262,48 @@ int upload_ranks(torus_comm* c, const std::vector<char*>& bases) {
     r.bar_epoch = c->d_epochs + (size_t)c->nlocal * c->G + l;
     r.err = c->d_err;
     r.ll_ctr = c->d_epochs + (size_t)c->nlocal * (c->G + 1) + 2 * (size_t)l;
+    r.pull_ctr = c->d_epochs + (size_t)c->nlocal * (c->G + 3) + 2 * (size_t)l;
   }
   CU(cudaMemcpy(c->d_ranks, rd.data(), sizeof(RankDev) * c->nlocal, cudaMemcpyHostToDevice));
   return TORUS_OK;
 }
 
-int pick_ctas(int device, int nlocal) {
+int pick_ctas(int device, int nlocal, int ctas_req) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   int per_sm = torus_kernel_max_ctas_per_sm(TORUS_F32, TORUS_F16);
   for (int d = 0; d < 4; ++d) per_sm = std::min(per_sm, torus_kernel_max_ctas_per_sm(d, d));
   if (per_sm < 1) per_sm = 1;
   const int resident = sms * per_sm;
-  int want = (int)env_size("TORUS_CTAS", nlocal > 1 ? 16 : sms * per_sm);
+  int want = ctas_req > 0 ? ctas_req : (int)env_size("TORUS_CTAS", nlocal > 1 ? 16 : sms * per_sm);
   want = std::max(1, want);
   // every CTA of every rank that waits on another must be co-resident
   // the TMA kernel appends one signal CTA on its own SM
   const char* k = getenv("TORUS_KERNEL");
   const int spare = (k && strcmp(k, "tma") == 0) ? 1 : 0;
   return std::min(want, std::max(1, (resident - spare) / nlocal));
+}
+
+// Knobs are read once, here; every rank must see the same values (torus_comm_config
+// exposes them so the binding can check agreement at init).
+void read_knobs(torus_comm* c) {
+  c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
+  const char* k = getenv("TORUS_KERNEL");
+  c->mode = kModePull;
+  if (k && (strcmp(k, "push") == 0 || strcmp(k, "ldg") == 0)) c->mode = kModePush;
+  if (k && strcmp(k, "tma") == 0) c->mode = kModeTma;
+  c->tma = c->mode == kModeTma;
+  c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // push kernel; 0 = auto (T ~ 3 tiles per slice)
+  c->one_tile_max = env_size("TORUS_ONE_TILE_MAX", 4096);
+  c->mid_tiles = std::max<size_t>(1, env_size("TORUS_MID_TILES", 1));
+  c->fence_early = (int)env_size("TORUS_FENCE_EARLY", 0);
+  c->poll_sleep = (unsigned)env_size("TORUS_POLL_SLEEP", 64);
+  c->pull_tv = (int)env_size("TORUS_PULL_TILE", 0);
+  c->pull_slots = (int)env_size("TORUS_PULL_SLOTS", 0);
+  c->pull_ctas = (int)env_size("TORUS_PULL_CTAS", 0);
+  if (const char* w = getenv("TORUS_PULL_W"))
+    sscanf(w, "%f,%f,%f,%f,%f", &c->pull_w[0], &c->pull_w[1], &c->pull_w[2], &c->pull_w[3], &c->pull_w[4]);
+  c->ll2_max = ll2_max_env(c->world);
 }
 
 void destroy_resources(torus_comm* c) {
@@ -397,15 +471,12 @@ int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t*
   c->local_ranks = {rank};
   c->slab_size = own.size;
   c->own_slabs.push_back(own.ptr);
-  c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
-  { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
-  c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // 0 = auto (T ~ 3 tiles per slice)
-  c->ll2_max = ll2_max_env(c->world);
+  read_knobs(c);
   int rc = TORUS_OK;
   std::vector<char*> bases(world, nullptr);
   if (cudaSetDevice(c->device) != cudaSuccess) rc = fail(TORUS_ERR_CUDA, "cudaSetDevice");
   if (!rc) {
-    c->G = pick_ctas(c->device, 1);
+    c->G = pick_ctas(c->device, 1, 0);
     c->layout = make_layout(c->slab_size, c->G, world, ll_max_env(world), c->ll2_max);
     if (round_elems(c, TORUS_F32) == 0) rc = fail(TORUS_ERR_INVALID_ARG, "workspace too small");
   }
@@ -453,12 +524,9 @@ int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_
   for (int r = 0; r < c->world; ++r) c->local_ranks.push_back(r);
   if (ws_bytes == 0) ws_bytes = env_size("TORUS_WS_BYTES", kDefaultSlab);
   c->slab_size = (ws_bytes + 65535) & ~(size_t)65535;
-  c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
-  { const char* k = getenv("TORUS_KERNEL"); c->tma = (k && strcmp(k, "tma") == 0); }
-  c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // 0 = auto (T ~ 3 tiles per slice)
-  c->ll2_max = ll2_max_env(c->world);
-  if (ctas > 0) setenv("TORUS_CTAS", std::to_string(ctas).c_str(), 1);
-  c->G = pick_ctas(device, c->nlocal);
+  read_knobs(c);
+  c->ctas_req = ctas;
+  c->G = pick_ctas(device, c->nlocal, ctas);
   c->layout = make_layout(c->slab_size, c->G, c->world, ll_max_env(c->world), c->ll2_max);
   int rc = TORUS_OK;
   if (round_elems(c, TORUS_F32) == 0) rc = fail(TORUS_ERR_INVALID_ARG, "workspace too small");
@@ -489,7 +557,13 @@ int torus_comm_destroy(torus_comm_t c) {
   if (!c) return TORUS_OK;
   int rc = TORUS_OK;
   cudaSetDevice(c->device);
-  if (!c->poisoned && *c->h_err == 0 && c->world > 1) {
+  // Every collective this comm enqueued -- on any stream -- must have finished before
+  // the teardown barrier is launched: the barrier's own stream is not ordered after the
+  // user's streams, and a 64-thread barrier CTA fits beside a running all-reduce (ADVICE
+  // r1).  After the local drain, the barrier tells each rank that no peer still reads it.
+  cudaError_t se = cudaDeviceSynchronize();
+  if (se != cudaSuccess) rc = cuda_fail(se, "destroy: device synchronize");
+  if (!rc && !c->poisoned && *c->h_err == 0 && c->world > 1) {
     cudaStream_t s;
     if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess) {
       cudaError_t e = launch_barrier(c->d_ranks, c->nlocal, c->layout.bar_off, c->timeout_ns, s);
@@ -498,11 +572,17 @@ int torus_comm_destroy(torus_comm_t c) {
       cudaStreamDestroy(s);
     }
     if (*c->h_err) rc = fail(TORUS_ERR_TIMEOUT, "destroy barrier timed out");
-  } else {
-    cudaDeviceSynchronize();
   }
   destroy_resources(c);
   return rc;
+}
+
+int torus_comm_abort(torus_comm_t c) {
+  if (!c) return TORUS_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();  // local work only; no collective barrier
+  destroy_resources(c);
+  return TORUS_OK;
 }
 
 int torus_comm_get_async_error(torus_comm_t c) {
@@ -583,6 +663,173 @@ int torus_comm_launches(torus_comm_t c, size_t count, torus_dtype_t dtype, torus
 
 namespace {
 
+// ---- routing: which kernel serves a call (same decision on every rank) ----
+enum Route { kRouteNone = 0, kRouteCast, kRouteLL, kRouteLL2, kRoutePull, kRoutePush };
+const char* route_name(int r) {
+  switch (r) {
+    case kRouteCast: return "castscale_kernel";
+    case kRouteLL: return "ll_kernel";
+    case kRouteLL2: return "ll2_kernel";
+    case kRoutePull: return "torus_pull_kernel";
+    case kRoutePush: return "torus_kernel";
+    default: return "none";
+  }
+}
+
+// Two-shot slot bytes for a message (0 if it does not fit the LL region).
+unsigned long long ll2_slot(const torus_comm* c, size_t count, unsigned long long sw) {
+  const int q = (int)(kVecBytes / sw);
+  unsigned long long o, l0, s0;
+  qpart(count, c->X, q, 0, &o, &l0);
+  qpart(l0, c->Y, q, 0, &o, &s0);
+  const unsigned long long slot = 2 * ((s0 * sw + kVecBytes - 1) / kVecBytes) * kVecBytes;
+  return (2ull * c->world * slot <= c->layout.ll_region / 2) ? slot : 0;
+}
+
+// Pull kernel ring and tile (auto: 16 KiB wire tiles, a ring of >= 2 jobs' operands in
+// <= ~100 KiB so two CTAs fit per SM).  TV decides tile boundaries and flag indices, so
+// it depends only on values every rank shares (grid, dtypes, env).
+void pull_ring(const torus_comm* c, int ratio, int* tv, int* ns) {
+  const int need = std::max(c->X, c->Y);
+  int n = c->pull_slots > 0 ? c->pull_slots : std::max(6, 2 * need);
+  n = std::max(n, need + 1);
+  int t = c->pull_tv;
+  if (t <= 0) {
+    t = 1024;
+    while (t > 128 && (size_t)n * t * 16 * ratio > (100u << 10)) t /= 2;
+  }
+  *tv = t;
+  *ns = n;
+}
+
+unsigned long long pull_kmax(unsigned long long n, int X, int Y, int q, int TV) {
+  unsigned long long o, l0, s0;
+  qpart(n, X, q, 0, &o, &l0);
+  qpart(l0, Y, q, 0, &o, &s0);
+  const unsigned long long nv = (s0 + q - 1) / q;
+  return (nv + TV - 1) / TV;
+}
+
+bool pull_fits(const torus_comm* c, unsigned long long R, int wire, int dtype) {
+  if (c->mode != kModePull || c->world < 2 || std::max(c->X, c->Y) > 32) return false;
+  const unsigned long long sw = wire_size(wire);
+  int tv, ns;
+  pull_ring(c, (int)(wire_size(dtype) / sw), &tv, &ns);
+  const unsigned long long K = pull_kmax(R, c->X, c->Y, (int)(kVecBytes / sw), tv);
+  const unsigned long long X = c->X, Y = c->Y;
+  const unsigned long long words = (std::max(X, Y) * Y + 2 * Y + X * Y) * K + kMaxRanks;
+  return words * 4 <= c->layout.data_off - c->layout.pull_flag_off;
+}
+
+int plan_route(const torus_comm* c, size_t count, int dtype, int wire) {
+  if (count == 0) return kRouteNone;
+  if (c->world == 1) return dtype == wire ? kRouteNone : kRouteCast;
+  const unsigned long long R = round_elems(c, wire), sw = wire_size(wire);
+  if (count * sw <= c->layout.ll_slot / 2 && count <= R) return kRouteLL;
+  if (c->world >= 3 && c->layout.ll_region && count * sw <= c->ll2_max && count <= R && ll2_slot(c, count, sw))
+    return kRouteLL2;
+  if (pull_fits(c, R, wire, dtype)) return kRoutePull;
+  return kRoutePush;
+}
+
+// Serialise against the previous kernel of a different kind on the shared data region
+// (a ring/hier/push/pull switch must not overwrite slots a slower peer still
+// reads).  Every rank issues the same call sequence, so every rank inserts the barrier.
+int switch_data_kernel(torus_comm* c, int kind, cudaStream_t stream) {
+  if (c->last_data_kernel != kDataNone && c->last_data_kernel != kind) {
+    cudaError_t e = launch_barrier(c->d_ranks, c->nlocal, c->layout.bar_off, c->timeout_ns, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "algorithm-switch barrier");
+  }
+  c->last_data_kernel = kind;
+  return TORUS_OK;
+}
+
+int launch_pull_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype, int wire, int op,
+                       bool aligned, cudaStream_t stream) {
+  const unsigned long long R = round_elems(c, wire), sw = wire_size(wire);
+  const int ratio = (int)(wire_size(dtype) / sw);
+  PullArgs a;
+  memset(&a, 0, sizeof a);
+  a.ranks = c->d_ranks;
+  for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];
+  a.nlocal = c->nlocal;
+  a.q = (int)(kVecBytes / sw);
+  a.op = op;
+  a.inv_n = 1.0f / (float)(c->X * c->Y);
+  a.aligned = aligned ? 1 : 0;
+  a.timeout_ns = c->timeout_ns;
+  const PullLayout L = pull_layout(c, R, sw);
+  for (int p = 0; p < 2; ++p) {
+    a.win_off[p] = L.win[p];
+    a.p1_off[p] = L.p1[p];
+    a.chunk_off[p] = L.chunk[p];
+  }
+  if (L.chunk[1] + (R / c->X) * sw + 64 > c->slab_size) return fail(TORUS_ERR_INVALID_ARG, "pull layout overflow");
+  a.flag_off = c->layout.pull_flag_off;
+  int tv, ns;
+  pull_ring(c, ratio, &tv, &ns);
+  a.TV = tv;
+  a.nslots = ns;
+  a.slot_bytes = tv * 16 * ratio;
+  // CTAs per kind, proportional to the bytes each kind moves (SURVEY 8(d) per-kernel
+  // table); every CTA of every rank must be co-resident (they spin on each other)
+  static int cached_smem = -1, cached_per_sm = 0;
+  const int smem = (int)pull_smem_bytes(ns, a.slot_bytes);
+  if (smem != cached_smem) {
+    cached_per_sm = pull_ctas_per_sm((size_t)smem);
+    cached_smem = smem;
+  }
+  if (cached_per_sm < 1) return fail(TORUS_ERR_UNSUPPORTED, "pull kernel does not fit an SM (%d B smem)", smem);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  int gtot = sms * cached_per_sm / c->nlocal;
+  if (c->pull_ctas > 0) gtot = std::min(gtot, c->pull_ctas);
+  const int X = c->X, Y = c->Y;
+  const bool own_copy = !(dtype == wire && aligned);  // S0 also copies my own chunk
+  double w[5] = {0, 0, 0, 0, 0};
+  const double f0 = X > 1 ? (double)(X - 1) / X + (own_copy ? 1.0 / X : 0.0)
+                          : (double)(Y - 1) / Y + (own_copy ? 1.0 / Y : 0.0);
+  w[0] = c->pull_w[0] * f0 * ratio;
+  if (X > 1) w[1] = c->pull_w[1] * (double)(X - 1) / X;
+  if (Y > 1) w[2] = c->pull_w[2] * (double)(Y - 1) / Y / X;
+  if (Y > 1) w[3] = c->pull_w[3] * (double)(Y - 1) / Y / X;
+  if (X > 1) w[4] = c->pull_w[4] * (double)(X - 1) / X;
+  double wsum = 0;
+  int kinds = 0;
+  for (int k = 0; k < 5; ++k) {
+    if (w[k] > 0) ++kinds;
+    wsum += w[k];
+  }
+  if (gtot < kinds) return fail(TORUS_ERR_UNSUPPORTED, "pull kernel needs %d CTAs per rank, %d fit", kinds, gtot);
+  int gs = 0;
+  for (int k = 0; k < 5; ++k) {
+    a.g[k] = w[k] > 0 ? std::max(1, (int)(gtot * w[k] / wsum)) : 0;
+    gs += a.g[k];
+  }
+  while (gs > gtot) {  // trim the largest kind
+    int kb = 0;
+    for (int k = 1; k < 5; ++k)
+      if (a.g[k] > a.g[kb]) kb = k;
+    --a.g[kb];
+    --gs;
+  }
+  a.gsum = gs;
+  for (unsigned long long r0 = 0; r0 < count; r0 += R) {
+    a.n = std::min<unsigned long long>(R, count - r0);
+    a.buf_off = r0;
+    const unsigned long long K = pull_kmax(a.n, X, Y, a.q, tv);
+    a.Kmax = (int)std::max<unsigned long long>(1, K);
+    a.fl_win = 0;
+    a.fl_p1 = (unsigned long long)std::max(X, Y) * Y * a.Kmax;
+    a.fl_v = a.fl_p1 + (unsigned long long)Y * a.Kmax;
+    a.fl_c = a.fl_v + (unsigned long long)Y * a.Kmax;
+    a.fl_pres = a.fl_c + (unsigned long long)X * Y * a.Kmax;
+    cudaError_t e = launch_pull(a, dtype, wire, c->virt, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "pull kernel launch");
+  }
+  return TORUS_OK;
+}
+
 int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, int wire, int op,
                    cudaStream_t stream) {
   if (!c) return fail(TORUS_ERR_INVALID_ARG, "comm is NULL");
@@ -605,31 +852,38 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
     if (p % kVecBytes) aligned = false;
   }
   if (count > (size_t)1 << 48) return fail(TORUS_ERR_INVALID_ARG, "count overflow");
-  if (c->world == 1) {
-    if (dtype == wire) return TORUS_OK;  // sum/mean over one rank of wire values: identity
+  const int route = plan_route(c, count, dtype, wire);
+  if (route == kRouteNone) return TORUS_OK;  // sum/mean over one rank of wire values: identity
+  if (route == kRouteCast) {
     cudaError_t e = launch_castscale(bufs[0], count, dtype, wire, stream);
     return e == cudaSuccess ? TORUS_OK : cuda_fail(e, "castscale launch");
   }
   const unsigned long long R = round_elems(c, wire);
   const unsigned long long sw = wire_size(wire);
+  if (route == kRoutePull) {
+    int rc = switch_data_kernel(c, kDataPull, stream);
+    if (rc) return rc;
+    return launch_pull_rounds(c, bufs, count, dtype, wire, op, aligned, stream);
+  }
   LaunchArgs a;
   memset(&a, 0, sizeof a);
-  if (count * sw <= c->layout.ll_slot / 2 && count <= R) {
-    // small message: one-shot broadcast + local fold in the torus order (NEXT-2)
-    a.ranks = c->d_ranks;
-    for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];
-    a.nlocal = c->nlocal;
-    a.q = (int)(kVecBytes / sw);
-    a.op = op;
-    a.inv_n = 1.0f / (float)(c->X * c->Y);
-    a.aligned = aligned ? 1 : 0;
-    a.timeout_ns = c->timeout_ns;
+  a.ranks = c->d_ranks;
+  for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];
+  a.nlocal = c->nlocal;
+  a.q = (int)(kVecBytes / sw);
+  a.op = op;
+  a.inv_n = 1.0f / (float)(c->X * c->Y);
+  a.aligned = aligned ? 1 : 0;
+  a.timeout_ns = c->timeout_ns;
+  if (route == kRouteLL || route == kRouteLL2) {
+    // small message: one-shot broadcast + local fold in the torus order, or mid-size:
+    // two-shot LL (scatter to the torus owners, fold, broadcast back) -- NEXT-2
     a.n = count;
     a.buf_off = 0;
     a.ll_off = c->layout.ll_off;
-    a.ll_slot = c->layout.ll_slot;
+    a.ll_slot = route == kRouteLL ? c->layout.ll_slot : ll2_slot(c, count, sw);
     a.ll_half = c->layout.ll_region / 2;
-    a.ll_two_shot = 0;
+    a.ll_two_shot = route == kRouteLL2 ? 1 : 0;
     const unsigned long long nvec = (count * sw + kVecBytes - 1) / kVecBytes;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -637,50 +891,15 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
     const int cap = std::max(1, (int)env_size("TORUS_LL_CTAS", 2 * sms) / c->nlocal);
     a.G = (int)std::min<unsigned long long>(cap, (nvec + kLLThreadsHost - 1) / kLLThreadsHost);
     cudaError_t e = launch_ll(a, dtype, wire, c->virt, stream);
-    return e == cudaSuccess ? TORUS_OK : cuda_fail(e, "one-shot kernel launch");
+    return e == cudaSuccess ? TORUS_OK : cuda_fail(e, route == kRouteLL ? "one-shot kernel launch"
+                                                                         : "two-shot kernel launch");
   }
-  if (c->world >= 3 && c->layout.ll_region && count * sw <= c->ll2_max && count <= R) {
-    // mid-size message: two-shot LL (scatter to the torus owners, fold, broadcast back)
-    const int q = (int)(kVecBytes / sw);
-    unsigned long long o, l0, s0;
-    qpart(count, c->X, q, 0, &o, &l0);
-    qpart(l0, c->Y, q, 0, &o, &s0);
-    const unsigned long long slot = 2 * ((s0 * sw + kVecBytes - 1) / kVecBytes) * kVecBytes;
-    if (2ull * c->world * slot <= c->layout.ll_region / 2) {
-      a.ranks = c->d_ranks;
-      for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];
-      a.nlocal = c->nlocal;
-      a.q = q;
-      a.op = op;
-      a.inv_n = 1.0f / (float)(c->X * c->Y);
-      a.aligned = aligned ? 1 : 0;
-      a.timeout_ns = c->timeout_ns;
-      a.n = count;
-      a.buf_off = 0;
-      a.ll_off = c->layout.ll_off;
-      a.ll_slot = slot;
-      a.ll_half = c->layout.ll_region / 2;
-      a.ll_two_shot = 1;
-      const unsigned long long nvec = (count * sw + kVecBytes - 1) / kVecBytes;
-      int sms = 148;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-      const int cap = std::max(1, (int)env_size("TORUS_LL_CTAS", 2 * sms) / c->nlocal);
-      a.G = (int)std::min<unsigned long long>(cap, (nvec + kLLThreadsHost - 1) / kLLThreadsHost);
-      cudaError_t e = launch_ll(a, dtype, wire, c->virt, stream);
-      return e == cudaSuccess ? TORUS_OK : cuda_fail(e, "two-shot kernel launch");
-    }
-  }
-  a.ranks = c->d_ranks;
-  for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];
-  a.nlocal = c->nlocal;
+  // the round-1 push kernel (TORUS_KERNEL=push / tma, or grids the pull kernel does not take)
+  int rc = switch_data_kernel(c, kDataPush, stream);
+  if (rc) return rc;
   a.G = c->G;
-  a.q = (int)(kVecBytes / sw);
-  a.op = op;
-  a.inv_n = 1.0f / (float)(c->X * c->Y);
-  a.aligned = aligned ? 1 : 0;
-  a.timeout_ns = c->timeout_ns;
-  a.fence_early = (int)env_size("TORUS_FENCE_EARLY", 0);
-  a.poll_sleep = (unsigned)env_size("TORUS_POLL_SLEEP", 64);
+  a.fence_early = c->fence_early;
+  a.poll_sleep = c->poll_sleep;
   a.tile_vecs = c->tile_vecs;
   if (a.tile_vecs <= 0) {
     // auto: about kAutoTiles tiles per CTA slice of the largest sub-chunk (measured best
@@ -691,12 +910,10 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
     qpart(l0, c->Y, (int)(kVecBytes / sw), 0, &o, &s0);
     const unsigned long long nv = (s0 * sw + kVecBytes - 1) / kVecBytes;
     const unsigned long long slice = (nv + c->G - 1) / c->G;
-    // up to kOneTile vectors per CTA slice the call is one tile (stage distance 1): five
-    // latency-bound iterations beat ~11 pipelined ones (measured, r01_single_tile_sizes)
-    const unsigned long long one_tile = env_size("TORUS_ONE_TILE_MAX", 4096);
-    const unsigned long long mid = std::max<size_t>(1, env_size("TORUS_MID_TILES", 1));
-    if (slice <= one_tile) {
-      a.tile_vecs = (int)std::max<unsigned long long>(1, (slice + mid - 1) / mid);
+    // up to one_tile_max vectors per CTA slice the call is one tile (stage distance 1):
+    // five latency-bound iterations beat ~11 pipelined ones (measured, r01_single_tile_sizes)
+    if (slice <= c->one_tile_max) {
+      a.tile_vecs = (int)std::max<unsigned long long>(1, (slice + c->mid_tiles - 1) / c->mid_tiles);
       a.sd1 = 1;
     } else {
       a.tile_vecs = (int)std::max<unsigned long long>(256, (slice + kAutoTiles - 1) / kAutoTiles);
@@ -810,6 +1027,8 @@ int baseline_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, int
   } else {
     a.hin_stride = (R / (unsigned long long)c->world) * sw;  // one ring chunk slot
   }
+  int rc = switch_data_kernel(c, hier ? kDataHier : kDataRing, stream);
+  if (rc) return rc;
   for (unsigned long long r0 = 0; r0 < count; r0 += R) {
     a.n = std::min<unsigned long long>(R, count - r0);
     a.buf_off = r0;
@@ -986,6 +1205,33 @@ int torus_nvls_allreduce(torus_comm_t c, void* buf, size_t count, torus_dtype_t 
     if (e != cudaSuccess) return cuda_fail(e, "nvls kernel launch");
   }
   return TORUS_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+const char* torus_comm_route(torus_comm_t c, size_t count, torus_dtype_t dtype, torus_dtype_t wire) {
+  if (!c || !valid_pair(dtype, wire)) return "invalid";
+  return route_name(plan_route(c, count, dtype, wire));
+}
+
+int torus_comm_config(torus_comm_t c, unsigned long long* words, int n) {
+  if (!c || !words || n < 1) return -fail(TORUS_ERR_INVALID_ARG, "config args");
+  // Everything that decides which bytes and flags a call touches on a PEER: the grid,
+  // the slab layout, the routing thresholds and every tiling knob of every kernel.
+  int tv16 = 0, ns16 = 0, tv32 = 0, ns32 = 0;
+  pull_ring(c, 1, &tv16, &ns16);
+  pull_ring(c, 2, &tv32, &ns32);
+  const unsigned long long v[] = {
+      (unsigned long long)c->world, (unsigned long long)c->X, (unsigned long long)c->Y,
+      (unsigned long long)c->G, c->slab_size, c->layout.data_off, c->layout.ll_off,
+      c->layout.ll_slot, c->layout.ll_region, c->layout.pull_flag_off, c->ll2_max,
+      (unsigned long long)c->mode, (unsigned long long)c->tile_vecs, c->one_tile_max, c->mid_tiles,
+      (unsigned long long)tv16, (unsigned long long)tv32, c->timeout_ns};
+  const int m = (int)(sizeof v / sizeof v[0]);
+  for (int i = 0; i < n; ++i) words[i] = i < m ? v[i] : 0;
+  return m;
 }
 
 }  // extern "C"

@@ -38,12 +38,14 @@ enum FlagKind : int {
 //        chunk[Lc]     MY chunk, complete after phase 2 (pulled by row peers in phase 3)
 //   [ll_off, +2*N*ll_slot)    small-message one-shot region (ll_kernel): [parity][src]
 //                             slots of ll_slot bytes (0 when the LL path is disabled)
+//   [pull_flag_off, data_off) pull-kernel per-tile flags (torus_pull.cu)
 struct SlabLayout {
   size_t flags_bytes;
   size_t bar_off;
   size_t ll_off;
   size_t ll_slot;
   size_t ll_region;   // bytes of the LL region (two parity halves)
+  size_t pull_flag_off;  // pull-kernel flag region (torus_pull.cu), up to kPullFlagBytes
   size_t data_off;
   size_t size;
 };
@@ -58,6 +60,7 @@ struct RankDev {
   uint32_t* bar_epoch;           // [1] barrier counter
   int* err;                      // host-mapped async error word
   uint32_t* ll_ctr;              // [2] one-shot kernel: epoch, CTAs done in the current call
+  uint32_t* pull_ctr;            // [2] pull kernel: call epoch, CTAs done in the current call
 };
 
 // Per-launch (per-round) arguments, passed by value.
@@ -94,6 +97,35 @@ struct LaunchArgs {
   unsigned poll_sleep;           // default kernel: ns of back-off between flag polls
   int sd1;                       // default kernel: stage distance 1 even with T > 1
 };
+
+// Per-launch arguments of the pull (dataflow) kernel, torus_pull.cu.  Everything that
+// decides WHICH bytes and flags a tile touches (n, q, TV, Kmax, region and flag offsets)
+// must be equal on every rank; the CTA split g[] and the ring (nslots, slot_bytes) are
+// rank-local choices.
+struct PullArgs {
+  const RankDev* ranks;          // device array [nlocal]
+  void* buf[kMaxLocal];          // user buffer of each local rank
+  unsigned long long n;          // elements in this round
+  unsigned long long buf_off;    // element offset of the round inside the user buffers
+  unsigned long long win_off[2], p1_off[2], chunk_off[2];  // slab byte offsets by parity
+  unsigned long long flag_off;   // slab byte offset of the pull flag region
+  unsigned long long fl_win, fl_p1, fl_v, fl_c, fl_pres;   // word offsets of the flag kinds
+  unsigned long long timeout_ns;
+  int nlocal;
+  int q;                         // partition quantum (elements) = one 16-byte wire vector
+  int TV;                        // 16-byte wire vectors per tile
+  int Kmax;                      // tiles of the largest sub-chunk
+  int op;                        // 0 sum, 1 mean
+  float inv_n;                   // f32(1/N)
+  int aligned;                   // all user buffers 16-byte aligned
+  int g[5];                      // CTAs per rank of each kind: S0, R, VR, VA, H
+  int gsum;
+  int nslots, slot_bytes;        // shared-memory ring
+};
+inline size_t pull_smem_bytes(int nslots, int slot_bytes) {
+  return (size_t)nslots * slot_bytes + 2 * (size_t)nslots * 8;
+}
+constexpr size_t kPullFlagBytes = 8ull << 20;  // pull flag region per slab
 
 // TMA kernel shared memory: nbufs ring buffers of one piece each (tile_vecs 16-byte wire
 // vectors, or the same elements in the user dtype: `ratio` = sizeof(dtype)/sizeof(wire),
@@ -180,6 +212,8 @@ int torus_kernel_max_ctas_per_sm(int dtype, int wire);
 cudaError_t launch_ring(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
 cudaError_t launch_hier(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
 cudaError_t launch_ll(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
+cudaError_t launch_pull(const PullArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
+int pull_ctas_per_sm(size_t smem);
 cudaError_t launch_multi_copy(const MultiTable& tab, int n, int dtype, int wire, void* staging,
                               bool pack, cudaStream_t stream);
 cudaError_t launch_probe(const RankDev* ranks, unsigned long long data_off, unsigned long long bytes,

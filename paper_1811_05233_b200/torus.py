@@ -109,6 +109,19 @@ class _CommBase:
         return _lib.load().torus_comm_launches(self._comm, count, _dtype_code(dtype),
                                                _dtype_code(wire or dtype))
 
+    def route(self, count: int, dtype: torch.dtype, wire: torch.dtype | None = None) -> str:
+        """Kernel a call with these arguments runs (torus_comm_route)."""
+        return _lib.load().torus_comm_route(self._comm, count, _dtype_code(dtype),
+                                            _dtype_code(wire or dtype)).decode()
+
+    def config(self) -> tuple[int, ...]:
+        """Configuration fingerprint that must agree across ranks (torus_comm_config)."""
+        words = (ctypes.c_ulonglong * 32)()
+        n = _lib.load().torus_comm_config(self._comm, words, 32)
+        if n < 0:
+            check(-n, "torus_comm_config")
+        return tuple(int(w) for w in words[:n])
+
     def ll_max_bytes(self) -> int:
         """Small-message threshold in wire bytes (torus_comm_ll_max_bytes; 0 = off)."""
         return int(_lib.load().torus_comm_ll_max_bytes(self._comm))
