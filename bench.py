@@ -56,6 +56,8 @@ def parse():
                    help="ring / hier = baseline kernels; nvls = in-switch-reduction variant")
     p.add_argument("--no-nccl", action="store_true", help="skip the NCCL comparison")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-register", action="store_true",
+                   help="do not register the buffer (the pull kernel then copies inputs into the slab)")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
     p.add_argument("--out", default=None, help="also append the JSON line to this file")
     return p.parse_args()
@@ -234,6 +236,8 @@ def run_torus(args):
     host = make_input(args, rank, dtype_s)
     x0 = to_tensor(host, dtype_s, dev)
     buf = x0.clone()
+    if world > 1 and not args.no_register:
+        comm.register(buf)  # zero-copy: peers read this buffer directly (torus_register_buffer)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     clean = torch.zeros(64 << 20, dtype=torch.int32, device=dev)  # 256 MiB, read only
@@ -428,6 +432,8 @@ def run_torus(args):
                    "algo": args.algo,
                    "parallelism": (f"ring{world}" if args.algo == "ring" else f"{args.algo}{X}x{Y}"),
                    "ctas_per_rank": comm_ctas(),
+                   "buffer": ("registered (zero-copy)" if world > 1 and not args.no_register
+                              else "unregistered"),
                    "message_bytes": S, "l2": "flushed before every timed call (256 MiB write, then 256 MiB read so no dirty flush lines are written back inside the timed call)",
                    "value_is": "busbw" if world > 1 else "algbw (busbw is 0 at N=1)"},
         "algbw": algbw, "busbw": busbw, "us_per_call": t * 1e6, "us_per_call_min": t_min * 1e6,

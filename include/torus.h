@@ -98,6 +98,23 @@ TORUS_API int torus_comm_destroy(torus_comm_t comm);
  * drains this rank's own work, frees its resources, no barrier.  NULL is a no-op. */
 TORUS_API int torus_comm_abort(torus_comm_t comm);
 
+/* Buffer registration (zero-copy): a collective promise that `ptr` (a device buffer of
+ * `bytes` bytes on the comm's device) is the buffer every rank passes to later calls.
+ * Step 1, local: torus_buffer_export(ptr, bytes, &h) -> h = the IPC handle of the
+ * allocation containing ptr + ptr's offset in it.  Step 2: all-gather h over the ranks
+ * (host side, e.g. torch.distributed).  Step 3: torus_register_buffer(comm, ptr, bytes,
+ * handles[world]) maps every peer's buffer.  Afterwards calls whose buf == ptr (and
+ * dtype == wire) let the pull kernel read the row peers' inputs straight from their
+ * buffers (TMA over NVLink): no pre-pass copy into the slab (SURVEY 8(d) HBM table).
+ * Ownership: the caller keeps ptr allocated until torus_deregister_buffer (peer mappings
+ * are closed at destroy).  Errors: MISMATCH if sizes differ across ranks, PEER if a
+ * mapping fails.  Every rank must register / deregister the same buffers in the same
+ * order, and call with the registered buffer on every rank or on none. */
+TORUS_API int torus_buffer_export(const void* ptr, size_t bytes, torus_ipc_handle_t* out);
+TORUS_API int torus_register_buffer(torus_comm_t comm, void* ptr, size_t bytes,
+                                    const torus_ipc_handle_t* handles /*[world]*/);
+TORUS_API int torus_deregister_buffer(torus_comm_t comm, void* ptr);
+
 /* Configuration fingerprint: writes up to n words that must be EQUAL on every
  * rank for the flag protocol to line up -- grid, CTA count, slab layout, routing
  * thresholds, kernel choice and tiling knobs (all read from the environment once, at
@@ -262,6 +279,15 @@ TORUS_API int torus_partition(unsigned long long n, int parts, int q, unsigned l
  * 5 worker READY passed, 6 worker data done).  Synchronizes the device.  UNSUPPORTED if
  * tracing is off. */
 TORUS_API int torus_comm_trace(torus_comm_t comm, unsigned long long* host, size_t bytes);
+
+/* Device trace of the last pull-kernel launch (TORUS_TRACE=1 at init): host array
+ * [ctas][64][4] u64 globaltimer stamps, CTAs of all local ranks in launch order; per job
+ * n < 63 of each CTA: 0 producer saw the inputs' flags, 1 operands landed in shared
+ * memory, 2 consumers done, 3 flags raised; [63][0..1] = CTA start / end.  Also writes
+ * the CTAs per rank and the split over the five CTA kinds (S0, R, VR, VA, H).
+ * Synchronizes the device. */
+TORUS_API int torus_comm_pull_trace(torus_comm_t comm, unsigned long long* host, size_t bytes,
+                                    int* ctas_per_rank, int* kinds /*[5]*/);
 
 /* Calibration probes (not part of the all-reduce; SURVEY.md 8(d) "Calibration"), enqueued
  * on `stream` with `ctas` CTAs (0 = the comm's count).  mode 0: push `bytes` split over

@@ -10,7 +10,7 @@ PKG = pathlib.Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 SOURCES = [CSRC / "torus_abi.cu", CSRC / "torus_kernels.cu", CSRC / "torus_pull.cu",
-           CSRC / "torus_nvls.cu"]
+           CSRC / "torus_baselines.cu", CSRC / "torus_ll.cu", CSRC / "torus_nvls.cu"]
 HEADERS = [CSRC / "torus_internal.h", CSRC / "torus_device.cuh", ROOT / "include" / "torus.h"]
 LIB = PKG / "libtorus.so"
 
@@ -34,38 +34,49 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False, out: pathlib.Path | None = None,
           defines: tuple[str, ...] = ()) -> pathlib.Path:
+    """Compile each translation unit to an object (in parallel; objects are cached under
+    build/ and reused while neither the source nor a header changed), then link."""
     lib = out or LIB
-    if force or out is not None or stale():
-        # one nvcc per translation unit, in parallel, then one link
-        tmp = lib.with_name(f"{lib.name}.tmp{os.getpid()}")
-        objs = [tmp.with_name(f"{p.stem}.{os.getpid()}.o") for p in SOURCES]
-        compile_flags = [f for f in FLAGS if f not in ("-shared", "-cudart", "static")]
-        procs = [subprocess.Popen([NVCC, *compile_flags, *[f"-D{d}" for d in defines], "-c", str(src),
-                                   "-o", str(o)], stdout=subprocess.PIPE, stderr=subprocess.PIPE,
-                                  text=True) for src, o in zip(SOURCES, objs)]
-        logs = []
-        failed = None
-        for p in procs:
-            out_s, err_s = p.communicate()
-            logs.append(err_s)
-            if p.returncode != 0:
-                failed = (p.returncode, err_s)
-        if failed is None:
-            res = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-                                  "-cudart", "static", *map(str, objs), "-o", str(tmp)],
-                                 capture_output=True, text=True)
-            if res.returncode != 0:
-                failed = (res.returncode, res.stderr)
-        for o in objs:
-            if o.exists():
-                o.unlink()
-        if failed is not None:
-            raise RuntimeError(f"nvcc failed ({failed[0]}):\n{failed[1][-4000:]}")
-        log = "\n".join(logs)
-        (PKG / "build_ptxas.log").write_text(log)
-        if verbose:
-            print(log)
-        os.replace(tmp, lib)
+    if not (force or out is not None or stale()):
+        return lib
+    odir = PKG / "build" / ("default" if not defines else "_".join(defines).replace("=", "-"))
+    odir.mkdir(parents=True, exist_ok=True)
+    hdr_t = max(p.stat().st_mtime for p in HEADERS)
+    compile_flags = [f for f in FLAGS if f not in ("-shared", "-cudart", "static")]
+    objs, procs = [], []
+    for src in SOURCES:
+        o = odir / f"{src.stem}.o"
+        objs.append(o)
+        if not force and o.exists() and o.stat().st_mtime > max(src.stat().st_mtime, hdr_t):
+            continue
+        tmp_o = o.with_name(f"{o.name}.tmp{os.getpid()}")
+        procs.append((src, tmp_o, o, subprocess.Popen(
+            [NVCC, *compile_flags, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(tmp_o)],
+            stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    failed = None
+    for src, tmp_o, o, p in procs:
+        _, err_s = p.communicate()
+        (odir / f"{src.stem}.ptxas.log").write_text(err_s)
+        if p.returncode != 0:
+            failed = (p.returncode, err_s)
+            if tmp_o.exists():
+                tmp_o.unlink()
+        else:
+            os.replace(tmp_o, o)
+    if failed is not None:
+        raise RuntimeError(f"nvcc failed ({failed[0]}):\n{failed[1][-4000:]}")
+    tmp = lib.with_name(f"{lib.name}.tmp{os.getpid()}")
+    res = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+                          "-cudart", "static", *map(str, objs), "-o", str(tmp)],
+                         capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc link failed ({res.returncode}):\n{res.stderr[-4000:]}")
+    log = "\n".join((odir / f"{s.stem}.ptxas.log").read_text() for s in SOURCES
+                     if (odir / f"{s.stem}.ptxas.log").exists())
+    (PKG / "build_ptxas.log").write_text(log)
+    if verbose:
+        print(log)
+    os.replace(tmp, lib)
     return lib
 
 

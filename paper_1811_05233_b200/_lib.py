@@ -35,6 +35,9 @@ PROTOTYPES = {
     "torus_vcomm_init": (_i, [_i, _i, _i, _i, _sz, _c.POINTER(_vp)]),
     "torus_comm_destroy": (_i, [_vp]),
     "torus_comm_abort": (_i, [_vp]),
+    "torus_buffer_export": (_i, [_vp, _sz, _c.POINTER(torus_ipc_handle_t)]),
+    "torus_register_buffer": (_i, [_vp, _vp, _sz, _c.POINTER(torus_ipc_handle_t)]),
+    "torus_deregister_buffer": (_i, [_vp, _vp]),
     "torus_comm_config": (_i, [_vp, _c.POINTER(_ull), _i]),
     "torus_comm_route": (_c.c_char_p, [_vp, _sz, _i, _i]),
     "torus_allreduce": (_i, [_vp, _vp, _sz, _i, _i, _vp]),
@@ -61,6 +64,7 @@ PROTOTYPES = {
     "torus_comm_ll_max_bytes": (_sz, [_vp]),
     "torus_comm_ll2_max_bytes": (_sz, [_vp]),
     "torus_comm_trace": (_i, [_vp, _c.POINTER(_ull), _sz]),
+    "torus_comm_pull_trace": (_i, [_vp, _c.POINTER(_ull), _sz, _c.POINTER(_i), _c.POINTER(_i)]),
     "torus_probe": (_i, [_vp, _i, _sz, _i, _i, _c.POINTER(_ull), _vp]),
     "torus_pick_grid": (_i, [_i, _c.POINTER(_i), _c.POINTER(_i), _c.POINTER(_i)]),
     "torus_partition": (_i, [_ull, _i, _i, _c.POINTER(_ull), _c.POINTER(_ull)]),

@@ -50,7 +50,9 @@ size_t env_size(const char* name, size_t dflt) {
   return (size_t)strtoull(v, nullptr, 10);
 }
 
-constexpr size_t kDefaultSlab = 320ull << 20;
+constexpr size_t kDefaultSlab = 512ull << 20;   // real ranks (f32 51M-element rounds fit)
+constexpr size_t kDefaultVirtualSlab = 320ull << 20;  // per virtual rank (N slabs on one GPU)
+constexpr size_t kPullTraceBytes = (size_t)kMaxLocal * 512 * kPullTraceJobs * 4 * 8;
 constexpr int kLLThreadsHost = 256;  // ll_kernel block size (torus_kernels.cu)
 
 struct Slab {
@@ -107,9 +109,21 @@ struct torus_comm {
   int pull_tv = 0;                        // pull kernel: vectors per tile (0 = auto)
   int pull_slots = 0;                     // pull kernel: shared-memory ring slots (0 = auto)
   int pull_ctas = 0;                      // pull kernel: CTA budget per rank (0 = all resident)
+  int pull_fence = 0;                     // pull kernel publish fence (see PullArgs::fence)
+  int pull_zc = 1;                        // pull kernel: zero-copy from registered buffers
+  struct Reg {                            // a registered user buffer (torus_register_buffer)
+    char* ptr;
+    size_t bytes;
+    bool aligned;                         // 16-byte aligned on every rank
+    std::vector<char*> peer;              // every rank's buffer, mapped here
+  };
+  std::vector<Reg> regs;
+  std::vector<std::pair<std::string, void*>> ipc_opened;  // IPC handle -> mapped base
   float pull_w[5] = {0.5f, 1.f, 1.f, 1.f, 1.f};  // pull kernel: CTA weight per kind
   uint32_t* d_pull_ctr = nullptr;         // [nlocal][2] pull call epochs
+  unsigned long long* d_pull_trace = nullptr;  // TORUS_TRACE=1: pull kernel stamps
   int last_data_kernel = 0;               // kernel that last used the shared data region
+  int last_pull_gsum = 0, last_pull_g[5] = {0, 0, 0, 0, 0};  // CTA split of the last pull launch
   int ctas_req = 0;                       // CTA count requested at init (0 = auto)
 };
 
@@ -241,6 +255,8 @@ int alloc_comm_common(torus_comm* c) {
     const size_t tb = (size_t)c->G * kTraceIters * kTraceEvents * sizeof(unsigned long long);
     CU(cudaMalloc(&c->d_trace, tb));
     CU(cudaMemset(c->d_trace, 0, tb));
+    CU(cudaMalloc(&c->d_pull_trace, kPullTraceBytes));
+    CU(cudaMemset(c->d_pull_trace, 0, kPullTraceBytes));
   }
   return TORUS_OK;
 }
@@ -301,6 +317,8 @@ void read_knobs(torus_comm* c) {
   c->pull_tv = (int)env_size("TORUS_PULL_TILE", 0);
   c->pull_slots = (int)env_size("TORUS_PULL_SLOTS", 0);
   c->pull_ctas = (int)env_size("TORUS_PULL_CTAS", 0);
+  c->pull_fence = (int)env_size("TORUS_PULL_FENCE", 0);
+  c->pull_zc = (int)env_size("TORUS_PULL_ZC", 1);
   if (const char* w = getenv("TORUS_PULL_W"))
     sscanf(w, "%f,%f,%f,%f,%f", &c->pull_w[0], &c->pull_w[1], &c->pull_w[2], &c->pull_w[3], &c->pull_w[4]);
   c->ll2_max = ll2_max_env(c->world);
@@ -309,10 +327,12 @@ void read_knobs(torus_comm* c) {
 void destroy_resources(torus_comm* c) {
   nvls_release(&c->nvls);
   for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  for (auto& h : c->ipc_opened) cudaIpcCloseMemHandle(h.second);
   for (void* p : c->own_slabs) cudaFree(p);
   if (c->d_ranks) cudaFree(c->d_ranks);
   if (c->d_epochs) cudaFree(c->d_epochs);
   if (c->d_trace) cudaFree(c->d_trace);
+  if (c->d_pull_trace) cudaFree(c->d_pull_trace);
   if (c->d_done_local) cudaFree(c->d_done_local);
   if (c->d_sig_ack) cudaFree(c->d_sig_ack);
   if (c->d_staging) cudaFree(c->d_staging);
@@ -522,7 +542,7 @@ int torus_vcomm_init(int device, int X, int Y, int ctas, size_t ws_bytes, torus_
   c->nlocal = X * Y;
   c->device = device;
   for (int r = 0; r < c->world; ++r) c->local_ranks.push_back(r);
-  if (ws_bytes == 0) ws_bytes = env_size("TORUS_WS_BYTES", kDefaultSlab);
+  if (ws_bytes == 0) ws_bytes = env_size("TORUS_WS_BYTES", kDefaultVirtualSlab);
   c->slab_size = (ws_bytes + 65535) & ~(size_t)65535;
   read_knobs(c);
   c->ctas_req = ctas;
@@ -605,6 +625,18 @@ int torus_comm_rank(torus_comm_t c, int* rank, int* world) {
 }
 
 int torus_comm_ctas(torus_comm_t c) { return c ? c->G : -1; }
+
+int torus_comm_pull_trace(torus_comm_t c, unsigned long long* host, size_t bytes, int* ctas_per_rank,
+                          int* kinds /*[5]*/) {
+  if (!c || !host) return fail(TORUS_ERR_INVALID_ARG, "null argument");
+  if (!c->d_pull_trace) return fail(TORUS_ERR_UNSUPPORTED, "tracing is off (set TORUS_TRACE=1 before init)");
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(host, c->d_pull_trace, std::min(bytes, kPullTraceBytes), cudaMemcpyDeviceToHost));
+  if (ctas_per_rank) *ctas_per_rank = c->last_pull_gsum;
+  if (kinds)
+    for (int k = 0; k < 5; ++k) kinds[k] = c->last_pull_g[k];
+  return TORUS_OK;
+}
 
 int torus_comm_trace(torus_comm_t c, unsigned long long* host, size_t bytes) {
   if (!c || !host) return fail(TORUS_ERR_INVALID_ARG, "null argument");
@@ -744,6 +776,25 @@ int switch_data_kernel(torus_comm* c, int kind, cudaStream_t stream) {
   return TORUS_OK;
 }
 
+// Zero-copy source table for a call: the peers' user buffers when the call's buffer is a
+// registered one (every rank calls with its registered buffer: same decision everywhere),
+// or -- virtual ranks -- the local buffers themselves.
+bool pull_zero_copy(const torus_comm* c, void* const* bufs, size_t bytes, int dtype, int wire, bool aligned,
+                    char** peer) {
+  if (!c->pull_zc || dtype != wire) return false;
+  if (c->virt) {
+    if (!aligned) return false;
+    for (int r = 0; r < c->world; ++r) peer[r] = static_cast<char*>(bufs[r]);
+    return true;
+  }
+  for (const auto& g : c->regs)
+    if (g.ptr == bufs[0] && bytes <= g.bytes && g.aligned) {
+      for (int r = 0; r < c->world; ++r) peer[r] = g.peer[r];
+      return true;
+    }
+  return false;
+}
+
 int launch_pull_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype, int wire, int op,
                        bool aligned, cudaStream_t stream) {
   const unsigned long long R = round_elems(c, wire), sw = wire_size(wire);
@@ -785,11 +836,12 @@ int launch_pull_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype
   int gtot = sms * cached_per_sm / c->nlocal;
   if (c->pull_ctas > 0) gtot = std::min(gtot, c->pull_ctas);
   const int X = c->X, Y = c->Y;
+  a.zc = pull_zero_copy(c, bufs, count * wire_size(dtype), dtype, wire, aligned, a.peer_buf) ? 1 : 0;
   const bool own_copy = !(dtype == wire && aligned);  // S0 also copies my own chunk
   double w[5] = {0, 0, 0, 0, 0};
   const double f0 = X > 1 ? (double)(X - 1) / X + (own_copy ? 1.0 / X : 0.0)
                           : (double)(Y - 1) / Y + (own_copy ? 1.0 / Y : 0.0);
-  w[0] = c->pull_w[0] * f0 * ratio;
+  w[0] = a.zc ? 0.02 : c->pull_w[0] * f0 * ratio;  // zero-copy: S0 only copies ragged tails
   if (X > 1) w[1] = c->pull_w[1] * (double)(X - 1) / X;
   if (Y > 1) w[2] = c->pull_w[2] * (double)(Y - 1) / Y / X;
   if (Y > 1) w[3] = c->pull_w[3] * (double)(Y - 1) / Y / X;
@@ -814,6 +866,8 @@ int launch_pull_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype
     --gs;
   }
   a.gsum = gs;
+  c->last_pull_gsum = gs;
+  for (int k = 0; k < 5; ++k) c->last_pull_g[k] = a.g[k];
   for (unsigned long long r0 = 0; r0 < count; r0 += R) {
     a.n = std::min<unsigned long long>(R, count - r0);
     a.buf_off = r0;
@@ -824,6 +878,8 @@ int launch_pull_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype
     a.fl_v = a.fl_p1 + (unsigned long long)Y * a.Kmax;
     a.fl_c = a.fl_v + (unsigned long long)Y * a.Kmax;
     a.fl_pres = a.fl_c + (unsigned long long)X * Y * a.Kmax;
+    a.trace = c->d_pull_trace;
+    a.fence = c->pull_fence;
     cudaError_t e = launch_pull(a, dtype, wire, c->virt, stream);
     if (e != cudaSuccess) return cuda_fail(e, "pull kernel launch");
   }
@@ -1232,6 +1288,103 @@ int torus_comm_config(torus_comm_t c, unsigned long long* words, int n) {
   const int m = (int)(sizeof v / sizeof v[0]);
   for (int i = 0; i < n; ++i) words[i] = i < m ? v[i] : 0;
   return m;
+}
+
+}  // extern "C"
+
+namespace {
+
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+// base and size of the allocation that contains p (driver API through the runtime's
+// entry-point query, so the library does not link libcuda)
+bool alloc_range(const void* p, char** base, size_t* size) {
+  static PFN_getAddressRange fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return false;
+    fn = reinterpret_cast<PFN_getAddressRange>(f);
+  }
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return false;
+  *base = reinterpret_cast<char*>(b);
+  *size = sz;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int torus_buffer_export(const void* ptr, size_t bytes, torus_ipc_handle_t* out) {
+  if (!ptr || !out || !bytes) return fail(TORUS_ERR_INVALID_ARG, "buffer_export args");
+  char* base = nullptr;
+  size_t size = 0;
+  if (!alloc_range(ptr, &base, &size)) return fail(TORUS_ERR_INVALID_ARG, "not a device allocation");
+  const size_t off = static_cast<const char*>(ptr) - base;
+  if (off + bytes > size) return fail(TORUS_ERR_INVALID_ARG, "buffer exceeds its allocation");
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, base));
+  memset(out, 0, sizeof *out);
+  memcpy(out->bytes, &h, 64);
+  out->offset = off;
+  out->size = bytes;
+  return TORUS_OK;
+}
+
+int torus_register_buffer(torus_comm_t c, void* ptr, size_t bytes, const torus_ipc_handle_t* handles) {
+  if (!c || !ptr || !handles || !bytes) return fail(TORUS_ERR_INVALID_ARG, "register args");
+  if (c->virt) return fail(TORUS_ERR_INVALID_ARG, "virtual comm: buffers are local already");
+  for (int r = 0; r < c->world; ++r)
+    if (handles[r].size != bytes) return fail(TORUS_ERR_MISMATCH, "registered sizes differ across ranks");
+  CU(cudaSetDevice(c->device));
+  torus_comm::Reg g;
+  g.ptr = static_cast<char*>(ptr);
+  g.bytes = bytes;
+  g.aligned = true;
+  g.peer.assign(c->world, nullptr);
+  for (int r = 0; r < c->world; ++r) {
+    if ((handles[r].offset & 15) != 0 || (r == c->rank && (reinterpret_cast<uintptr_t>(ptr) & 15) != 0))
+      g.aligned = false;  // every rank sees the same handles: the same decision everywhere
+    if (r == c->rank) {
+      g.peer[r] = g.ptr;
+      continue;
+    }
+    const std::string key(reinterpret_cast<const char*>(handles[r].bytes), 64);
+    void* base = nullptr;
+    for (auto& h : c->ipc_opened)
+      if (h.first == key) base = h.second;
+    if (!base) {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, handles[r].bytes, 64);
+      cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return fail(TORUS_ERR_PEER, "cudaIpcOpenMemHandle(buffer of rank %d): %s", r,
+                                        cudaGetErrorString(e));
+      c->ipc_opened.emplace_back(key, base);
+    }
+    g.peer[r] = static_cast<char*>(base) + handles[r].offset;
+  }
+  for (auto& old : c->regs)
+    if (old.ptr == g.ptr) {
+      old = g;
+      return TORUS_OK;
+    }
+  c->regs.push_back(g);
+  return TORUS_OK;
+}
+
+int torus_deregister_buffer(torus_comm_t c, void* ptr) {
+  if (!c) return fail(TORUS_ERR_INVALID_ARG, "comm is NULL");
+  for (size_t i = 0; i < c->regs.size(); ++i)
+    if (c->regs[i].ptr == ptr) {
+      c->regs.erase(c->regs.begin() + i);
+      return TORUS_OK;  // the peer mappings stay open until destroy (others may share them)
+    }
+  return fail(TORUS_ERR_INVALID_ARG, "buffer is not registered");
 }
 
 }  // extern "C"

@@ -121,7 +121,13 @@ struct PullArgs {
   int g[5];                      // CTAs per rank of each kind: S0, R, VR, VA, H
   int gsum;
   int nslots, slot_bytes;        // shared-memory ring
+  unsigned long long* trace;     // optional [nlocal*gsum][kPullTraceJobs][4] globaltimer stamps
+  int fence;                     // publish fence: 0 fence.acq_rel.sys, 1 .gpu, 2 none (measurement only)
+  int zc;                        // zero-copy: the peers' user buffers are mapped here (registered,
+                                 // dtype == wire, 16-byte aligned on every rank) -- no S0 copy
+  char* peer_buf[kMaxRanks];     // zc: every rank's user buffer as mapped in this process
 };
+constexpr int kPullTraceJobs = 64;  // trace: first 64 jobs of every CTA; slot 63 = CTA start/end
 inline size_t pull_smem_bytes(int nslots, int slot_bytes) {
   return (size_t)nslots * slot_bytes + 2 * (size_t)nslots * 8;
 }

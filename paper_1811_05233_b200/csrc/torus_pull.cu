@@ -74,13 +74,6 @@ __device__ __forceinline__ Tile tile_of(const PullArgs& a, int X, int Y, int j, 
   return t;
 }
 
-// the own operand of a reduce can be read straight from the user buffer (no S0 copy)
-// when the buffer holds wire values, is 16-byte aligned and the tile has no ragged tail
-template <int DT, int W>
-__device__ __forceinline__ bool own_from_buf(const PullArgs& a, const Tile& t) {
-  return DT == W && a.aligned && (t.nel % (unsigned long long)a.q) == 0;
-}
-
 // Flag word index inside the pull flag region (u32 epochs, value = call epoch + 1).
 //   WIN[src][s][k]  src's win tile (s, k) of my chunk is ready   (src = column j, or row i if X == 1)
 //   P1 [i][k]       row i's P1 tile k of my sub-chunk is ready    (column peers)
@@ -157,13 +150,6 @@ __device__ __forceinline__ Job job_of(const PullArgs& a, int kind, int J, int X,
   }
   jb.t = tile_of(a, X, Y, jb.j, jb.s, jb.k);
   jb.ok = jb.t.ok;
-  if (jb.ok && kind == kS0) {
-    // S0 copies what a peer reads in the first reduce phase: the chunks of my row peers
-    // (X > 1) or the sub-chunks of my column peers (X == 1), plus my own tiles the
-    // reduce cannot take from the user buffer directly
-    const bool own = X > 1 ? (jb.j == c) : (jb.s == rho);
-    if (own && own_from_buf<DT, W>(a, jb.t)) jb.ok = false;
-  }
   return jb;
 }
 
@@ -194,16 +180,73 @@ __device__ __forceinline__ bool mbar_wait_abortable(uint64_t* bar, uint32_t phas
 __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// generic-proxy shared-memory writes -> visible to a later async-proxy (TMA) read
+__device__ __forceinline__ void fence_view_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void consumer_bar() {  // named barrier 1 over the consumer warps
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+}
+
+__device__ __forceinline__ bool ragged(const PullArgs& a, const Tile& t) {
+  return (t.nel % (unsigned long long)a.q) != 0;
+}
+
+// Where a reduce reads the first-phase input tile of rank `src`: its user buffer (own
+// buffer, or a peer's registered buffer in zero-copy mode) or its slab's `win` copy.
+template <int DT, int W>
+__device__ __forceinline__ bool input_from_buf(const PullArgs& a, const Tile& t, bool own) {
+  if (ragged(a, t)) return false;  // a TMA read of the last partial vector would overrun
+  return own ? (DT == W && a.aligned) : (a.zc != 0);
+}
+
+// the final values of a tile go to the user buffer by a TMA bulk store when they are
+// wire-typed, aligned and whole vectors; otherwise the consumers store them (cast fused)
+template <int DT, int W>
+__device__ __forceinline__ bool buf_bulk(const PullArgs& a, const Tile& t) {
+  return DT == W && a.aligned && !ragged(a, t);
+}
+
+// S0 jobs: copy the tiles some reduce reads from `win` (see input_from_buf)
+template <int DT, int W>
+__device__ __forceinline__ Job job_of_checked(const PullArgs& a, int kind, int J, int X, int Y, int rho, int c) {
+  Job jb = job_of<DT, W>(a, kind, J, X, Y, rho, c);
+  if (jb.ok && kind == kS0) {
+    const bool own = X > 1 ? (jb.j == c) : (jb.s == rho);
+    if (input_from_buf<DT, W>(a, jb.t, own)) jb.ok = false;
+  }
+  return jb;
+}
+
+// Trace (TORUS_TRACE=1): per CTA, per job n < 63 four globaltimer stamps -- 0 producer saw
+// the inputs' flags, 1 consumers saw the operands land, 2 consumers done, 3 signaler
+// raised the flags; slot 63 holds the CTA's start and end.
+__device__ __forceinline__ void pstamp(const PullArgs& a, int cta, int n, int ev) {
+  if (a.trace && n < kPullTraceJobs - 1 && cta < kMaxLocal * 512)
+    a.trace[((size_t)cta * kPullTraceJobs + n) * 4 + ev] = gtimer();
+}
 
 // ------------------------------------------------------------------------------------
 // the kernel
 // ------------------------------------------------------------------------------------
+//   warp 0 (lane 0)  producer: per job, wait for the input tiles' flags, then TMA-load the
+//                    operands (fold order) into consecutive ring slots
+//   warps 2..5       consumers: fold the operands (f32 / u32) into slot 0 of the job in
+//                    shared memory, or cast (S0); ILP: each thread holds 4 vectors
+//   warp 1 (lane 0)  storer + signaler: TMA bulk-stores every finished job's result from
+//                    shared memory to its LOCAL destinations (win / P1 / chunk / user
+//                    buffer), frees the slots once read, waits for the writes, then ONE
+//                    fence publishes all jobs stored so far and their flags are raised.
+// No generic global store sits on the hot path (consumers store only for a cast or a
+// ragged/unaligned user buffer), so the publishing fence is not stuck behind a backlog
+// of st.global.
 template <int DT, int W>
 __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs a) {
   using Acc = typename Wire<W>::Acc;
   constexpr int VE = Wire<W>::VE;
   constexpr int SW = kVecBytes / VE;           // bytes per wire element
   constexpr int DB = sizeof(typename Elem<DT>::T);
+  constexpr int U = 4;                         // vectors in flight per consumer thread
 
   // ---- which rank, which kind, which CTA of the kind ----
   const int lr = blockIdx.x / a.gsum;
@@ -221,7 +264,7 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
   uint64_t* empty = full + NS;
   __shared__ uint32_t s_epoch;
   __shared__ int s_abort;
-  __shared__ int s_done;      // consumer-warp job completions (signaler polls)
+  __shared__ int s_done;      // consumer-warp job completions (storer polls)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -230,11 +273,13 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
     s_done = 0;
     for (int i = 0; i < NS; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kConsumerWarps);
+      mbar_init(&empty[i], 1);
     }
     fence_mbar_init();
   }
   __syncthreads();
+  if (tid == 0 && a.trace && blockIdx.x < kMaxLocal * 512)
+    a.trace[((size_t)blockIdx.x * kPullTraceJobs + kPullTraceJobs - 1) * 4] = gtimer();
   const uint32_t epoch = s_epoch;
   const uint32_t v = epoch + 1u;               // flag value of this call
   const int par = (int)(epoch & 1u);
@@ -242,6 +287,10 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
   uint32_t* const myflags = reinterpret_cast<uint32_t*>(myws + a.flag_off);
   auto flag_at = [&](int rank, size_t idx) -> uint32_t* {
     return reinterpret_cast<uint32_t*>(R->ws[rank] + a.flag_off) + idx;
+  };
+  auto bufp = [&](int rank, const Tile& t) -> char* {  // a rank's user buffer at a tile
+    char* base = (rank == me) ? reinterpret_cast<char*>(buf) : a.peer_buf[rank];
+    return base + (a.buf_off + t.co + t.e0) * DB;
   };
   const int njobs = job_count(a, kind, X, Y);
   const int nops = job_nops(kind, X, Y);
@@ -251,79 +300,76 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
     if (lane == 0) {
       const unsigned long long deadline = gtimer() + a.timeout_ns;
       // Presence: CTA 0 of S0 tells every row and column peer that this rank has entered
-      // the call, and does not finish before all of them have -- so every call observes
-      // every peer, which the parity double-buffering relies on even when a short round
-      // leaves some sub-chunks (and their flags) empty.
+      // the call (so its user buffer holds this call's input), and does not finish before
+      // all of them have -- so every call observes every peer, which the parity double-
+      // buffering relies on even when a short round leaves some tiles (and flags) empty.
       const bool presence = (kind == kS0 && b == 0);
       if (presence) {
         for (int jj = 1; jj < X; ++jj) st_relaxed_sys(flag_at(rho * X + (c + jj) % X, a.fl_pres + me), v);
         for (int ii = 1; ii < Y; ++ii) st_relaxed_sys(flag_at(((rho + ii) % Y) * X + c, a.fl_pres + me), v);
       }
+      bool ok = true;
+      auto need = [&](size_t idx) {
+        if (!ok) return;
+        const uint32_t* f = myflags + idx;
+        unsigned spin = 0;
+        while ((int32_t)(ld_relaxed_sys(f) - v) < 0) {
+          __nanosleep(32);
+          if ((++spin & 255u) == 0 && (gtimer() > deadline || *(volatile int*)&s_abort)) {
+            ok = false;
+            return;
+          }
+        }
+        (void)ld_acquire_sys(f);  // synchronizes with the peer's fence + flag store
+      };
       uint32_t ps = 0;  // operand loads issued (ring position)
-      for (int J = b; J < njobs; J += G) {
-        const Job jb = job_of<DT, W>(a, kind, J, X, Y, rho, c);
+      int nj = 0;       // valid jobs so far (trace index)
+      for (int J = b; J < njobs && ok; J += G) {
+        const Job jb = job_of_checked<DT, W>(a, kind, J, X, Y, rho, c);
         if (!jb.ok) continue;
         // -- wait for this job's inputs --
-        bool ok = true;
-        auto need = [&](size_t idx) {
-          if (!ok) return;
-          const uint32_t* f = myflags + idx;
-          unsigned spin = 0;
-          while ((int32_t)(ld_relaxed_sys(f) - v) < 0) {
-            __nanosleep(32);
-            if ((++spin & 255u) == 0 && (gtimer() > deadline || *(volatile int*)&s_abort)) {
-              ok = false;
-              return;
+        if (kind == kR) {
+          for (int j = 0; j < X; ++j) {
+            if (input_from_buf<DT, W>(a, jb.t, j == c)) {
+              if (j != c) need(a.fl_pres + rho * X + j);
+            } else {
+              need(fl_win(a, Y, j, jb.s, jb.k));
             }
           }
-          (void)ld_acquire_sys(f);  // synchronizes with the peer's fence + flag store
-        };
-        const bool ownbuf = own_from_buf<DT, W>(a, jb.t);
-        if (kind == kR) {
-          for (int j = 0; j < X; ++j)
-            if (j != c || !ownbuf) need(fl_win(a, Y, j, jb.s, jb.k));
         } else if (kind == kVR) {
           for (int i = 0; i < Y; ++i) {
             if (X > 1) need(fl_p1(a, i, jb.k));
-            else if (i != rho || !ownbuf) need(fl_win(a, Y, i, 0, jb.k));
+            else if (input_from_buf<DT, W>(a, jb.t, i == rho)) { if (i != rho) need(a.fl_pres + i * X); }
+            else need(fl_win(a, Y, i, 0, jb.k));
           }
         } else if (kind == kVA) {
           need(fl_v(a, jb.i, jb.k));
         } else if (kind == kH) {
           need(fl_c(a, Y, jb.j, jb.s, jb.k));
         }
-        if (!ok) {
-          atomicExch_system(R->err, kErrTimeout);
-          s_abort = 1;
-          break;
-        }
+        if (!ok) break;
         fence_proxy_async();  // generic-proxy acquire before the async-proxy (TMA) reads
+        pstamp(a, blockIdx.x, nj++, 0);
         // -- issue the operand loads (fold order) --
-        const bool direct = (kind == kS0) && !(a.aligned && (jb.t.nel % a.q) == 0);
-        for (int o = 0; o < nops; ++o) {
+        const bool direct = (kind == kS0) && !(a.aligned && !ragged(a, jb.t));
+        for (int o = 0; o < nops && ok; ++o) {
           const uint32_t slot = ps % NS, use = ps / NS;
           ++ps;
           if (use > 0 && !mbar_wait_abortable(&empty[slot], (use - 1) & 1u, &s_abort)) { ok = false; break; }
           const char* src = nullptr;
           uint32_t bytes = (uint32_t)jb.t.nvec * kVecBytes;
           if (kind == kS0) {
-            // my buffer's tile (dtype bytes)
-            bytes = (uint32_t)jb.t.nvec * VE * DB;
-            src = reinterpret_cast<const char*>(buf) + (a.buf_off + jb.t.co + jb.t.e0) * DB;
+            bytes = (uint32_t)jb.t.nvec * VE * DB;  // my buffer's tile (dtype bytes)
+            src = bufp(me, jb.t);
           } else if (kind == kR) {
             const int j = (c + 1 + o) % X;  // fold order: columns c+1, ..., c
-            if (j == c && ownbuf)
-              src = reinterpret_cast<const char*>(buf) + (a.buf_off + jb.t.co + jb.t.e0) * DB;
-            else
-              src = R->ws[rho * X + j] + a.win_off[par] + (jb.t.co + jb.t.e0) * SW;
+            src = input_from_buf<DT, W>(a, jb.t, j == c) ? bufp(rho * X + j, jb.t)
+                                                        : R->ws[rho * X + j] + a.win_off[par] + (jb.t.co + jb.t.e0) * SW;
           } else if (kind == kVR) {
             const int i = (rho + 1 + o) % Y;  // fold order: rows rho+1, ..., rho
-            if (X > 1)
-              src = R->ws[i * X + c] + a.p1_off[par] + jb.t.e0 * SW;
-            else if (i == rho && ownbuf)
-              src = reinterpret_cast<const char*>(buf) + (a.buf_off + jb.t.co + jb.t.e0) * DB;
-            else
-              src = R->ws[i * X + c] + a.win_off[par] + (jb.t.co + jb.t.e0) * SW;
+            if (X > 1) src = R->ws[i * X + c] + a.p1_off[par] + jb.t.e0 * SW;
+            else src = input_from_buf<DT, W>(a, jb.t, i == rho) ? bufp(i * X, jb.t)
+                                                               : R->ws[i * X] + a.win_off[par] + (jb.t.co + jb.t.e0) * SW;
           } else if (kind == kVA) {
             src = R->ws[jb.i * X + c] + a.chunk_off[par] + jb.t.e0 * SW;
           } else {
@@ -336,13 +382,12 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
             tma_load(smem + (size_t)slot * a.slot_bytes, src, bytes, &full[slot]);
           }
         }
-        if (!ok) {
-          s_abort = 1;
-          break;
-        }
       }
-      if (presence && !*(volatile int*)&s_abort) {
-        bool ok = true;
+      if (!ok) {
+        atomicExch_system(R->err, kErrTimeout);
+        s_abort = 1;
+      }
+      if (presence && ok) {
         auto seen = [&](int peer) {
           const uint32_t* f = myflags + a.fl_pres + peer;
           unsigned spin = 0;
@@ -357,63 +402,88 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
       }
     }
   } else if (warp == 1) {
-    // =============================== signaler =====================================
-    // After the consumers finish job J (all its stores issued, local), one system-scope
-    // fence publishes every completed job, then the flag stores tell the consumers of
-    // each tile that it may be pulled.  Jobs complete in order; one fence covers all
-    // jobs completed so far.
-    if (lane == 0 && kind != kH) {
-      int signaled = 0;  // jobs of this CTA signaled so far (valid jobs only)
-      int J = b;
-      while (true) {
-        // next valid job
-        Job jb;
-        jb.ok = false;
+    // ========================== storer + signaler ==================================
+    if (lane == 0) {
+      int Js = b, Jg = b;          // cursors: next job to store / to signal
+      int nst = 0, nsig = 0;       // jobs stored / signaled
+      uint32_t rs = 0;             // ring position of the next job to release
+      auto next_valid = [&](int& J, Job& jb) -> bool {
         for (; J < njobs; J += G) {
-          jb = job_of<DT, W>(a, kind, J, X, Y, rho, c);
-          if (jb.ok) break;
+          jb = job_of_checked<DT, W>(a, kind, J, X, Y, rho, c);
+          if (jb.ok) return true;
         }
-        if (J >= njobs) break;
-        bool aborted = false;
-        while (ld_acquire_cta(&s_done) < kConsumerWarps * (signaled + 1)) {
-          if (*(volatile int*)&s_abort) { aborted = true; break; }
+        return false;
+      };
+      Job js, jg;
+      bool more_s = next_valid(Js, js);
+      bool more_g = next_valid(Jg, jg);
+      while (more_g) {
+        // consumers finished jobs [0, done)
+        int done;
+        while ((done = ld_acquire_cta(&s_done) / kConsumerWarps) <= nst) {
+          if (*(volatile int*)&s_abort) break;
           __nanosleep(20);
         }
-        if (aborted) break;
-        fence_proxy_async();
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
-        // signal every job completed so far (at least this one)
-        const int done = ld_acquire_cta(&s_done) / kConsumerWarps;
-        while (true) {
-          // ---- raise the flags of job jb ----
+        if (*(volatile int*)&s_abort) break;
+        // ---- bulk-store every finished job from its slot 0 ----
+        const uint32_t rs0 = rs;
+        while (nst < done && more_s) {
+          const Tile& t = js.t;
+          const unsigned char* src = smem + (size_t)(rs % NS) * a.slot_bytes;
+          const uint32_t bytes = (uint32_t)t.nvec * kVecBytes;
+          const bool bb = buf_bulk<DT, W>(a, t);
           if (kind == kS0) {
-            if (X > 1) st_relaxed_sys(flag_at(rho * X + jb.j, fl_win(a, Y, c, jb.s, jb.k)), v);
-            else st_relaxed_sys(flag_at(jb.s * X, fl_win(a, Y, rho, 0, jb.k)), v);
+            tma_store(myws + a.win_off[par] + (t.co + t.e0) * SW, src, bytes);
+          } else if (kind == kR && Y > 1) {
+            tma_store(myws + a.p1_off[par] + t.e0 * SW, src, bytes);
+          } else {  // final values: my chunk region (read by peers) and my buffer
+            const bool chunk_out = (kind == kVR) || (kind == kR) || (kind == kVA && X > 1);
+            if (chunk_out) tma_store(myws + a.chunk_off[par] + t.e0 * SW, src, bytes);
+            if (bb) tma_store(bufp(me, t), src, bytes);
+          }
+          tma_commit();
+          rs += (uint32_t)nops;
+          ++nst;
+          Js += G;
+          more_s = next_valid(Js, js);
+        }
+        // ---- free the slots once the bulk stores have read them ----
+        tma_wait_read<0>();
+        for (uint32_t p = rs0; p < rs; ++p) mbar_arrive1(&empty[p % NS]);
+        if (kind == kH) {
+          nsig = nst;  // H raises no flags (its result is final and local)
+          if (!more_s) { tma_wait_all<0>(); break; }
+          continue;
+        }
+        // ---- wait for the writes, publish, raise the flags of every stored job ----
+        tma_wait_all<0>();
+        fence_proxy_async();
+        if (a.fence == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
+        else if (a.fence == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        while (nsig < nst && more_g) {
+          if (kind == kS0) {
+            if (X > 1) st_relaxed_sys(flag_at(rho * X + jg.j, fl_win(a, Y, c, jg.s, jg.k)), v);
+            else st_relaxed_sys(flag_at(jg.s * X, fl_win(a, Y, rho, 0, jg.k)), v);
           } else if (kind == kR) {
             if (Y > 1) {
-              st_relaxed_sys(flag_at(jb.s * X + c, fl_p1(a, rho, jb.k)), v);
+              st_relaxed_sys(flag_at(jg.s * X + c, fl_p1(a, rho, jg.k)), v);
             } else {
               for (int jj = 1; jj < X; ++jj)
-                st_relaxed_sys(flag_at(rho * X + (c + jj) % X, fl_c(a, Y, c, 0, jb.k)), v);
+                st_relaxed_sys(flag_at(rho * X + (c + jj) % X, fl_c(a, Y, c, 0, jg.k)), v);
             }
           } else if (kind == kVR) {
             for (int ii = 1; ii < Y; ++ii)
-              st_relaxed_sys(flag_at(((rho + ii) % Y) * X + c, fl_v(a, rho, jb.k)), v);
+              st_relaxed_sys(flag_at(((rho + ii) % Y) * X + c, fl_v(a, rho, jg.k)), v);
             for (int jj = 1; jj < X; ++jj)
-              st_relaxed_sys(flag_at(rho * X + (c + jj) % X, fl_c(a, Y, c, rho, jb.k)), v);
+              st_relaxed_sys(flag_at(rho * X + (c + jj) % X, fl_c(a, Y, c, rho, jg.k)), v);
           } else if (kind == kVA) {
             for (int jj = 1; jj < X; ++jj)
-              st_relaxed_sys(flag_at(rho * X + (c + jj) % X, fl_c(a, Y, c, jb.i, jb.k)), v);
+              st_relaxed_sys(flag_at(rho * X + (c + jj) % X, fl_c(a, Y, c, jg.i, jg.k)), v);
           }
-          ++signaled;
-          J += G;
-          if (signaled >= done) break;
-          jb.ok = false;
-          for (; J < njobs; J += G) {
-            jb = job_of<DT, W>(a, kind, J, X, Y, rho, c);
-            if (jb.ok) break;
-          }
-          if (J >= njobs) break;
+          pstamp(a, blockIdx.x, nsig, 3);
+          ++nsig;
+          Jg += G;
+          more_g = next_valid(Jg, jg);
         }
       }
     }
@@ -421,84 +491,115 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
     // =============================== consumers ====================================
     const int ct = tid - 64;  // 0 .. kConsumers-1
     uint32_t cs = 0;          // operands consumed (ring position)
+    int nj = 0;               // valid jobs so far (trace index)
     for (int J = b; J < njobs; J += G) {
-      const Job jb = job_of<DT, W>(a, kind, J, X, Y, rho, c);
+      const Job jb = job_of_checked<DT, W>(a, kind, J, X, Y, rho, c);
       if (!jb.ok) continue;
       const uint32_t slot0 = cs;
       bool ok = true;
       for (int o = 0; o < nops && ok; ++o)
         ok = mbar_wait_abortable(&full[(slot0 + o) % NS], ((slot0 + o) / NS) & 1u, &s_abort);
       if (!ok) break;
+      if (ct == 0) pstamp(a, blockIdx.x, nj, 1);
       const Tile& t = jb.t;
       const unsigned long long cbase = t.co;                  // chunk offset in the round
+      unsigned char* const out = smem + (size_t)(slot0 % NS) * a.slot_bytes;  // slot 0 = result
       auto slotp = [&](int o) -> const unsigned char* {
         return smem + (size_t)((slot0 + o) % NS) * a.slot_bytes;
       };
+      const bool bb = buf_bulk<DT, W>(a, t);
       if (kind == kS0) {
-        // cast/copy my buffer's tile into win (C1: w = to_wire(in))
-        const bool direct = !(a.aligned && (t.nel % a.q) == 0);
-        char* dst = myws + a.win_off[par] + (cbase + t.e0) * SW;
-        for (int vv = ct; vv < t.nvec; vv += kConsumers) {
-          uint4 w;
-          if (direct) {
-            const unsigned long long el = t.e0 + (unsigned long long)vv * VE;
-            const int nrem = (int)min((unsigned long long)VE, t.nel - (unsigned long long)vv * VE);
-            w = load_user<DT, W>(buf, a.buf_off + cbase + el, nrem, a.aligned != 0);
-          } else if constexpr (DT == W) {
-            w = *reinterpret_cast<const uint4*>(slotp(0) + (size_t)vv * 16);
-          } else {
-            const float4* f = reinterpret_cast<const float4*>(slotp(0) + (size_t)vv * 32);
-            const float4 f0 = f[0], f1 = f[1];
-            const float ff[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-            w = pack<W>(ff);
+        // C1: w = to_wire(in) into the slot (then the storer bulk-stores it to win)
+        const bool direct = !(a.aligned && !ragged(a, t));
+        if (direct || DT != W) {
+          for (int base = 0; base < t.nvec; base += kConsumers * U) {  // uniform trip count
+            const int v0 = base + ct;
+            uint4 w[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int vv = v0 + u * kConsumers;
+              if (vv >= t.nvec) continue;
+              const unsigned long long el = t.e0 + (unsigned long long)vv * VE;
+              const int nrem = (int)min((unsigned long long)VE, t.nel - (unsigned long long)vv * VE);
+              if (direct) {
+                w[u] = load_user<DT, W>(buf, a.buf_off + cbase + el, nrem, a.aligned != 0);
+              } else if constexpr (DT != W) {
+                const float4* f = reinterpret_cast<const float4*>(slotp(0) + (size_t)vv * 32);
+                const float4 f0 = f[0], f1 = f[1];
+                const float ff[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+                w[u] = pack<W>(ff);
+              }
+            }
+            if (!direct && DT != W) consumer_bar();  // in-place f32 -> wire: all reads first
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int vv = v0 + u * kConsumers;
+              if (vv < t.nvec) *reinterpret_cast<uint4*>(out + (size_t)vv * 16) = w[u];
+            }
+            if (!direct && DT != W) consumer_bar();
           }
-          st_ws(dst + (size_t)vv * 16, w);
         }
       } else if (kind == kR || kind == kVR) {
         // fold the operands in ring order (loaded in that order), f32 / u32 accumulation
         const bool last_reduce = (kind == kVR) || (Y == 1);
-        for (int vv = ct; vv < t.nvec; vv += kConsumers) {
-          Acc acc[VE];
-          {
-            Acc tmp[VE];
-            unpack<W>(*reinterpret_cast<const uint4*>(slotp(0) + (size_t)vv * 16), acc);
-            for (int o = 1; o < nops; ++o) {
-              unpack<W>(*reinterpret_cast<const uint4*>(slotp(o) + (size_t)vv * 16), tmp);
-              acc_add<W>(acc, tmp);
+        for (int v0 = ct; v0 < t.nvec; v0 += kConsumers * U) {  // vectors v0 + u * kConsumers
+          Acc acc[U][VE];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int vv = v0 + u * kConsumers;
+            if (vv < t.nvec) unpack<W>(*reinterpret_cast<const uint4*>(slotp(0) + (size_t)vv * 16), acc[u]);
+          }
+          for (int o = 1; o < nops; ++o) {
+            uint4 r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int vv = v0 + u * kConsumers;
+              if (vv < t.nvec) r[u] = *reinterpret_cast<const uint4*>(slotp(o) + (size_t)vv * 16);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int vv = v0 + u * kConsumers;
+              if (vv < t.nvec) {
+                Acc tmp[VE];
+                unpack<W>(r[u], tmp);
+                acc_add<W>(acc[u], tmp);
+              }
             }
           }
-          const unsigned long long el = t.e0 + (unsigned long long)vv * VE;  // in chunk
-          if (!last_reduce) {
-            st_ws(myws + a.p1_off[par] + el * SW, pack<W>(acc));
-          } else {
-            if (a.op == 1) acc_mean<W>(acc, a.inv_n, N);
-            const uint4 out = pack<W>(acc);
-            if (X > 1 || Y > 1) st_ws(myws + a.chunk_off[par] + el * SW, out);
-            const int nrem = (int)min((unsigned long long)VE, t.nel - (unsigned long long)vv * VE);
-            store_user<DT, W>(buf, a.buf_off + cbase + el, nrem, out, a.aligned != 0);
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int vv = v0 + u * kConsumers;
+            if (vv >= t.nvec) continue;
+            if (last_reduce && a.op == 1) acc_mean<W>(acc[u], a.inv_n, N);
+            const uint4 o4 = pack<W>(acc[u]);
+            *reinterpret_cast<uint4*>(out + (size_t)vv * 16) = o4;
+            if (last_reduce && !bb) {
+              const unsigned long long el = t.e0 + (unsigned long long)vv * VE;
+              const int nrem = (int)min((unsigned long long)VE, t.nel - (unsigned long long)vv * VE);
+              store_user<DT, W>(buf, a.buf_off + cbase + el, nrem, o4, a.aligned != 0);
+            }
           }
         }
-      } else {
-        // VA / H: copy a peer's final tile into my buffer (and my chunk region for VA,
-        // which my row peers pull next)
+      } else if (!bb) {
+        // VA / H into a buffer the bulk store cannot take (cast, unaligned, ragged)
         for (int vv = ct; vv < t.nvec; vv += kConsumers) {
           const uint4 w = *reinterpret_cast<const uint4*>(slotp(0) + (size_t)vv * 16);
           const unsigned long long el = t.e0 + (unsigned long long)vv * VE;
-          if (kind == kVA && X > 1) st_ws(myws + a.chunk_off[par] + el * SW, w);
           const int nrem = (int)min((unsigned long long)VE, t.nel - (unsigned long long)vv * VE);
           store_user<DT, W>(buf, a.buf_off + cbase + el, nrem, w, a.aligned != 0);
         }
       }
       cs += nops;
+      fence_view_async_smem();  // my shared-memory writes -> the storer's TMA reads
       __syncwarp();
-      if (lane == 0) {
-        for (int o = 0; o < nops; ++o) mbar_arrive1(&empty[(slot0 + o) % NS]);
-        __threadfence_block();
-        atomicAdd(&s_done, 1);
-      }
+      if (lane == 0) atomicAdd(&s_done, 1);
+      if (ct == 0) pstamp(a, blockIdx.x, nj, 2);
+      ++nj;
     }
   }
   __syncthreads();
+  if (tid == 0 && a.trace && blockIdx.x < kMaxLocal * 512)
+    a.trace[((size_t)blockIdx.x * kPullTraceJobs + kPullTraceJobs - 1) * 4 + 1] = gtimer();
   // the last CTA of this rank to finish advances the call epoch (device-resident, so the
   // call can be captured in a CUDA graph)
   if (tid == 0) {

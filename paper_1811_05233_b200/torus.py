@@ -148,6 +148,18 @@ class _CommBase:
             "torus_comm_trace")
         return out
 
+    def pull_trace(self, max_ctas: int = 1024):
+        """Device trace of the last pull-kernel launch (TORUS_TRACE=1): (numpy [ctas, 64, 4]
+        of ns, ctas per rank, CTA split [S0, R, VR, VA, H])."""
+        import numpy as np
+        out = np.zeros((max_ctas, 64, 4), dtype=np.uint64)
+        g = ctypes.c_int()
+        kinds = (ctypes.c_int * 5)()
+        check(_lib.load().torus_comm_pull_trace(
+            self._comm, out.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), out.nbytes,
+            ctypes.byref(g), kinds), "torus_comm_pull_trace")
+        return out, g.value, list(kinds)
+
     def async_error(self) -> int:
         return _lib.load().torus_comm_get_async_error(self._comm)
 
@@ -215,6 +227,26 @@ class TorusComm(_CommBase):
             _dtype_code(wire or t.dtype), OPS[op], _stream_ptr(stream)), "torus_allreduce_ex")
         return t
 
+
+    def register(self, t: torch.Tensor, group=None) -> torch.Tensor:
+        """Collective: register `t` (a contiguous CUDA tensor every rank will pass to
+        all_reduce) for zero-copy -- peers then read its inputs straight over NVLink
+        (torus_buffer_export / all-gather / torus_register_buffer)."""
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("register needs a contiguous CUDA tensor")
+        L = _lib.load()
+        h = torus_ipc_handle_t()
+        nbytes = t.numel() * t.element_size()
+        check(L.torus_buffer_export(ctypes.c_void_p(t.data_ptr()), nbytes, ctypes.byref(h)),
+              "torus_buffer_export")
+        arr = handles_array(exchange_blobs(bytes(h), self.world, group))
+        check(L.torus_register_buffer(self._comm, ctypes.c_void_p(t.data_ptr()), nbytes, arr),
+              "torus_register_buffer")
+        return t
+
+    def deregister(self, t: torch.Tensor) -> None:
+        check(_lib.load().torus_deregister_buffer(self._comm, ctypes.c_void_p(t.data_ptr())),
+              "torus_deregister_buffer")
 
     def reserve(self, staging_bytes: int) -> None:
         check(_lib.load().torus_comm_reserve(self._comm, staging_bytes), "torus_comm_reserve")
