@@ -281,9 +281,10 @@ TORUS_API int torus_partition(unsigned long long n, int parts, int q, unsigned l
 TORUS_API int torus_comm_trace(torus_comm_t comm, unsigned long long* host, size_t bytes);
 
 /* Device trace of the last pull-kernel launch (TORUS_TRACE=1 at init): host array
- * [ctas][64][4] u64 globaltimer stamps, CTAs of all local ranks in launch order; per job
+ * [ctas][64][8] u64 globaltimer stamps, CTAs of all local ranks in launch order; per job
  * n < 63 of each CTA: 0 producer saw the inputs' flags, 1 operands landed in shared
- * memory, 2 consumers done, 3 flags raised; [63][0..1] = CTA start / end.  Also writes
+ * memory, 2 consumers done, 3 flags raised, 4 bulk stores issued, 5 stores read the
+ * shared memory; [63][0..1] = CTA start / end.  Also writes
  * the CTAs per rank and the split over the five CTA kinds (S0, R, VR, VA, H).
  * Synchronizes the device. */
 TORUS_API int torus_comm_pull_trace(torus_comm_t comm, unsigned long long* host, size_t bytes,

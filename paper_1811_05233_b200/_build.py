@@ -11,7 +11,20 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 SOURCES = [CSRC / "torus_abi.cu", CSRC / "torus_kernels.cu", CSRC / "torus_pull.cu",
            CSRC / "torus_baselines.cu", CSRC / "torus_ll.cu", CSRC / "torus_nvls.cu"]
-HEADERS = [CSRC / "torus_internal.h", CSRC / "torus_device.cuh", ROOT / "include" / "torus.h"]
+HEADERS = [CSRC / "torus_internal.h", CSRC / "torus_device.cuh", CSRC / "torus_pull.h",
+           ROOT / "include" / "torus.h"]
+
+
+def _deps(src: pathlib.Path, seen=None) -> set:
+    """Headers a source includes (transitively, quoted includes only)."""
+    import re
+    seen = set() if seen is None else seen
+    for m in re.finditer(r'#include "([^"]+)"', src.read_text()):
+        h = (src.parent / m.group(1)).resolve()
+        if h.exists() and h not in seen:
+            seen.add(h)
+            _deps(h, seen)
+    return seen
 LIB = PKG / "libtorus.so"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -41,13 +54,13 @@ def build(force: bool = False, verbose: bool = False, out: pathlib.Path | None =
         return lib
     odir = PKG / "build" / ("default" if not defines else "_".join(defines).replace("=", "-"))
     odir.mkdir(parents=True, exist_ok=True)
-    hdr_t = max(p.stat().st_mtime for p in HEADERS)
     compile_flags = [f for f in FLAGS if f not in ("-shared", "-cudart", "static")]
     objs, procs = [], []
     for src in SOURCES:
         o = odir / f"{src.stem}.o"
         objs.append(o)
-        if not force and o.exists() and o.stat().st_mtime > max(src.stat().st_mtime, hdr_t):
+        dep_t = max([src.stat().st_mtime] + [h.stat().st_mtime for h in _deps(src)])
+        if not force and o.exists() and o.stat().st_mtime > dep_t:
             continue
         tmp_o = o.with_name(f"{o.name}.tmp{os.getpid()}")
         procs.append((src, tmp_o, o, subprocess.Popen(

@@ -17,6 +17,7 @@
 
 #include "../../include/torus.h"
 #include "torus_internal.h"
+#include "torus_pull.h"
 
 using namespace torus;
 
@@ -52,7 +53,7 @@ size_t env_size(const char* name, size_t dflt) {
 
 constexpr size_t kDefaultSlab = 512ull << 20;   // real ranks (f32 51M-element rounds fit)
 constexpr size_t kDefaultVirtualSlab = 320ull << 20;  // per virtual rank (N slabs on one GPU)
-constexpr size_t kPullTraceBytes = (size_t)kMaxLocal * 512 * kPullTraceJobs * 4 * 8;
+constexpr size_t kPullTraceBytes = (size_t)kMaxLocal * 512 * kPullTraceJobs * kPullTraceEv * 8;
 constexpr int kLLThreadsHost = 256;  // ll_kernel block size (torus_kernels.cu)
 
 struct Slab {

@@ -98,41 +98,6 @@ struct LaunchArgs {
   int sd1;                       // default kernel: stage distance 1 even with T > 1
 };
 
-// Per-launch arguments of the pull (dataflow) kernel, torus_pull.cu.  Everything that
-// decides WHICH bytes and flags a tile touches (n, q, TV, Kmax, region and flag offsets)
-// must be equal on every rank; the CTA split g[] and the ring (nslots, slot_bytes) are
-// rank-local choices.
-struct PullArgs {
-  const RankDev* ranks;          // device array [nlocal]
-  void* buf[kMaxLocal];          // user buffer of each local rank
-  unsigned long long n;          // elements in this round
-  unsigned long long buf_off;    // element offset of the round inside the user buffers
-  unsigned long long win_off[2], p1_off[2], chunk_off[2];  // slab byte offsets by parity
-  unsigned long long flag_off;   // slab byte offset of the pull flag region
-  unsigned long long fl_win, fl_p1, fl_v, fl_c, fl_pres;   // word offsets of the flag kinds
-  unsigned long long timeout_ns;
-  int nlocal;
-  int q;                         // partition quantum (elements) = one 16-byte wire vector
-  int TV;                        // 16-byte wire vectors per tile
-  int Kmax;                      // tiles of the largest sub-chunk
-  int op;                        // 0 sum, 1 mean
-  float inv_n;                   // f32(1/N)
-  int aligned;                   // all user buffers 16-byte aligned
-  int g[5];                      // CTAs per rank of each kind: S0, R, VR, VA, H
-  int gsum;
-  int nslots, slot_bytes;        // shared-memory ring
-  unsigned long long* trace;     // optional [nlocal*gsum][kPullTraceJobs][4] globaltimer stamps
-  int fence;                     // publish fence: 0 fence.acq_rel.sys, 1 .gpu, 2 none (measurement only)
-  int zc;                        // zero-copy: the peers' user buffers are mapped here (registered,
-                                 // dtype == wire, 16-byte aligned on every rank) -- no S0 copy
-  char* peer_buf[kMaxRanks];     // zc: every rank's user buffer as mapped in this process
-};
-constexpr int kPullTraceJobs = 64;  // trace: first 64 jobs of every CTA; slot 63 = CTA start/end
-inline size_t pull_smem_bytes(int nslots, int slot_bytes) {
-  return (size_t)nslots * slot_bytes + 2 * (size_t)nslots * 8;
-}
-constexpr size_t kPullFlagBytes = 8ull << 20;  // pull flag region per slab
-
 // TMA kernel shared memory: nbufs ring buffers of one piece each (tile_vecs 16-byte wire
 // vectors, or the same elements in the user dtype: `ratio` = sizeof(dtype)/sizeof(wire),
 // at least 1) + 3 mbarriers per buffer
@@ -218,8 +183,6 @@ int torus_kernel_max_ctas_per_sm(int dtype, int wire);
 cudaError_t launch_ring(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
 cudaError_t launch_hier(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
 cudaError_t launch_ll(const LaunchArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
-cudaError_t launch_pull(const PullArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
-int pull_ctas_per_sm(size_t smem);
 cudaError_t launch_multi_copy(const MultiTable& tab, int n, int dtype, int wire, void* staging,
                               bool pack, cudaStream_t stream);
 cudaError_t launch_probe(const RankDev* ranks, unsigned long long data_off, unsigned long long bytes,

@@ -40,6 +40,7 @@
 #include <cstdlib>
 
 #include "torus_device.cuh"
+#include "torus_pull.h"
 
 namespace torus {
 namespace {
@@ -218,12 +219,12 @@ __device__ __forceinline__ Job job_of_checked(const PullArgs& a, int kind, int J
   return jb;
 }
 
-// Trace (TORUS_TRACE=1): per CTA, per job n < 63 four globaltimer stamps -- 0 producer saw
-// the inputs' flags, 1 consumers saw the operands land, 2 consumers done, 3 signaler
-// raised the flags; slot 63 holds the CTA's start and end.
+// Trace (TORUS_TRACE=1): per CTA, per job n < 63 globaltimer stamps -- 0 producer saw the
+// inputs' flags, 1 consumers saw the operands land, 2 consumers done, 3 flags raised,
+// 4 bulk stores issued, 5 stores read (slots freed); slot 63 = the CTA's start and end.
 __device__ __forceinline__ void pstamp(const PullArgs& a, int cta, int n, int ev) {
   if (a.trace && n < kPullTraceJobs - 1 && cta < kMaxLocal * 512)
-    a.trace[((size_t)cta * kPullTraceJobs + n) * 4 + ev] = gtimer();
+    a.trace[((size_t)cta * kPullTraceJobs + n) * kPullTraceEv + ev] = gtimer();
 }
 
 // ------------------------------------------------------------------------------------
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
   }
   __syncthreads();
   if (tid == 0 && a.trace && blockIdx.x < kMaxLocal * 512)
-    a.trace[((size_t)blockIdx.x * kPullTraceJobs + kPullTraceJobs - 1) * 4] = gtimer();
+    a.trace[((size_t)blockIdx.x * kPullTraceJobs + kPullTraceJobs - 1) * kPullTraceEv] = gtimer();
   const uint32_t epoch = s_epoch;
   const uint32_t v = epoch + 1u;               // flag value of this call
   const int par = (int)(epoch & 1u);
@@ -403,9 +404,14 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
     }
   } else if (warp == 1) {
     // ========================== storer + signaler ==================================
+    // Stores are issued one bulk group per batch of finished jobs; a batch's flags are
+    // raised once the NEXT batch has been issued (wait_group 1) or, when no new job has
+    // finished, after waiting for it alone (wait_group 0) -- so waiting for write
+    // completion never holds up slot recycling.
     if (lane == 0) {
       int Js = b, Jg = b;          // cursors: next job to store / to signal
       int nst = 0, nsig = 0;       // jobs stored / signaled
+      int older = 0;               // stored jobs of the older unsignaled batch (rest: newest)
       uint32_t rs = 0;             // ring position of the next job to release
       auto next_valid = [&](int& J, Job& jb) -> bool {
         for (; J < njobs; J += G) {
@@ -417,50 +423,11 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
       Job js, jg;
       bool more_s = next_valid(Js, js);
       bool more_g = next_valid(Jg, jg);
-      while (more_g) {
-        // consumers finished jobs [0, done)
-        int done;
-        while ((done = ld_acquire_cta(&s_done) / kConsumerWarps) <= nst) {
-          if (*(volatile int*)&s_abort) break;
-          __nanosleep(20);
-        }
-        if (*(volatile int*)&s_abort) break;
-        // ---- bulk-store every finished job from its slot 0 ----
-        const uint32_t rs0 = rs;
-        while (nst < done && more_s) {
-          const Tile& t = js.t;
-          const unsigned char* src = smem + (size_t)(rs % NS) * a.slot_bytes;
-          const uint32_t bytes = (uint32_t)t.nvec * kVecBytes;
-          const bool bb = buf_bulk<DT, W>(a, t);
-          if (kind == kS0) {
-            tma_store(myws + a.win_off[par] + (t.co + t.e0) * SW, src, bytes);
-          } else if (kind == kR && Y > 1) {
-            tma_store(myws + a.p1_off[par] + t.e0 * SW, src, bytes);
-          } else {  // final values: my chunk region (read by peers) and my buffer
-            const bool chunk_out = (kind == kVR) || (kind == kR) || (kind == kVA && X > 1);
-            if (chunk_out) tma_store(myws + a.chunk_off[par] + t.e0 * SW, src, bytes);
-            if (bb) tma_store(bufp(me, t), src, bytes);
-          }
-          tma_commit();
-          rs += (uint32_t)nops;
-          ++nst;
-          Js += G;
-          more_s = next_valid(Js, js);
-        }
-        // ---- free the slots once the bulk stores have read them ----
-        tma_wait_read<0>();
-        for (uint32_t p = rs0; p < rs; ++p) mbar_arrive1(&empty[p % NS]);
-        if (kind == kH) {
-          nsig = nst;  // H raises no flags (its result is final and local)
-          if (!more_s) { tma_wait_all<0>(); break; }
-          continue;
-        }
-        // ---- wait for the writes, publish, raise the flags of every stored job ----
-        tma_wait_all<0>();
+      auto publish = [&](int upto) {  // raise the flags of jobs [nsig, upto)
         fence_proxy_async();
         if (a.fence == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
         else if (a.fence == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        while (nsig < nst && more_g) {
+        while (nsig < upto && more_g) {
           if (kind == kS0) {
             if (X > 1) st_relaxed_sys(flag_at(rho * X + jg.j, fl_win(a, Y, c, jg.s, jg.k)), v);
             else st_relaxed_sys(flag_at(jg.s * X, fl_win(a, Y, rho, 0, jg.k)), v);
@@ -485,7 +452,55 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
           Jg += G;
           more_g = next_valid(Jg, jg);
         }
+      };
+      while (more_s || nsig < nst) {
+        if (*(volatile int*)&s_abort) break;
+        const int done = ld_acquire_cta(&s_done) / kConsumerWarps;  // consumers finished [0, done)
+        if (done > nst && more_s) {
+          // ---- one bulk group: every finished job, from its slot 0 ----
+          const uint32_t rs0 = rs;
+          const int nst0 = nst;
+          while (nst < done && more_s) {
+            const Tile& t = js.t;
+            const unsigned char* src = smem + (size_t)(rs % NS) * a.slot_bytes;
+            const uint32_t bytes = (uint32_t)t.nvec * kVecBytes;
+            if (kind == kS0) {
+              tma_store(myws + a.win_off[par] + (t.co + t.e0) * SW, src, bytes);
+            } else if (kind == kR && Y > 1) {
+              tma_store(myws + a.p1_off[par] + t.e0 * SW, src, bytes);
+            } else {  // final values: my chunk region (read by peers) and my buffer
+              const bool chunk_out = (kind == kVR) || (kind == kR) || (kind == kVA && X > 1);
+              if (chunk_out) tma_store(myws + a.chunk_off[par] + t.e0 * SW, src, bytes);
+              if (buf_bulk<DT, W>(a, t)) tma_store(bufp(me, t), src, bytes);
+            }
+            pstamp(a, blockIdx.x, nst, 4);
+            rs += (uint32_t)nops;
+            ++nst;
+            Js += G;
+            more_s = next_valid(Js, js);
+          }
+          tma_commit();
+          // ---- free the slots once the bulk stores have read them ----
+          tma_wait_read<0>();
+          for (uint32_t p = rs0; p < rs; ++p) mbar_arrive1(&empty[p % NS]);
+          for (int n = nst0; n < nst; ++n) pstamp(a, blockIdx.x, n, 5);
+          if (kind == kH) continue;
+          if (older > 0) {  // the previous batch is complete once only this one may pend
+            tma_wait_all<1>();
+            publish(nsig + older);
+          }
+          older = nst - nsig;
+        } else if (nsig < nst && kind != kH) {
+          tma_wait_all<0>();  // nothing new finished: publish what is stored
+          publish(nst);
+          older = 0;
+        } else if (!more_s) {
+          break;
+        } else {
+          __nanosleep(20);
+        }
       }
+      tma_wait_all<0>();
     }
   } else {
     // =============================== consumers ====================================
@@ -599,7 +614,7 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
   }
   __syncthreads();
   if (tid == 0 && a.trace && blockIdx.x < kMaxLocal * 512)
-    a.trace[((size_t)blockIdx.x * kPullTraceJobs + kPullTraceJobs - 1) * 4 + 1] = gtimer();
+    a.trace[((size_t)blockIdx.x * kPullTraceJobs + kPullTraceJobs - 1) * kPullTraceEv + 1] = gtimer();
   // the last CTA of this rank to finish advances the call epoch (device-resident, so the
   // call can be captured in a CUDA graph)
   if (tid == 0) {

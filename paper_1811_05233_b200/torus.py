@@ -149,10 +149,10 @@ class _CommBase:
         return out
 
     def pull_trace(self, max_ctas: int = 1024):
-        """Device trace of the last pull-kernel launch (TORUS_TRACE=1): (numpy [ctas, 64, 4]
+        """Device trace of the last pull-kernel launch (TORUS_TRACE=1): (numpy [ctas, 64, 8]
         of ns, ctas per rank, CTA split [S0, R, VR, VA, H])."""
         import numpy as np
-        out = np.zeros((max_ctas, 64, 4), dtype=np.uint64)
+        out = np.zeros((max_ctas, 64, 8), dtype=np.uint64)
         g = ctypes.c_int()
         kinds = (ctypes.c_int * 5)()
         check(_lib.load().torus_comm_pull_trace(

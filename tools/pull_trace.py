@@ -35,6 +35,8 @@ def worker(rank, world, port, X, Y, D, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     comm = TorusComm.init(X=X, Y=Y)
     x = torch.from_numpy(synthetic.make("grad", D, rank, "f16")).cuda()
+    if os.environ.get("TRACE_REGISTER", "1") == "1":
+        comm.register(x)
     for _ in range(5):
         comm.all_reduce(x, op="mean")
     torch.cuda.synchronize()
@@ -71,6 +73,10 @@ def summarise(out, world):
             cons = (j[:, :, 2] - j[:, :, 1])[valid] / 1e3
             sig_ok = valid & (j[:, :, 3] > 0)
             sig = (j[:, :, 3] - j[:, :, 2])[sig_ok] / 1e3
+            st_ok = valid & (j[:, :, 4] > 0) & (j[:, :, 5] > 0)
+            st_issue = (j[:, :, 4] - j[:, :, 2])[st_ok] / 1e3
+            st_read = (j[:, :, 5] - j[:, :, 4])[st_ok] / 1e3
+            st_pub = (j[:, :, 3] - j[:, :, 5])[st_ok & sig_ok] / 1e3
             first = (j[:, 0, 0] - t0)[j[:, 0, 0] > 0] / 1e3
             gaps = []
             for row in j[:, :, 0]:
@@ -81,6 +87,7 @@ def summarise(out, world):
             print(f"  {k:2s} x{g:3d}: start {st.min():.1f}-{st.max():.1f} end {en.min():.1f}-{en.max():.1f} us; "
                   f"jobs/CTA {valid.sum(1).mean():.1f}; first flags-seen {pc(first)}")
             print(f"        land {pc(land)} | consume {pc(cons)} | signal {pc(sig)} | job gap {pc(np.array(gaps))}")
+            print(f"        store issue {pc(st_issue)} | store read {pc(st_read)} | read->flags {pc(st_pub)}")
 
 
 if __name__ == "__main__":
