@@ -285,10 +285,10 @@ TORUS_API int torus_comm_trace(torus_comm_t comm, unsigned long long* host, size
  * n < 63 of each CTA: 0 producer saw the inputs' flags, 1 operands landed in shared
  * memory, 2 consumers done, 3 flags raised, 4 bulk stores issued, 5 stores read the
  * shared memory; [63][0..1] = CTA start / end.  Also writes
- * the CTAs per rank and the split over the five CTA kinds (S0, R, VR, VA, H).
+ * the CTAs per rank and the split over the CTA kinds (S0, R, VR, VA, H, SIG).
  * Synchronizes the device. */
 TORUS_API int torus_comm_pull_trace(torus_comm_t comm, unsigned long long* host, size_t bytes,
-                                    int* ctas_per_rank, int* kinds /*[5]*/);
+                                    int* ctas_per_rank, int* kinds /*[6]*/);
 
 /* Calibration probes (not part of the all-reduce; SURVEY.md 8(d) "Calibration"), enqueued
  * on `stream` with `ctas` CTAs (0 = the comm's count).  mode 0: push `bytes` split over

@@ -124,7 +124,8 @@ struct torus_comm {
   uint32_t* d_pull_ctr = nullptr;         // [nlocal][2] pull call epochs
   unsigned long long* d_pull_trace = nullptr;  // TORUS_TRACE=1: pull kernel stamps
   int last_data_kernel = 0;               // kernel that last used the shared data region
-  int last_pull_gsum = 0, last_pull_g[5] = {0, 0, 0, 0, 0};  // CTA split of the last pull launch
+  int last_pull_gsum = 0, last_pull_g[6] = {0, 0, 0, 0, 0, 0};  // CTA split of the last pull launch
+  unsigned long long* d_pull_pub = nullptr;  // pull kernel fence mode 3: [nlocal * 1024] job counts
   int ctas_req = 0;                       // CTA count requested at init (0 = auto)
 };
 
@@ -245,6 +246,8 @@ int alloc_comm_common(torus_comm* c) {
   *c->h_err = 0;
   CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_err), c->h_err, 0));
   CU(cudaMalloc(&c->d_ranks, sizeof(RankDev) * c->nlocal));
+  CU(cudaMalloc(&c->d_pull_pub, (size_t)c->nlocal * 1024 * sizeof(unsigned long long)));
+  CU(cudaMemset(c->d_pull_pub, 0, (size_t)c->nlocal * 1024 * sizeof(unsigned long long)));
   {
     const size_t nd = (size_t)c->nlocal * c->G;
     CU(cudaMalloc(&c->d_done_local, nd * 8 * sizeof(uint32_t)));
@@ -334,6 +337,7 @@ void destroy_resources(torus_comm* c) {
   if (c->d_epochs) cudaFree(c->d_epochs);
   if (c->d_trace) cudaFree(c->d_trace);
   if (c->d_pull_trace) cudaFree(c->d_pull_trace);
+  if (c->d_pull_pub) cudaFree(c->d_pull_pub);
   if (c->d_done_local) cudaFree(c->d_done_local);
   if (c->d_sig_ack) cudaFree(c->d_sig_ack);
   if (c->d_staging) cudaFree(c->d_staging);
@@ -628,14 +632,14 @@ int torus_comm_rank(torus_comm_t c, int* rank, int* world) {
 int torus_comm_ctas(torus_comm_t c) { return c ? c->G : -1; }
 
 int torus_comm_pull_trace(torus_comm_t c, unsigned long long* host, size_t bytes, int* ctas_per_rank,
-                          int* kinds /*[5]*/) {
+                          int* kinds /*[6]*/) {
   if (!c || !host) return fail(TORUS_ERR_INVALID_ARG, "null argument");
   if (!c->d_pull_trace) return fail(TORUS_ERR_UNSUPPORTED, "tracing is off (set TORUS_TRACE=1 before init)");
   CU(cudaDeviceSynchronize());
   CU(cudaMemcpy(host, c->d_pull_trace, std::min(bytes, kPullTraceBytes), cudaMemcpyDeviceToHost));
   if (ctas_per_rank) *ctas_per_rank = c->last_pull_gsum;
   if (kinds)
-    for (int k = 0; k < 5; ++k) kinds[k] = c->last_pull_g[k];
+    for (int k = 0; k < 6; ++k) kinds[k] = c->last_pull_g[k];
   return TORUS_OK;
 }
 
@@ -744,7 +748,7 @@ unsigned long long pull_kmax(unsigned long long n, int X, int Y, int q, int TV) 
 }
 
 bool pull_fits(const torus_comm* c, unsigned long long R, int wire, int dtype) {
-  if (c->mode != kModePull || c->world < 2 || std::max(c->X, c->Y) > 32) return false;
+  if (c->mode != kModePull || c->world < 2 || c->world > kMaxRanks || std::max(c->X, c->Y) > 32) return false;
   const unsigned long long sw = wire_size(wire);
   int tv, ns;
   pull_ring(c, (int)(wire_size(dtype) / sw), &tv, &ns);
@@ -839,7 +843,7 @@ int launch_pull_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype
   const int X = c->X, Y = c->Y;
   a.zc = pull_zero_copy(c, bufs, count * wire_size(dtype), dtype, wire, aligned, a.peer_buf) ? 1 : 0;
   const bool own_copy = !(dtype == wire && aligned);  // S0 also copies my own chunk
-  double w[5] = {0, 0, 0, 0, 0};
+  double w[6] = {0, 0, 0, 0, 0, 0};
   const double f0 = X > 1 ? (double)(X - 1) / X + (own_copy ? 1.0 / X : 0.0)
                           : (double)(Y - 1) / Y + (own_copy ? 1.0 / Y : 0.0);
   w[0] = a.zc ? 0.02 : c->pull_w[0] * f0 * ratio;  // zero-copy: S0 only copies ragged tails
@@ -854,6 +858,9 @@ int launch_pull_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype
     wsum += w[k];
   }
   if (gtot < kinds) return fail(TORUS_ERR_UNSUPPORTED, "pull kernel needs %d CTAs per rank, %d fit", kinds, gtot);
+  // fence mode 3: SIG CTAs (one thread per data CTA, 192 threads, up to 4 each)
+  const int nsig_ctas = c->pull_fence == 3 ? std::max(1, (gtot + 4 * 192 - 1) / (4 * 192)) : 0;
+  gtot -= nsig_ctas;
   int gs = 0;
   for (int k = 0; k < 5; ++k) {
     a.g[k] = w[k] > 0 ? std::max(1, (int)(gtot * w[k] / wsum)) : 0;
@@ -866,12 +873,23 @@ int launch_pull_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype
     --a.g[kb];
     --gs;
   }
-  a.gsum = gs;
+  a.g[5] = nsig_ctas;
+  a.gsum = gs + nsig_ctas;
+  a.pub = c->d_pull_pub;
   c->last_pull_gsum = gs;
-  for (int k = 0; k < 5; ++k) c->last_pull_g[k] = a.g[k];
+  for (int k = 0; k < 6; ++k) c->last_pull_g[k] = a.g[k];
   for (unsigned long long r0 = 0; r0 < count; r0 += R) {
     a.n = std::min<unsigned long long>(R, count - r0);
     a.buf_off = r0;
+    for (int j = 0; j < X; ++j) {
+      unsigned long long cl;
+      qpart(a.n, X, a.q, j, &a.g_co[j], &cl);
+      for (int s = 0; s < Y; ++s) {
+        qpart(cl, Y, a.q, s, &a.g_cs[j * Y + s], &a.g_sl[j * Y + s]);
+        const unsigned long long nv = (a.g_sl[j * Y + s] + a.q - 1) / a.q;
+        a.g_K[j * Y + s] = (int)((nv + tv - 1) / tv);
+      }
+    }
     const unsigned long long K = pull_kmax(a.n, X, Y, a.q, tv);
     a.Kmax = (int)std::max<unsigned long long>(1, K);
     a.fl_win = 0;

@@ -63,15 +63,16 @@ struct Tile {
 
 __device__ __forceinline__ Tile tile_of(const PullArgs& a, int X, int Y, int j, int s, int k) {
   Tile t;
-  unsigned long long cl, sl;
-  qpart(a.n, X, a.q, j, &t.co, &cl);
-  qpart(cl, Y, a.q, s, &t.cs, &sl);
+  const int js = j * Y + s;
   const unsigned long long per = (unsigned long long)a.TV * a.q;
   const unsigned long long st = (unsigned long long)k * per;
-  t.ok = st < sl;
+  const unsigned long long sl = a.g_sl[js];
+  t.ok = k < a.g_K[js];
+  t.co = a.g_co[j];
+  t.cs = a.g_cs[js];
   t.e0 = t.cs + st;
   t.nel = t.ok ? min(per, sl - st) : 0;
-  t.nvec = (int)((t.nel + a.q - 1) / a.q);
+  t.nvec = ((int)t.nel + a.q - 1) / a.q;  // nel <= TV * q fits 32 bits
   return t;
 }
 
@@ -89,7 +90,7 @@ __device__ __forceinline__ size_t fl_c(const PullArgs& a, int Y, int j, int s, i
   return a.fl_c + ((size_t)j * Y + s) * a.Kmax + k;
 }
 
-enum PullKind { kS0 = 0, kR = 1, kVR = 2, kVA = 3, kH = 4, kKinds = 5 };
+enum PullKind { kS0 = 0, kR = 1, kVR = 2, kVA = 3, kH = 4, kSig = 5, kKinds = 6 };
 
 // One job of a CTA: the tile, where its operands come from, where it waits.
 struct Job {
@@ -102,11 +103,12 @@ struct Job {
 // J = b, b + g, ...).  k-major order so that every rank produces tile k before k + 1.
 __device__ __forceinline__ int job_count(const PullArgs& a, int kind, int X, int Y) {
   switch (kind) {
-    case kS0: return a.Kmax * (X > 1 ? X * Y : Y);
+    case kS0: return (a.zc ? 1 : a.Kmax) * (X > 1 ? X * Y : Y);
     case kR: return a.Kmax * Y;
     case kVR: return a.Kmax;
     case kVA: return a.Kmax * (Y - 1);
-    default: return a.Kmax * (X - 1) * Y;
+    case kH: return a.Kmax * (X - 1) * Y;
+    default: return 0;
   }
 }
 
@@ -125,6 +127,8 @@ __device__ __forceinline__ Job job_of(const PullArgs& a, int kind, int J, int X,
         jb.j = 0;
         jb.s = J % Y;
       }
+      // zero-copy: S0 only copies ragged tails, i.e. each sub-chunk's last tile
+      if (a.zc) jb.k = max(0, a.g_K[jb.j * Y + jb.s] - 1);
       break;
     case kR:
       jb.k = J / Y;
@@ -189,6 +193,16 @@ __device__ __forceinline__ void consumer_bar() {  // named barrier 1 over the co
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
 
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
 __device__ __forceinline__ bool ragged(const PullArgs& a, const Tile& t) {
   return (t.nel % (unsigned long long)a.q) != 0;
 }
@@ -217,6 +231,45 @@ __device__ __forceinline__ Job job_of_checked(const PullArgs& a, int kind, int J
     if (input_from_buf<DT, W>(a, jb.t, own)) jb.ok = false;
   }
   return jb;
+}
+
+__device__ __forceinline__ void st_release_gpu64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Raise the flags that announce job `jg` of a CTA of `kind` to the ranks that consume it
+// (called after a fence that orders the job's stores before the flags).
+__device__ __forceinline__ void raise_flags(const PullArgs& a, const RankDev* R, int kind, const Job& jg,
+                                            uint32_t v) {
+  const int X = R->X, Y = R->Y, rho = R->rho, c = R->c;
+  auto flag_at = [&](int rank, size_t idx) -> uint32_t* {
+    return reinterpret_cast<uint32_t*>(R->ws[rank] + a.flag_off) + idx;
+  };
+  if (kind == kS0) {
+    if (X > 1) st_relaxed_sys(flag_at(rho * X + jg.j, fl_win(a, Y, c, jg.s, jg.k)), v);
+    else st_relaxed_sys(flag_at(jg.s * X, fl_win(a, Y, rho, 0, jg.k)), v);
+  } else if (kind == kR) {
+    if (Y > 1) {
+      st_relaxed_sys(flag_at(jg.s * X + c, fl_p1(a, rho, jg.k)), v);
+    } else {
+      for (int jj = 1; jj < X; ++jj) st_relaxed_sys(flag_at(rho * X + (c + jj) % X, fl_c(a, Y, c, 0, jg.k)), v);
+    }
+  } else if (kind == kVR) {
+    for (int ii = 1; ii < Y; ++ii) st_relaxed_sys(flag_at(((rho + ii) % Y) * X + c, fl_v(a, rho, jg.k)), v);
+    for (int jj = 1; jj < X; ++jj) st_relaxed_sys(flag_at(rho * X + (c + jj) % X, fl_c(a, Y, c, rho, jg.k)), v);
+  } else if (kind == kVA) {
+    for (int jj = 1; jj < X; ++jj) st_relaxed_sys(flag_at(rho * X + (c + jj) % X, fl_c(a, Y, c, jg.i, jg.k)), v);
+  }
 }
 
 // Trace (TORUS_TRACE=1): per CTA, per job n < 63 globaltimer stamps -- 0 producer saw the
@@ -296,7 +349,78 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
   const int njobs = job_count(a, kind, X, Y);
   const int nops = job_nops(kind, X, Y);
 
-  if (warp == 0) {
+  if (kind == kSig) {
+    // ================================ SIG CTA ======================================
+    // Every thread watches up to 4 data CTAs of this rank: when one publishes (gpu-scope
+    // release of its job count), acquire it, fence at system scope -- on this SM, which
+    // moves no bulk data -- and raise the flags of the newly published jobs.
+    const int ndata = a.gsum - a.g[kSig];
+    const unsigned long long deadline = gtimer() + a.timeout_ns;
+    constexpr int M = 4;
+    int dk[M], db[M], dJ[M], dn[M], dtot[M], dcta[M];
+    for (int m = 0; m < M; ++m) {
+      const int d = (b + m * G) * kPullThreads + tid;
+      dk[m] = -1;
+      if (d >= ndata) continue;
+      int k2 = 0, b2 = d;
+      while (k2 < kSig - 1 && b2 >= a.g[k2]) b2 -= a.g[k2++];
+      if (k2 == kH) continue;  // H raises no flags
+      const int nj2 = job_count(a, k2, X, Y);
+      int tot = 0;
+      for (int J = b2; J < nj2; J += a.g[k2])
+        if (job_of_checked<DT, W>(a, k2, J, X, Y, rho, c).ok) ++tot;
+      if (tot == 0) continue;
+      dk[m] = k2;
+      db[m] = b2;
+      dcta[m] = d;
+      dJ[m] = b2;
+      dn[m] = 0;
+      dtot[m] = tot;
+    }
+    const unsigned long long* pub = a.pub + (size_t)lr * a.gsum;
+    unsigned spin = 0;
+    while (true) {
+      bool live = false, work = false;
+      int cnt[M];
+      for (int m = 0; m < M; ++m) {
+        cnt[m] = 0;
+        if (dk[m] < 0) continue;
+        live = true;
+        const unsigned long long w = ld_relaxed_gpu64(pub + dcta[m]);
+        if ((uint32_t)(w >> 32) == epoch && (int)(uint32_t)w > dn[m]) {
+          cnt[m] = (int)(uint32_t)w;
+          work = true;
+        }
+      }
+      if (!live) break;
+      if (!work) {
+        __nanosleep(64);
+        if ((++spin & 255u) == 0 && (gtimer() > deadline || *(volatile int*)&s_abort)) {
+          atomicExch_system(R->err, kErrTimeout);
+          break;
+        }
+        continue;
+      }
+      // acquire what was published, then one system-scope fence for all of it
+      for (int m = 0; m < M; ++m) {
+        if (cnt[m] == 0) continue;
+        (void)ld_acquire_gpu64(pub + dcta[m]);
+      }
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int m = 0; m < M; ++m) {
+        if (cnt[m] == 0) continue;
+        const int k2 = dk[m], g2 = a.g[k2], nj2 = job_count(a, k2, X, Y);
+        while (dn[m] < cnt[m] && dJ[m] < nj2) {
+          const Job jg = job_of_checked<DT, W>(a, k2, dJ[m], X, Y, rho, c);
+          dJ[m] += g2;
+          if (!jg.ok) continue;
+          raise_flags(a, R, k2, jg, v);
+          ++dn[m];
+        }
+        if (dn[m] >= dtot[m]) dk[m] = -1;
+      }
+    }
+  } else if (warp == 0) {
     // =============================== producer =====================================
     if (lane == 0) {
       const unsigned long long deadline = gtimer() + a.timeout_ns;
@@ -425,28 +549,17 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
       bool more_g = next_valid(Jg, jg);
       auto publish = [&](int upto) {  // raise the flags of jobs [nsig, upto)
         fence_proxy_async();
+        if (a.fence == 3) {
+          // hand the jobs to a SIG CTA: gpu-scope release here, the system-scope fence
+          // and the remote flag stores happen on an SM without bulk traffic
+          st_release_gpu64(a.pub + blockIdx.x, ((unsigned long long)epoch << 32) | (unsigned)upto);
+          for (; nsig < upto; ++nsig) pstamp(a, blockIdx.x, nsig, 3);
+          return;
+        }
         if (a.fence == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
         else if (a.fence == 1) asm volatile("fence.acq_rel.gpu;" ::: "memory");
         while (nsig < upto && more_g) {
-          if (kind == kS0) {
-            if (X > 1) st_relaxed_sys(flag_at(rho * X + jg.j, fl_win(a, Y, c, jg.s, jg.k)), v);
-            else st_relaxed_sys(flag_at(jg.s * X, fl_win(a, Y, rho, 0, jg.k)), v);
-          } else if (kind == kR) {
-            if (Y > 1) {
-              st_relaxed_sys(flag_at(jg.s * X + c, fl_p1(a, rho, jg.k)), v);
-            } else {
-              for (int jj = 1; jj < X; ++jj)
-                st_relaxed_sys(flag_at(rho * X + (c + jj) % X, fl_c(a, Y, c, 0, jg.k)), v);
-            }
-          } else if (kind == kVR) {
-            for (int ii = 1; ii < Y; ++ii)
-              st_relaxed_sys(flag_at(((rho + ii) % Y) * X + c, fl_v(a, rho, jg.k)), v);
-            for (int jj = 1; jj < X; ++jj)
-              st_relaxed_sys(flag_at(rho * X + (c + jj) % X, fl_c(a, Y, c, rho, jg.k)), v);
-          } else if (kind == kVA) {
-            for (int jj = 1; jj < X; ++jj)
-              st_relaxed_sys(flag_at(rho * X + (c + jj) % X, fl_c(a, Y, c, jg.i, jg.k)), v);
-          }
+          raise_flags(a, R, kind, jg, v);
           pstamp(a, blockIdx.x, nsig, 3);
           ++nsig;
           Jg += G;
@@ -518,10 +631,9 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
       if (ct == 0) pstamp(a, blockIdx.x, nj, 1);
       const Tile& t = jb.t;
       const unsigned long long cbase = t.co;                  // chunk offset in the round
-      unsigned char* const out = smem + (size_t)(slot0 % NS) * a.slot_bytes;  // slot 0 = result
-      auto slotp = [&](int o) -> const unsigned char* {
-        return smem + (size_t)((slot0 + o) % NS) * a.slot_bytes;
-      };
+      const uint32_t sbase = smem_u32(smem);
+      const uint32_t out = sbase + (slot0 % NS) * (uint32_t)a.slot_bytes;  // slot 0 = result
+      auto slota = [&](int o) -> uint32_t { return sbase + ((slot0 + o) % NS) * (uint32_t)a.slot_bytes; };
       const bool bb = buf_bulk<DT, W>(a, t);
       if (kind == kS0) {
         // C1: w = to_wire(in) into the slot (then the storer bulk-stores it to win)
@@ -539,9 +651,10 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
               if (direct) {
                 w[u] = load_user<DT, W>(buf, a.buf_off + cbase + el, nrem, a.aligned != 0);
               } else if constexpr (DT != W) {
-                const float4* f = reinterpret_cast<const float4*>(slotp(0) + (size_t)vv * 32);
-                const float4 f0 = f[0], f1 = f[1];
-                const float ff[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+                const uint4 f0 = lds128(slota(0) + vv * 32), f1 = lds128(slota(0) + vv * 32 + 16);
+                const float ff[8] = {__uint_as_float(f0.x), __uint_as_float(f0.y), __uint_as_float(f0.z),
+                                     __uint_as_float(f0.w), __uint_as_float(f1.x), __uint_as_float(f1.y),
+                                     __uint_as_float(f1.z), __uint_as_float(f1.w)};
                 w[u] = pack<W>(ff);
               }
             }
@@ -549,7 +662,7 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               const int vv = v0 + u * kConsumers;
-              if (vv < t.nvec) *reinterpret_cast<uint4*>(out + (size_t)vv * 16) = w[u];
+              if (vv < t.nvec) sts128(out + vv * 16, w[u]);
             }
             if (!direct && DT != W) consumer_bar();
           }
@@ -562,14 +675,14 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int vv = v0 + u * kConsumers;
-            if (vv < t.nvec) unpack<W>(*reinterpret_cast<const uint4*>(slotp(0) + (size_t)vv * 16), acc[u]);
+            if (vv < t.nvec) unpack<W>(lds128(out + vv * 16), acc[u]);
           }
           for (int o = 1; o < nops; ++o) {
             uint4 r[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
               const int vv = v0 + u * kConsumers;
-              if (vv < t.nvec) r[u] = *reinterpret_cast<const uint4*>(slotp(o) + (size_t)vv * 16);
+              if (vv < t.nvec) r[u] = lds128(slota(o) + vv * 16);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -587,7 +700,7 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
             if (vv >= t.nvec) continue;
             if (last_reduce && a.op == 1) acc_mean<W>(acc[u], a.inv_n, N);
             const uint4 o4 = pack<W>(acc[u]);
-            *reinterpret_cast<uint4*>(out + (size_t)vv * 16) = o4;
+            sts128(out + vv * 16, o4);
             if (last_reduce && !bb) {
               const unsigned long long el = t.e0 + (unsigned long long)vv * VE;
               const int nrem = (int)min((unsigned long long)VE, t.nel - (unsigned long long)vv * VE);
@@ -598,7 +711,7 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
       } else if (!bb) {
         // VA / H into a buffer the bulk store cannot take (cast, unaligned, ragged)
         for (int vv = ct; vv < t.nvec; vv += kConsumers) {
-          const uint4 w = *reinterpret_cast<const uint4*>(slotp(0) + (size_t)vv * 16);
+          const uint4 w = lds128(out + vv * 16);
           const unsigned long long el = t.e0 + (unsigned long long)vv * VE;
           const int nrem = (int)min((unsigned long long)VE, t.nel - (unsigned long long)vv * VE);
           store_user<DT, W>(buf, a.buf_off + cbase + el, nrem, w, a.aligned != 0);

@@ -25,14 +25,22 @@ struct PullArgs {
   int op;                        // 0 sum, 1 mean
   float inv_n;                   // f32(1/N)
   int aligned;                   // all user buffers 16-byte aligned
-  int g[5];                      // CTAs per rank of each kind: S0, R, VR, VA, H
+  int g[6];                      // CTAs per rank of each kind: S0, R, VR, VA, H, SIG
   int gsum;
   int nslots, slot_bytes;        // shared-memory ring
   unsigned long long* trace;     // optional [nlocal*gsum][kPullTraceJobs][kPullTraceEv] stamps
-  int fence;                     // publish fence: 0 fence.acq_rel.sys, 1 .gpu, 2 none (measurement only)
+  int fence;                     // publish: 0 fence.acq_rel.sys in the data CTA; 1 .gpu (measurement
+                                 // only); 2 none (measurement only); 3 the data CTA releases at gpu
+                                 // scope to SIG CTAs, which fence at sys scope and raise the flags
+  unsigned long long* pub;       // fence 3: [nlocal * gsum] (epoch << 32 | jobs published) per CTA
   int zc;                        // zero-copy: the peers' user buffers are mapped here (registered,
                                  // dtype == wire, 16-byte aligned on every rank) -- no S0 copy
   char* peer_buf[kMaxRanks];     // zc: every rank's user buffer as mapped in this process
+  // round geometry (SURVEY C3 nested quantum partition), computed on the host per round:
+  unsigned long long g_co[kMaxRanks];    // chunk j: offset in the round (elements)
+  unsigned long long g_cs[kMaxRanks];    // sub-chunk (j, s) at [j * Y + s]: offset inside chunk j
+  unsigned long long g_sl[kMaxRanks];    // sub-chunk (j, s): length (elements)
+  int g_K[kMaxRanks];                    // sub-chunk (j, s): tiles
 };
 constexpr int kPullTraceJobs = 64;  // trace: first 63 jobs of every CTA; slot 63 = CTA start/end
 constexpr int kPullTraceEv = 8;     // stamps per job

@@ -150,11 +150,11 @@ class _CommBase:
 
     def pull_trace(self, max_ctas: int = 1024):
         """Device trace of the last pull-kernel launch (TORUS_TRACE=1): (numpy [ctas, 64, 8]
-        of ns, ctas per rank, CTA split [S0, R, VR, VA, H])."""
+        of ns, ctas per rank, CTA split [S0, R, VR, VA, H, SIG])."""
         import numpy as np
         out = np.zeros((max_ctas, 64, 8), dtype=np.uint64)
         g = ctypes.c_int()
-        kinds = (ctypes.c_int * 5)()
+        kinds = (ctypes.c_int * 6)()
         check(_lib.load().torus_comm_pull_trace(
             self._comm, out.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), out.nbytes,
             ctypes.byref(g), kinds), "torus_comm_pull_trace")

@@ -14,7 +14,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-KINDS = ["S0", "R", "VR", "VA", "H"]
+KINDS = ["S0", "R", "VR", "VA", "H", "SIG"]
 
 
 def free_port():
