@@ -321,7 +321,7 @@ void read_knobs(torus_comm* c) {
   c->pull_tv = (int)env_size("TORUS_PULL_TILE", 0);
   c->pull_slots = (int)env_size("TORUS_PULL_SLOTS", 0);
   c->pull_ctas = (int)env_size("TORUS_PULL_CTAS", 0);
-  c->pull_fence = (int)env_size("TORUS_PULL_FENCE", 0);
+  c->pull_fence = (int)env_size("TORUS_PULL_FENCE", 3);
   c->pull_zc = (int)env_size("TORUS_PULL_ZC", 1);
   if (const char* w = getenv("TORUS_PULL_W"))
     sscanf(w, "%f,%f,%f,%f,%f", &c->pull_w[0], &c->pull_w[1], &c->pull_w[2], &c->pull_w[3], &c->pull_w[4]);

@@ -45,9 +45,15 @@
 namespace torus {
 namespace {
 
-constexpr int kPullThreads = 192;   // warp 0 producer, warp 1 signaler, warps 2..5 consumers
-constexpr int kConsumerWarps = 4;
+#ifndef TORUS_PULL_CW
+#define TORUS_PULL_CW 4
+#endif
+#ifndef TORUS_PULL_U
+#define TORUS_PULL_U 4
+#endif
+constexpr int kConsumerWarps = TORUS_PULL_CW;           // warps 2.. : consumers
 constexpr int kConsumers = kConsumerWarps * 32;
+constexpr int kPullThreads = 64 + kConsumers;           // warp 0 producer, warp 1 storer
 
 // ------------------------------------------------------------------------------------
 // tile geometry (identical on every rank: host and device derive it from n, X, Y, q, TV)
@@ -300,7 +306,7 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
   constexpr int VE = Wire<W>::VE;
   constexpr int SW = kVecBytes / VE;           // bytes per wire element
   constexpr int DB = sizeof(typename Elem<DT>::T);
-  constexpr int U = 4;                         // vectors in flight per consumer thread
+  constexpr int U = TORUS_PULL_U;              // vectors in flight per consumer thread
 
   // ---- which rank, which kind, which CTA of the kind ----
   const int lr = blockIdx.x / a.gsum;
@@ -718,7 +724,8 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
         }
       }
       cs += nops;
-      fence_view_async_smem();  // my shared-memory writes -> the storer's TMA reads
+      if (kind == kR || kind == kVR || (kind == kS0 && (DT != W || !(a.aligned && !ragged(a, t)))))
+        fence_view_async_smem();  // my shared-memory writes -> the storer's TMA reads
       __syncwarp();
       if (lane == 0) atomicAdd(&s_done, 1);
       if (ct == 0) pstamp(a, blockIdx.x, nj, 2);
