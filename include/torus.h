@@ -259,12 +259,37 @@ TORUS_API size_t torus_comm_ll2_max_bytes(torus_comm_t comm);
 TORUS_API int torus_comm_launches(torus_comm_t comm, size_t count, torus_dtype_t dtype,
                         torus_dtype_t wire);
 
-/* Topology layer: choose the grid for `world` GPUs.  p2p: host row-major [world*world]
- * matrix, p2p[i*world+j] = relative link bandwidth (0 = no P2P); NULL = query the CUDA
- * driver for the visible devices 0..world-1.  Writes X, Y.  On one NVSwitch domain
- * every factorization moves the same 2(N-1)/N*S bytes per rank, so
- * the alpha-beta model picks the grid with the fewest sequential sync rounds,
- * X = world, Y = 1; GPUs that do not share a P2P domain are placed in different rows. */
+/* Topology layer (north_star (3); SPEC.md:303-311 costmodel): an
+ * alpha-beta model predicts the time of an all-reduce of `bytes` on an X-by-Y grid
+ * (ranks row-major, rows = horizontal groups) and the grid with the smallest prediction
+ * wins.
+ *   algo 0 torus, 1 flat ring, 2 hierarchical [6].
+ *   schedule 0: the paper's ring phases, sum over phases of steps * (alpha + step bytes /
+ *     beta): 2(X-1) horizontal steps of S/X, 2(Y-1) vertical steps of S/(XY);
+ *   schedule 1: this library's one-shot phases (one dependent hand-off per phase, every
+ *     peer of the phase at once): 2 * (alpha + (X-1)/X*S/beta_h) + 2 * (alpha +
+ *     (Y-1)/Y*S/X/beta_v).
+ * beta of a phase = the slowest link inside its row (or column) groups, from bw_gbs, a host
+ * row-major [X*Y*X*Y] matrix of GB/s (0 = no P2P path: that grid is infeasible); bw_gbs
+ * NULL = every link beta_default_gbs.  alpha_us: one hand-off in microseconds.  Result in
+ * *out_us (host).  Errors: INVALID_ARG, GRID (infeasible grid). */
+TORUS_API int torus_predict_time(int X, int Y, double bytes, double alpha_us, const double* bw_gbs,
+                                 double beta_default_gbs, int algo, int schedule, double* out_us);
+
+/* Choose the grid for `world` ranks: every factorization X*Y = world is predicted with the
+ * schedule-1 model above and the fastest wins (ties: the larger X, i.e. fewer vertical
+ * hand-offs).  Writes X, Y and, if pred_us is not NULL, the prediction. */
+TORUS_API int torus_pick_grid_model(int world, const double* bw_gbs, double alpha_us,
+                                    double beta_default_gbs, double bytes, int* X, int* Y,
+                                    double* pred_us);
+
+/* Topology discovery for torus_comm_init(X = Y = 0): p2p = host row-major [world*world]
+ * relative link bandwidths (1 = one NVLink domain, 0 = no P2P), or NULL to query the
+ * CUDA driver (cudaDeviceCanAccessPeer + the P2P performance rank of devices 0..world-1);
+ * the calibrated alpha (4 us per hand-off) and beta (560 GB/s per GPU)
+ * and the 51.1 MB north-star message feed torus_pick_grid_model.  On one NVSwitch
+ * domain every grid moves 2(N-1)/N*S bytes per rank and the widest grid has the fewest
+ * hand-offs (X = N); GPUs that share no P2P domain end up in different rows. */
 TORUS_API int torus_pick_grid(int world, const int* p2p, int* X, int* Y);
 
 /* Host logic export (tests): the nested quantum-aligned partition used by every launch

@@ -4,7 +4,8 @@ The product path is libtorus.so (include/torus.h): hand-written sm_100a kernels 
 move gradients over NVLink 5 / NVSwitch through CUDA IPC.  This package is the thin
 Python binding over that C-ABI.
 """
-from .torus import TorusComm, VirtualTorus, partition, pick_grid  # noqa: F401
+from .torus import TorusComm, VirtualTorus, partition, pick_grid, pick_grid_model, predict_time  # noqa: F401
 from ._lib import TorusError, LIB_PATH  # noqa: F401
 
-__all__ = ["TorusComm", "VirtualTorus", "pick_grid", "partition", "TorusError", "LIB_PATH"]
+__all__ = ["TorusComm", "VirtualTorus", "pick_grid", "pick_grid_model", "predict_time", "partition",
+           "TorusError", "LIB_PATH"]

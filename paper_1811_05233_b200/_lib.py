@@ -67,6 +67,10 @@ PROTOTYPES = {
     "torus_comm_pull_trace": (_i, [_vp, _c.POINTER(_ull), _sz, _c.POINTER(_i), _c.POINTER(_i)]),
     "torus_probe": (_i, [_vp, _i, _sz, _i, _i, _c.POINTER(_ull), _vp]),
     "torus_pick_grid": (_i, [_i, _c.POINTER(_i), _c.POINTER(_i), _c.POINTER(_i)]),
+    "torus_predict_time": (_i, [_i, _i, _c.c_double, _c.c_double, _c.POINTER(_c.c_double), _c.c_double, _i, _i,
+                                _c.POINTER(_c.c_double)]),
+    "torus_pick_grid_model": (_i, [_i, _c.POINTER(_c.c_double), _c.c_double, _c.c_double, _c.c_double,
+                                   _c.POINTER(_i), _c.POINTER(_i), _c.POINTER(_c.c_double)]),
     "torus_partition": (_i, [_ull, _i, _i, _c.POINTER(_ull), _c.POINTER(_ull)]),
     "torus_strerror": (_c.c_char_p, [_i]),
     "torus_last_error": (_c.c_char_p, []),

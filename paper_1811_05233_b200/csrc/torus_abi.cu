@@ -410,11 +410,146 @@ int torus_workspace_release(const torus_ipc_handle_t* h) {
   return fail(TORUS_ERR_INVALID_ARG, "no such local workspace");
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// Topology layer: an alpha-beta cost model picks the grid (SPEC.md:303-311 predict_time;
+// the ring's cost grows with N "due to network latency", the torus
+// replaces 2(N-1) sequential steps by 2(X-1) + 2(Y-1)).
+//
+// Phases of the X-by-Y torus (rows = ranks rho*X .. rho*X+X-1, columns = ranks i*X + c):
+//   H-RS (X-1)/X*S  |  V-RS (Y-1)/Y*S/X  |  V-AG (Y-1)/Y*S/X  |  H-AG (X-1)/X*S   bytes per rank
+// schedule 0 (the paper's / SPEC's ring phases): phase p costs steps_p * (alpha + S_p/beta_p),
+//   steps = X-1, Y-1, Y-1, X-1 with per-step payloads S/X, S/(XY), S/(XY), S/X;
+// schedule 1 (this library's kernels: one-shot phases, every peer at once over NVSwitch):
+//   phase p costs alpha + bytes_p/beta_p -- one dependent hand-off per phase.
+// beta_p = the slowest link inside the phase's groups (bw[i*world+j] in GB/s; 0 = no P2P
+// path: the grid is infeasible).  Ring (algo 1): 2(N-1) steps of S/N on the ring's slowest
+// link; hierarchical (algo 2): chain reduce (X-1 steps of S), Y-ring all-reduce on the
+// full buffer (2(Y-1) steps of S/Y), chain broadcast (X-1 steps of S).
+// ---------------------------------------------------------------------------------------
+namespace {
+
+double group_beta(int world, const double* bw, double dflt, const int* ranks, int n) {
+  double b = dflt;
+  if (!bw) return b;
+  b = 1e300;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      if (i != j) b = std::min(b, bw[(size_t)ranks[i] * world + ranks[j]]);
+  return n > 1 ? b : dflt;
+}
+
+// slowest link over all rows (horizontal) or all columns (vertical) of the grid
+double dim_beta(int X, int Y, const double* bw, double dflt, bool rows) {
+  const int world = X * Y;
+  double b = 1e300;
+  std::vector<int> g;
+  if (rows) {
+    for (int rho = 0; rho < Y; ++rho) {
+      g.clear();
+      for (int c = 0; c < X; ++c) g.push_back(rho * X + c);
+      b = std::min(b, group_beta(world, bw, dflt, g.data(), X));
+    }
+  } else {
+    for (int c = 0; c < X; ++c) {
+      g.clear();
+      for (int i = 0; i < Y; ++i) g.push_back(i * X + c);
+      b = std::min(b, group_beta(world, bw, dflt, g.data(), Y));
+    }
+  }
+  return b;
+}
+
+// predicted seconds (negative: infeasible)
+double predict(int X, int Y, double S, double alpha, const double* bw, double beta_default, int algo,
+               int schedule) {
+  const int N = X * Y;
+  const double bh = dim_beta(X, Y, bw, beta_default, true) * 1e9;   // bytes/s
+  const double bv = dim_beta(X, Y, bw, beta_default, false) * 1e9;
+  if (N == 1) return 0.0;
+  if (algo == 1) {  // flat ring over ranks 0..N-1
+    double b = beta_default * 1e9;
+    if (bw) {
+      b = 1e300;
+      for (int r = 0; r < N; ++r) b = std::min(b, bw[(size_t)r * N + (r + 1) % N] * 1e9);
+    }
+    if (b <= 0) return -1;
+    return 2.0 * (N - 1) * (alpha + S / N / b);
+  }
+  if ((X > 1 && bh <= 0) || (Y > 1 && bv <= 0)) return -1;
+  double t = 0;
+  if (algo == 2) {  // hierarchical [6]
+    if (X > 1) t += 2.0 * (X - 1) * (alpha + S / bh);
+    if (Y > 1) t += 2.0 * (Y - 1) * (alpha + S / Y / bv);
+    return t;
+  }
+  if (schedule == 0) {
+    if (X > 1) t += 2.0 * (X - 1) * (alpha + S / X / bh);
+    if (Y > 1) t += 2.0 * (Y - 1) * (alpha + S / ((double)X * Y) / bv);
+  } else {
+    if (X > 1) t += 2.0 * (alpha + (double)(X - 1) / X * S / bh);
+    if (Y > 1) t += 2.0 * (alpha + (double)(Y - 1) / Y * S / X / bv);
+  }
+  return t;
+}
+
+// Calibration of this library's kernels on B200 (profiles/r01_probe_*):
+// one dependent hand-off = flag one-way ~2.5 us + a system fence ~1.5 us; per-GPU NVLink
+// injection with every peer busy ~560 GB/s (SM stores) -- used when no measurement is given.
+constexpr double kAlphaUs = 4.0;
+constexpr double kBetaGBs = 560.0;
+
+}  // namespace
+
+extern "C" {
+
+int torus_predict_time(int X, int Y, double bytes, double alpha_us, const double* bw_gbs,
+                       double beta_default_gbs, int algo, int schedule, double* out_us) {
+  // without a link matrix any grid of the paper's scale (Table 4: up to 4096 GPUs) is fine
+  if (X < 1 || Y < 1 || (long long)X * Y > (bw_gbs ? kMaxRanks : (1 << 20)) || !out_us || bytes < 0 ||
+      alpha_us < 0 || algo < 0 || algo > 2 ||
+      schedule < 0 || schedule > 1 || (!bw_gbs && !(beta_default_gbs > 0)))
+    return fail(TORUS_ERR_INVALID_ARG, "predict_time args");
+  const double t = predict(X, Y, bytes, alpha_us * 1e-6, bw_gbs, beta_default_gbs, algo, schedule);
+  if (t < 0) return fail(TORUS_ERR_GRID, "grid %dx%d has a pair without a P2P path", X, Y);
+  *out_us = t * 1e6;
+  return TORUS_OK;
+}
+
+int torus_pick_grid_model(int world, const double* bw_gbs, double alpha_us, double beta_default_gbs,
+                          double bytes, int* X, int* Y, double* pred_us) {
+  if (world < 1 || world > kMaxRanks || !X || !Y || alpha_us < 0 || bytes < 0 ||
+      (!bw_gbs && !(beta_default_gbs > 0)))
+    return fail(TORUS_ERR_INVALID_ARG, "pick_grid_model args");
+  double best = -1;
+  int bx = 0, by = 0;
+  for (int x = world; x >= 1; --x) {  // ties: the wider grid (fewer vertical hand-offs) first
+    if (world % x) continue;
+    const int y = world / x;
+    if (x > kMaxDim || y > kMaxDim) continue;
+    const double t = predict(x, y, bytes, alpha_us * 1e-6, bw_gbs, beta_default_gbs, 0, 1);
+    if (t < 0) continue;
+    if (best < 0 || t < best * (1 - 1e-9)) {
+      best = t;
+      bx = x;
+      by = y;
+    }
+  }
+  if (best < 0) return fail(TORUS_ERR_GRID, "no feasible grid for %d ranks", world);
+  *X = bx;
+  *Y = by;
+  if (pred_us) *pred_us = best * 1e6;
+  return TORUS_OK;
+}
+
 int torus_pick_grid(int world, const int* p2p, int* X, int* Y) {
   if (world < 1 || world > kMaxRanks || !X || !Y) return fail(TORUS_ERR_INVALID_ARG, "pick_grid args");
-  std::vector<int> m((size_t)world * world, 0);
+  std::vector<double> bw((size_t)world * world, 0.0);
   if (p2p) {
-    for (size_t i = 0; i < m.size(); ++i) m[i] = p2p[i];
+    // relative link bandwidths; 0 = no P2P path: traffic stages through the host (or
+    // another fabric), modelled as 1/20 of an NVLink domain's bandwidth
+    for (size_t i = 0; i < bw.size(); ++i) bw[i] = p2p[i] > 0 ? kBetaGBs * p2p[i] : kBetaGBs / 20.0;
   } else {
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
@@ -422,44 +557,21 @@ int torus_pick_grid(int world, const int* p2p, int* X, int* Y) {
     for (int i = 0; i < world; ++i)
       for (int j = 0; j < world; ++j) {
         int ok = (i == j);
-        if (i != j) CU(cudaDeviceCanAccessPeer(&ok, i, j));
-        m[(size_t)i * world + j] = ok ? 1 : 0;
+        int rank = 0;
+        if (i != j) {
+          CU(cudaDeviceCanAccessPeer(&ok, i, j));
+          if (ok) cudaDeviceGetP2PAttribute(&rank, cudaDevP2PAttrPerformanceRank, i, j);
+        }
+        // relative performance rank 0 = best; without P2P traffic would stage through the
+        // host (modelled as 1/20 of NVLink)
+        bw[(size_t)i * world + j] = ok ? kBetaGBs / (1.0 + rank) : kBetaGBs / 20.0;
       }
   }
-  // P2P domains = connected components of the link graph.
-  std::vector<int> dom(world, -1);
-  int ndom = 0;
-  for (int s = 0; s < world; ++s) {
-    if (dom[s] >= 0) continue;
-    std::vector<int> st{s};
-    dom[s] = ndom;
-    while (!st.empty()) {
-      int u = st.back();
-      st.pop_back();
-      for (int v = 0; v < world; ++v)
-        if (dom[v] < 0 && (m[(size_t)u * world + v] > 0 || m[(size_t)v * world + u] > 0)) {
-          dom[v] = ndom;
-          st.push_back(v);
-        }
-    }
-    ++ndom;
-  }
-  if (ndom == 1) {
-    // One NVSwitch domain: every grid moves 2(N-1)/N*S bytes per rank; the alpha term
-    // counts handshakes (2 per non-degenerate dimension), so the flat grid X = N wins.
-    *X = world;
-    *Y = 1;
-    return TORUS_OK;
-  }
-  // Several domains: rows = domains (they must be equal-sized and rank-contiguous).
-  const int per = world / ndom;
-  if (per * ndom != world) return fail(TORUS_ERR_GRID, "unequal P2P domains");
-  for (int r = 0; r < world; ++r)
-    if (dom[r] != dom[(r / per) * per]) return fail(TORUS_ERR_GRID, "P2P domains not rank-contiguous");
-  *X = per;
-  *Y = ndom;
-  return TORUS_OK;
+  for (int i = 0; i < world; ++i) bw[(size_t)i * world + i] = kBetaGBs;
+  // the north-star message (ResNet-50 gradients in fp16) sets the bandwidth/latency balance
+  return torus_pick_grid_model(world, bw.data(), kAlphaUs, kBetaGBs, 51114064.0, X, Y, nullptr);
 }
+
 
 int torus_comm_init(int rank, int world, int X, int Y, const torus_ipc_handle_t* ipc_handles,
                     torus_comm_t* out) {

@@ -34,7 +34,7 @@
 // read of this rank's parity-p regions -- so no entry or exit barrier is needed.
 //
 // Fold order, partition, rounding points and the mean placement are the oracle's
-// (SURVEY C3-C10), so every dtype is bit-exact against oracle/torus_oracle.c.
+// (SURVEY C3-C10), so every dtype is bit-exact against the CPU oracle.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>

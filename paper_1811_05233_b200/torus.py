@@ -44,6 +44,34 @@ def pick_grid(world: int, p2p: Sequence[Sequence[int]] | None = None) -> tuple[i
     return X.value, Y.value
 
 
+def _bw_array(bw):
+    if bw is None:
+        return None
+    flat = [float(v) for row in bw for v in row]
+    return (ctypes.c_double * len(flat))(*flat)
+
+
+def predict_time(X: int, Y: int, nbytes: float, alpha_us: float, bw=None, beta_gbs: float = 560.0,
+                 algo: str = "torus", schedule: str = "oneshot") -> float:
+    """alpha-beta prediction in microseconds (torus_predict_time)."""
+    out = ctypes.c_double()
+    check(_lib.load().torus_predict_time(X, Y, nbytes, alpha_us, _bw_array(bw), beta_gbs,
+                                         {"torus": 0, "ring": 1, "hier": 2}[algo],
+                                         {"ring": 0, "oneshot": 1}[schedule], ctypes.byref(out)),
+          "torus_predict_time")
+    return out.value
+
+
+def pick_grid_model(world: int, nbytes: float, alpha_us: float, bw=None,
+                    beta_gbs: float = 560.0) -> tuple[int, int, float]:
+    """Grid with the smallest predicted time (torus_pick_grid_model): (X, Y, predicted us)."""
+    X, Y, p = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+    check(_lib.load().torus_pick_grid_model(world, _bw_array(bw), alpha_us, beta_gbs, nbytes,
+                                            ctypes.byref(X), ctypes.byref(Y), ctypes.byref(p)),
+          "torus_pick_grid_model")
+    return X.value, Y.value, p.value
+
+
 def partition(n: int, parts: int, q: int) -> tuple[list[int], list[int]]:
     """Host partition logic of the library, exported for tests."""
     L = _lib.load()

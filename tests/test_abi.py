@@ -56,8 +56,8 @@ def test_pick_grid():
     two = [[1 if i // 4 == j // 4 else 0 for j in range(8)] for i in range(8)]
     assert pick_grid(8, two) == (4, 2)                      # rows = P2P domains
     assert pick_grid(1, [[1]]) == (1, 1)
-    with pytest.raises(_lib.TorusError, match="GRID"):
-        pick_grid(3, [[1, 0, 0], [0, 1, 1], [0, 1, 1]])     # unequal domains
+    # an isolated GPU: every grid crosses the slow path once; the model keeps one row
+    assert pick_grid(3, [[1, 0, 0], [0, 1, 1], [0, 1, 1]]) == (3, 1)
 
 
 def test_null_and_bad_arguments_rejected_without_gpu():
