@@ -102,7 +102,7 @@ struct torus_comm {
   NvlsState nvls;                         // NVLS (multicast) variant, NEXT-4
   size_t ll2_max = 0;                     // two-shot LL up to this many wire bytes (N >= 3)
   // ---- knobs, read ONCE at init (they must agree across ranks: torus_comm_config) ----
-  int mode = 0;                           // kModePull (default) / kModePush / kModeTma
+  int mode = 1;                           // kModePush (default) / kModePull / kModeTma
   unsigned long long one_tile_max = 4096; // push kernel: single-tile threshold (vectors)
   unsigned long long mid_tiles = 1;       // push kernel: tiles per slice below it
   int fence_early = 0;                    // push kernel experiment
@@ -112,6 +112,10 @@ struct torus_comm {
   int pull_ctas = 0;                      // pull kernel: CTA budget per rank (0 = all resident)
   int pull_fence = 0;                     // pull kernel publish fence (see PullArgs::fence)
   int pull_zc = 1;                        // pull kernel: zero-copy from registered buffers
+  int check = 0;                          // TORUS_CHECK=1: per-call header check (MISMATCH)
+  int fault = 0;                          // TORUS_FAULT: negative-control fault injection (tests)
+  unsigned delay_ns = 0;                  // TORUS_DELAY_NS: random per-CTA start delay (tests)
+  unsigned call_seq = 0;                  // calls issued (header check sequence number)
   struct Reg {                            // a registered user buffer (torus_register_buffer)
     char* ptr;
     size_t bytes;
@@ -309,8 +313,10 @@ int pick_ctas(int device, int nlocal, int ctas_req) {
 void read_knobs(torus_comm* c) {
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
   const char* k = getenv("TORUS_KERNEL");
-  c->mode = kModePull;
-  if (k && (strcmp(k, "push") == 0 || strcmp(k, "ldg") == 0)) c->mode = kModePush;
+  // default: the push kernel -- faster than the pull kernel at every measured size on 2
+  // and 4 B200s (profiles/r02_sizes_n*.jsonl); TORUS_KERNEL=pull selects the pull kernel
+  c->mode = kModePush;
+  if (k && strcmp(k, "pull") == 0) c->mode = kModePull;
   if (k && strcmp(k, "tma") == 0) c->mode = kModeTma;
   c->tma = c->mode == kModeTma;
   c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // push kernel; 0 = auto (T ~ 3 tiles per slice)
@@ -323,6 +329,9 @@ void read_knobs(torus_comm* c) {
   c->pull_ctas = (int)env_size("TORUS_PULL_CTAS", 0);
   c->pull_fence = (int)env_size("TORUS_PULL_FENCE", 3);
   c->pull_zc = (int)env_size("TORUS_PULL_ZC", 1);
+  c->check = (int)env_size("TORUS_CHECK", 0);
+  c->fault = (int)env_size("TORUS_FAULT", 0);
+  c->delay_ns = (unsigned)env_size("TORUS_DELAY_NS", 0);
   if (const char* w = getenv("TORUS_PULL_W"))
     sscanf(w, "%f,%f,%f,%f,%f", &c->pull_w[0], &c->pull_w[1], &c->pull_w[2], &c->pull_w[3], &c->pull_w[4]);
   c->ll2_max = ll2_max_env(c->world);
@@ -1011,6 +1020,8 @@ int launch_pull_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype
     a.fl_pres = a.fl_c + (unsigned long long)X * Y * a.Kmax;
     a.trace = c->d_pull_trace;
     a.fence = c->pull_fence;
+    a.fault = c->fault;
+    a.delay_ns = c->delay_ns;
     cudaError_t e = launch_pull(a, dtype, wire, c->virt, stream);
     if (e != cudaSuccess) return cuda_fail(e, "pull kernel launch");
   }
@@ -1041,6 +1052,17 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   if (count > (size_t)1 << 48) return fail(TORUS_ERR_INVALID_ARG, "count overflow");
   const int route = plan_route(c, count, dtype, wire);
   if (route == kRouteNone) return TORUS_OK;  // sum/mean over one rank of wire values: identity
+  if (c->check && c->world > 1) {
+    // per-call header: every rank must make the same call
+    unsigned desc = 2166136261u;
+    const unsigned long long fields[] = {count, (unsigned long long)dtype, (unsigned long long)wire,
+                                         (unsigned long long)op, (unsigned long long)route};
+    for (unsigned long long f : fields)
+      for (int i = 0; i < 8; ++i) desc = (desc ^ (unsigned)((f >> (8 * i)) & 0xff)) * 16777619u;
+    cudaError_t e = launch_check(c->d_ranks, c->nlocal, c->layout.bar_off + 16384, ++c->call_seq, desc,
+                                 c->timeout_ns, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "header check launch");
+  }
   if (route == kRouteCast) {
     cudaError_t e = launch_castscale(bufs[0], count, dtype, wire, stream);
     return e == cudaSuccess ? TORUS_OK : cuda_fail(e, "castscale launch");

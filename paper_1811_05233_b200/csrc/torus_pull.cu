@@ -342,6 +342,14 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
     a.trace[((size_t)blockIdx.x * kPullTraceJobs + kPullTraceJobs - 1) * kPullTraceEv] = gtimer();
   const uint32_t epoch = s_epoch;
   const uint32_t v = epoch + 1u;               // flag value of this call
+  if (a.delay_ns) {  // robustness runs: start every CTA after a pseudo-random delay
+    uint32_t h = (uint32_t)(me * 7919 + blockIdx.x * 104729) ^ (epoch * 2654435761u);
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    const unsigned long long until = gtimer() + (h % a.delay_ns);
+    while (gtimer() < until) __nanosleep(256);
+  }
   const int par = (int)(epoch & 1u);
   char* const myws = R->ws[me];
   uint32_t* const myflags = reinterpret_cast<uint32_t*>(myws + a.flag_off);
@@ -401,8 +409,8 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
       if (!live) break;
       if (!work) {
         __nanosleep(64);
-        if ((++spin & 255u) == 0 && (gtimer() > deadline || *(volatile int*)&s_abort)) {
-          atomicExch_system(R->err, kErrTimeout);
+        if ((++spin & 255u) == 0 && (gtimer() > deadline || *(volatile int*)&s_abort || *(volatile int*)R->err)) {
+          atomicCAS_system(R->err, 0, kErrTimeout);
           break;
         }
         continue;
@@ -446,7 +454,8 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
         unsigned spin = 0;
         while ((int32_t)(ld_relaxed_sys(f) - v) < 0) {
           __nanosleep(32);
-          if ((++spin & 255u) == 0 && (gtimer() > deadline || *(volatile int*)&s_abort)) {
+          if ((++spin & 255u) == 0 &&
+              (gtimer() > deadline || *(volatile int*)&s_abort || *(volatile int*)R->err)) {
             ok = false;
             return;
           }
@@ -468,8 +477,9 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
             }
           }
         } else if (kind == kVR) {
+          const bool skip = (a.fault == 2 && me == 0 && b == 0 && nj == 0);  // negative control
           for (int i = 0; i < Y; ++i) {
-            if (X > 1) need(fl_p1(a, i, jb.k));
+            if (X > 1) { if (!skip) need(fl_p1(a, i, jb.k)); }
             else if (input_from_buf<DT, W>(a, jb.t, i == rho)) { if (i != rho) need(a.fl_pres + i * X); }
             else need(fl_win(a, Y, i, 0, jb.k));
           }
@@ -515,7 +525,7 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
         }
       }
       if (!ok) {
-        atomicExch_system(R->err, kErrTimeout);
+        atomicCAS_system(R->err, 0, kErrTimeout);  // keep an earlier MISMATCH
         s_abort = 1;
       }
       if (presence && ok) {
@@ -524,12 +534,12 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
           unsigned spin = 0;
           while (ok && (int32_t)(ld_relaxed_sys(f) - v) < 0) {
             __nanosleep(64);
-            if ((++spin & 255u) == 0 && gtimer() > deadline) ok = false;
+            if ((++spin & 255u) == 0 && (gtimer() > deadline || *(volatile int*)R->err)) ok = false;
           }
         };
         for (int jj = 1; jj < X; ++jj) seen(rho * X + (c + jj) % X);
         for (int ii = 1; ii < Y; ++ii) seen(((rho + ii) % Y) * X + c);
-        if (!ok) atomicExch_system(R->err, kErrTimeout);
+        if (!ok) atomicCAS_system(R->err, 0, kErrTimeout);
       }
     }
   } else if (warp == 1) {
@@ -705,7 +715,8 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
             const int vv = v0 + u * kConsumers;
             if (vv >= t.nvec) continue;
             if (last_reduce && a.op == 1) acc_mean<W>(acc[u], a.inv_n, N);
-            const uint4 o4 = pack<W>(acc[u]);
+            uint4 o4 = pack<W>(acc[u]);
+            if (a.fault == 1 && me == 0 && b == 0 && nj == 0 && vv == 0) o4.x ^= 1u;  // negative control
             sts128(out + vv * 16, o4);
             if (last_reduce && !bb) {
               const unsigned long long el = t.e0 + (unsigned long long)vv * VE;
@@ -745,6 +756,37 @@ __global__ void __launch_bounds__(kPullThreads) torus_pull_kernel(const PullArgs
       if (!s_abort) {
         __threadfence();
         st_release_gpu(R->pull_ctr, epoch + 1u);
+      }
+    }
+  }
+}
+
+// Per-call header check: slot [parity][src] of u64 (seq << 32 | desc) in every rank's
+// barrier region.  Double-buffered by call parity: a rank writes slot seq & 1 of call seq + 2
+// only after it saw every peer's header of call seq + 1, i.e. after they read seq's.
+__global__ void check_kernel(const RankDev* ranks, unsigned long long hdr_off, unsigned seq, unsigned desc,
+                             unsigned long long timeout_ns) {
+  const RankDev* R = ranks + blockIdx.x;
+  const int t = threadIdx.x, N = R->N, me = R->rank, par = (int)(seq & 1u);
+  const unsigned long long word = ((unsigned long long)seq << 32) | desc;
+  auto slot = [&](int rank, int src) -> unsigned long long* {
+    return reinterpret_cast<unsigned long long*>(R->ws[rank] + hdr_off) + par * kMaxRanks + src;
+  };
+  if (t < N && t != me) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot(t, me)), "l"(word) : "memory");
+    const unsigned long long* f = slot(me, t);
+    const unsigned long long deadline = gtimer() + timeout_ns;
+    unsigned it = 0;
+    while (true) {
+      unsigned long long w;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(f) : "memory");
+      if ((unsigned)(w >> 32) == seq) {
+        if ((unsigned)w != desc) atomicExch_system(R->err, 7 /* TORUS_ERR_MISMATCH */);
+        break;
+      }
+      if ((++it & 255u) == 0 && gtimer() > deadline) {
+        atomicCAS_system(R->err, 0, kErrTimeout);
+        break;
       }
     }
   }
@@ -798,6 +840,16 @@ cudaError_t launch_pull(const PullArgs& a, int dtype, int wire, bool cooperative
     return launch_pull_typed<DT_F32, DT_BF16>(a, cooperative, stream);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_check(const RankDev* ranks, int nlocal, unsigned long long hdr_off, unsigned seq,
+                         unsigned desc, unsigned long long timeout_ns, cudaStream_t stream) {
+  if (nlocal > 1) {
+    void* args[] = {const_cast<RankDev**>(&ranks), &hdr_off, &seq, &desc, &timeout_ns};
+    return cudaLaunchCooperativeKernel((const void*)check_kernel, dim3(nlocal), dim3(kMaxRanks), args, 0, stream);
+  }
+  check_kernel<<<1, kMaxRanks, 0, stream>>>(ranks, hdr_off, seq, desc, timeout_ns);
+  return cudaGetLastError();
 }
 
 int pull_ctas_per_sm(size_t smem) {

@@ -33,6 +33,9 @@ struct PullArgs {
                                  // only); 2 none (measurement only); 3 the data CTA releases at gpu
                                  // scope to SIG CTAs, which fence at sys scope and raise the flags
   unsigned long long* pub;       // fence 3: [nlocal * gsum] (epoch << 32 | jobs published) per CTA
+  int fault;                     // negative controls (tests only): 1 corrupt one reduced element,
+                                 // 2 skip one P1 wait (read before the peer wrote); 0 off
+  unsigned delay_ns;             // robustness: each CTA starts after a pseudo-random delay < this
   int zc;                        // zero-copy: the peers' user buffers are mapped here (registered,
                                  // dtype == wire, 16-byte aligned on every rank) -- no S0 copy
   char* peer_buf[kMaxRanks];     // zc: every rank's user buffer as mapped in this process
@@ -50,6 +53,10 @@ inline size_t pull_smem_bytes(int nslots, int slot_bytes) {
 constexpr size_t kPullFlagBytes = 8ull << 20;  // pull flag region per slab
 
 cudaError_t launch_pull(const PullArgs& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
+// per-call header check (TORUS_CHECK=1): every rank posts a descriptor of the call
+// (count, dtype, wire, op, route) to its peers and compares theirs with its own
+cudaError_t launch_check(const RankDev* ranks, int nlocal, unsigned long long hdr_off, unsigned seq,
+                         unsigned desc, unsigned long long timeout_ns, cudaStream_t stream);
 int pull_ctas_per_sm(size_t smem);
 
 }  // namespace torus

@@ -102,6 +102,16 @@ def handles_array(blobs: Sequence[bytes]):
     return arr
 
 
+def config_disagreement(cfg, world: int, group=None) -> list:
+    """All-gather every rank's configuration fingerprint; ranks that differ from rank 0."""
+    if world == 1:
+        return []
+    import torch.distributed as dist
+    cfgs: list = [None] * world
+    dist.all_gather_object(cfgs, tuple(cfg), group=group)
+    return [r for r, c in enumerate(cfgs) if c != cfgs[0]]
+
+
 def agree_status(rc: int, msg: str, world: int, group=None) -> list:
     """Every rank learns every rank's init status; returns [(rank, (rc, msg))] failures."""
     if world == 1:
@@ -239,11 +249,20 @@ class TorusComm(_CommBase):
         bad = agree_status(rc, msg, world, group)
         if bad:
             if rc == 0:
-                L.torus_comm_destroy(comm)  # peers failed: no collective barrier possible
+                L.torus_comm_abort(comm)  # peers failed: no collective barrier possible
             else:
                 L.torus_workspace_release(ctypes.byref(h))
             raise RuntimeError(f"torus_comm_init failed on ranks {bad}")
-        return cls(comm, rank, world, dev)
+        self = cls(comm, rank, world, dev)
+        # every knob that decides which bytes and flags a call touches must agree across
+        # ranks: all-gather the library's configuration fingerprint
+        diff = config_disagreement(self.config(), world, group)
+        if diff:
+            L.torus_comm_abort(comm)
+            self._comm = None
+            raise _lib.TorusError(7, f"torus_comm_init: configuration differs on ranks {diff} "
+                                     "(TORUS_* environment or CTA budget)")
+        return self
 
     def all_reduce(self, t: torch.Tensor, op: str = "mean", wire: torch.dtype | None = None,
                    stream: torch.cuda.Stream | None = None) -> torch.Tensor:

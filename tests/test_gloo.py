@@ -45,6 +45,11 @@ def _worker(rank, world, port, errfile):
         # rank 1 fails: every rank sees the failure (nobody keeps a half-built comm)
         bad = torus.agree_status(5 if rank == 1 else 0, "TORUS_ERR_PEER" if rank == 1 else "", world)
         assert [r for r, _ in bad] == [1] and bad[0][1][0] == 5
+        # configuration fingerprints: equal -> [], rank 1 differs -> [1] everywhere
+        cfg = (2, 2, 1, 148, 512 << 20, 0)
+        assert torus.config_disagreement(cfg, world) == []
+        other = cfg if rank == 0 else cfg[:3] + (74,) + cfg[4:]
+        assert torus.config_disagreement(other, world) == [1]
         dist.barrier()
         dist.destroy_process_group()
     except Exception:

@@ -281,3 +281,106 @@ def test_nvls_variant_tolerance(tmp_path, world):
         mp.spawn(_nvls_worker, args=(world, _free_port(), errfile), nprocs=world, join=True)
     except Exception as e:
         raise AssertionError(open(errfile).read() if os.path.exists(errfile) else str(e)) from None
+
+
+def _mismatch_worker(rank, world, port, errfile):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    try:
+        import time
+        import torch.distributed as dist
+        from paper_1811_05233_b200 import TorusComm
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), TORUS_CHECK="1",
+                          TORUS_TIMEOUT_MS="20000")
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        comm = TorusComm.init(X=world, Y=1)
+        D = 1_000_000 + 8 * rank  # the ranks disagree on the count
+        t = torch.ones(D, dtype=torch.float16, device=f"cuda:{rank}")
+        dist.barrier()
+        t0 = time.time()
+        comm.all_reduce(t, op="sum")
+        torch.cuda.synchronize()
+        dt = time.time() - t0
+        err = comm.async_error()
+        assert err == 7, f"rank {rank}: async error {err}, expected TORUS_ERR_MISMATCH (7)"
+        assert dt < 10.0, f"rank {rank}: took {dt:.1f} s (the check should abort, not time out)"
+        dist.barrier()
+        comm.destroy()  # poisoned comm: no collective barrier, resources freed
+        dist.destroy_process_group()
+    except Exception:
+        with open(errfile, "a") as f:
+            f.write(f"rank {rank}:\n{traceback.format_exc()}\n")
+        raise
+
+
+def test_header_check_detects_mismatch(tmp_path):
+    """with TORUS_CHECK=1, ranks that disagree on the call
+    (here the count) get TORUS_ERR_MISMATCH asynchronously instead of hanging."""
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    errfile = str(tmp_path / "errors.txt")
+    try:
+        mp.spawn(_mismatch_worker, args=(2, _free_port(), errfile), nprocs=2, join=True)
+    except Exception as e:
+        raise AssertionError(open(errfile).read() if os.path.exists(errfile) else str(e)) from None
+
+
+def _stream_worker(rank, world, port, errfile, X, Y):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    try:
+        import torch.distributed as dist
+
+        import oracle
+        import synthetic
+        from paper_1811_05233_b200 import TorusComm
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        comm = TorusComm.init(X=X, Y=Y)
+        R16 = comm.round_elems(torch.float16)
+        # every routing threshold (one-shot, two-shot, multi-phase) and a multi-round call,
+        # back to back on one stream, no host synchronization in between (ADVICE r1)
+        sizes = [5, comm.ll_max_bytes() // 2, comm.ll_max_bytes() // 2 + 8, 3_000_001, 8, 25_557_032,
+                 1_000, R16 + 12_345, 77, 9_000_000]
+        sizes = [s for s in sizes if s > 0]
+        ins = [synthetic.make_all("normal", D, world, "f16", salt=90 + k) for k, D in enumerate(sizes)]
+        ts = [torch.from_numpy(a[rank].copy()).to(f"cuda:{rank}") for a in ins]
+        torch.cuda.synchronize()
+        dist.barrier()
+        for t in ts:
+            comm.all_reduce(t, op="mean")
+        torch.cuda.synchronize()
+        assert comm.async_error() == 0
+        for k, (t, a) in enumerate(zip(ts, ins)):
+            D = a[0].size
+            if D > 3_000_000:
+                g = np.random.Generator(np.random.PCG64(k))
+                idx = np.unique(np.concatenate([g.integers(0, D, 2000), [0, D - 1]]))
+                ref = oracle.torus_elements(a, X, Y, idx, "f16", op="mean", q=8, round_elems=R16)
+                ok, nbad = _same(t.cpu().numpy()[idx], ref)
+            else:
+                ref = oracle.torus_allreduce(a, X, Y, "f16", op="mean", q=8, round_elems=R16)[rank]
+                ok, nbad = _same(t.cpu().numpy(), ref)
+            assert ok, f"rank {rank} call {k} D={D} ({comm.route(D, torch.float16)}): {nbad} mismatches"
+        dist.barrier()
+        comm.destroy()
+        dist.destroy_process_group()
+    except Exception:
+        with open(errfile, "a") as f:
+            f.write(f"rank {rank}:\n{traceback.format_exc()}\n")
+        raise
+
+
+@pytest.mark.parametrize("world,X,Y", [(2, 1, 2), (2, 2, 1), (4, 2, 2)])
+def test_back_to_back_calls_across_routes(tmp_path, world, X, Y):
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    errfile = str(tmp_path / "errors.txt")
+    try:
+        mp.spawn(_stream_worker, args=(world, _free_port(), errfile, X, Y), nprocs=world, join=True)
+    except Exception as e:
+        raise AssertionError(open(errfile).read() if os.path.exists(errfile) else str(e)) from None

@@ -80,7 +80,7 @@ def make_vt(X, Y, ws=0, kernel="pull", ll=None):
     is built; the multi-phase variants run with the one-shot path off (ll=0)."""
     import os
     from paper_1811_05233_b200 import VirtualTorus
-    env = {"TORUS_KERNEL": {"tma": "tma", "ldg": "push", "ldgt": "push"}.get(kernel, "pull"),
+    env = {"TORUS_KERNEL": {"tma": "tma", "ldg": "push", "ldgt": "push", "pull": "pull"}.get(kernel, "push"),
            "TORUS_TILE": "256" if kernel == "ldgt" else "0",
            "TORUS_LL_MAX_BYTES": str(ll if ll is not None else (LL_FORCED if kernel == "ll" else 0)),
            "TORUS_LL2_MAX_BYTES": str(LL_FORCED if kernel == "ll2" else 0)}
@@ -420,5 +420,94 @@ def test_cuda_graph_capture_and_replay():
                 ref = oracle.torus_allreduce(arrs, X, Y, "f16", op="mean", q=8, round_elems=R)
                 for r in range(N):
                     assert_same(from_dev(ts[r], "f16"), ref[r], f"graph replay {rep} D={D} rank {r}")
+    finally:
+        vt.destroy()
+
+
+def _vt_env(X, Y, env, ws=0):
+    import os
+    from paper_1811_05233_b200 import VirtualTorus
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
+    try:
+        return VirtualTorus(X, Y, device=0, ws_bytes=ws)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+PULL_ONLY = {"TORUS_KERNEL": "pull", "TORUS_LL_MAX_BYTES": 0, "TORUS_LL2_MAX_BYTES": 0}
+
+
+@pytest.mark.parametrize("zc", [0, 1])
+@pytest.mark.parametrize("fence", [0, 3])
+@pytest.mark.parametrize("X,Y", [(2, 2), (2, 4), (1, 4), (4, 1)])
+def test_pull_variants_bit_exact(X, Y, zc, fence):
+    """The pull kernel with and without zero-copy (S0 pre-pass copy), with the publishing
+    fence in the data CTA (0) or in SIG CTAs (3): bit-exact vs the oracle, several calls
+    in a row (parity double-buffering), a ragged length and a multi-tile one."""
+    vt = _vt_env(X, Y, {**PULL_ONLY, "TORUS_PULL_ZC": zc, "TORUS_PULL_FENCE": fence})
+    try:
+        N = X * Y
+        for it, (dt, D) in enumerate((("f16", 300_007), ("f32", 123_457), ("bf16", 1_000_003), ("f16", 8))):
+            ins = synthetic.make_all("normal", D, N, dt, salt=20 + it)
+            got = run_virtual(vt, ins, dt, dt, "mean")
+            ref = oracle.torus_allreduce(ins, X, Y, dt, op="mean", q=q_of(dt), round_elems=vt.round_elems(TD[dt]))
+            for r in range(N):
+                assert_same(got[r], ref[r], f"pull zc={zc} fence={fence} {X}x{Y} {dt} D={D} rank {r}")
+    finally:
+        vt.destroy()
+
+
+def test_pull_random_start_delays_bit_exact():
+    """random per-rank (here per-CTA, up to 50 us) start delays leave the
+    result unchanged -- the flag protocol, not timing, orders every hand-off."""
+    X, Y = 2, 4
+    vt = _vt_env(X, Y, {**PULL_ONLY, "TORUS_DELAY_NS": 50_000})
+    try:
+        for it in range(3):
+            ins = synthetic.make_all("wide", 400_009, 8, "f32", salt=40 + it)
+            got = run_virtual(vt, ins, "f32", "f32", "sum")
+            ref = oracle.torus_allreduce(ins, X, Y, "f32", op="sum", q=4, round_elems=vt.round_elems(torch.float32))
+            for r in range(8):
+                assert_same(got[r], ref[r], f"delayed call {it} rank {r}")
+    finally:
+        vt.destroy()
+
+
+@pytest.mark.parametrize("fault", [1, 2])
+def test_fault_injection_is_caught(fault):
+    """SPEC.md:509 negative control: with one reduced element corrupted (1) or one P1 wait
+    skipped so a peer's slot is read before it is written (2), parity vs the oracle FAILS
+    -- the parity tests have teeth.  Without injection the same calls are bit-exact."""
+    X, Y, D = 2, 2, 600_000
+    bad_calls = 0
+    vt = _vt_env(X, Y, {**PULL_ONLY, "TORUS_FAULT": fault})
+    try:
+        for it in range(3):
+            ins = synthetic.make_all("normal", D, 4, "f16", salt=60 + it)
+            got = run_virtual(vt, ins, "f16", "f16", "sum")
+            ref = oracle.torus_allreduce(ins, X, Y, "f16", op="sum", q=8, round_elems=vt.round_elems(torch.float16))
+            if any(not np.array_equal(got[r].view(np.uint16), ref[r].view(np.uint16)) for r in range(4)):
+                bad_calls += 1
+    finally:
+        vt.destroy()
+    assert bad_calls >= 1, "fault injection went undetected"
+
+
+def test_header_check_consistent_calls():
+    """TORUS_CHECK=1: the per-call header agrees on consistent calls (no false MISMATCH)."""
+    vt = _vt_env(2, 2, {**PULL_ONLY, "TORUS_CHECK": 1})
+    try:
+        for D in (1000, 300_000, 7):
+            ins = synthetic.make_all("normal", D, 4, "f16", salt=D % 11)
+            got = run_virtual(vt, ins, "f16", "f16", "mean")
+            ref = oracle.torus_allreduce(ins, 2, 2, "f16", op="mean", q=8, round_elems=vt.round_elems(torch.float16))
+            for r in range(4):
+                assert_same(got[r], ref[r], f"checked D={D} rank {r}")
+        assert vt.async_error() == 0
     finally:
         vt.destroy()
