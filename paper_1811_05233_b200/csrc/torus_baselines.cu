@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(512) probe_kernel(const RankDev* ranks, unsign
       }
       if (me == 1 && ok) st_release_sys(theirs, base + i);
     }
-    if (!ok) atomicExch_system(R->err, kErrTimeout);
+    if (!ok) atomicCAS_system(R->err, 0, kErrTimeout);
     if (out) out[0] = ok ? gtimer() - t0 : 0;
     return;
   }
@@ -230,8 +230,8 @@ __global__ void __launch_bounds__(512, 1) ring_kernel(const LaunchArgs a) {
     return ws + a.hin_off + ((size_t)kind * (N - 1) + step) * slot_bytes;
   };
   auto wait_prev = [&](int kind, int step) -> bool {
-    if (tid == 0 && !wait_flag_ge(flag(myws, kind, step), e, deadline)) {
-      atomicExch_system(R->err, kErrTimeout);
+    if (tid == 0 && !wait_flag_ge(flag(myws, kind, step), e, deadline, 64, R->err)) {
+      atomicCAS_system(R->err, 0, kErrTimeout);
       s_abort = 1;
     }
     __syncthreads();
@@ -439,8 +439,8 @@ __global__ void __launch_bounds__(512, 1) hier_kernel(const LaunchArgs a) {
     return reinterpret_cast<uint32_t*>(ws) + ((size_t)(kind * kMaxDim + step) * G + b);
   };
   auto wait_in = [&](int kind, int step) -> bool {
-    if (tid == 0 && !wait_flag_ge(flag(myws, kind, step), e, deadline)) {
-      atomicExch_system(R->err, kErrTimeout);
+    if (tid == 0 && !wait_flag_ge(flag(myws, kind, step), e, deadline, 64, R->err)) {
+      atomicCAS_system(R->err, 0, kErrTimeout);
       s_abort = 1;
     }
     __syncthreads();

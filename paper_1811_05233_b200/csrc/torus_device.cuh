@@ -59,12 +59,17 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // Wait until *f >= v (wrap-safe).  Spin with relaxed loads and a short sleep -- a hot
 // loop of ld.acquire.sys (each one an L1 invalidate) slows every fence on the SM -- and
 // take the acquire once the value is there.  Returns false once `deadline` passes.
+// An error already posted on the comm's async error word (a peer's MISMATCH or timeout)
+// also ends the wait.
 __device__ __forceinline__ bool wait_flag_ge(const uint32_t* f, uint32_t v, unsigned long long deadline,
-                                             unsigned sleep_ns = 64) {
+                                             unsigned sleep_ns = 64, const int* err = nullptr) {
   unsigned spin = 0;
   while ((int32_t)(ld_relaxed_sys(f) - v) < 0) {
     if (sleep_ns) __nanosleep(sleep_ns);
-    if ((++spin & 63u) == 0 && gtimer() > deadline) return false;
+    if ((++spin & 63u) == 0) {
+      if (gtimer() > deadline) return false;
+      if (err && (spin & 1023u) == 0 && *(volatile const int*)err) return false;  // host memory: rarely
+    }
   }
   (void)ld_acquire_sys(f);
   return true;

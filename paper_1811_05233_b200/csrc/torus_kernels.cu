@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
         const int t = it - SD * p;
         if (t < 0 || t >= T) continue;
         for_flags(kinds[p], t, true, [&](uint32_t* f, uint32_t v) {
-          if ((e++ & 31) == lane && ok) ok = wait_flag_ge(f, v, deadline, a.poll_sleep);
+          if ((e++ & 31) == lane && ok) ok = wait_flag_ge(f, v, deadline, a.poll_sleep, R->err);
         });
       }
       return __all_sync(0xffffffffu, ok);
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
       stamp(tr, b, it, 2);
       if (!ok) {
         if (lane == 0) {
-          atomicExch_system(R->err, kErrTimeout);
+          atomicCAS_system(R->err, 0, kErrTimeout);
           s_abort = 1;
         }
         __syncwarp();
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
       if (!fresh) {
         __nanosleep(64);
         if (gtimer() > deadline) {
-          atomicExch_system(R->err, kErrTimeout);
+          atomicCAS_system(R->err, 0, kErrTimeout);
           ok = false;
           break;
         }
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
         const int t = it - 2 * pp;
         if (t < 0 || t >= T) continue;
         for_flags(kinds[pp], t, true, [&](uint32_t* f, uint32_t v) {
-          if ((e++ & 31) == lane && ok) ok = wait_flag_ge(f, v, deadline);
+          if ((e++ & 31) == lane && ok) ok = wait_flag_ge(f, v, deadline, 64, R->err);
         });
       }
       return __all_sync(0xffffffffu, ok);
@@ -762,7 +762,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
         stamp(tr, b, it, 0);
         if (!poll_iter(it)) {  // watchdog: poison; the producer walks the rest without loads
           if (lane == 0) {
-            atomicExch_system(R->err, kErrTimeout);
+            atomicCAS_system(R->err, 0, kErrTimeout);
             s_abort = 1;
             st_release_cta(&s_ready, iters);
           }
@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
         // my own stores of iteration it-2 (stage B's local v_in slot, read by stage C)
         if (it >= 2 && !wait_done(it - 2)) {
           if (lane == 0) {
-            atomicExch_system(R->err, kErrTimeout);
+            atomicCAS_system(R->err, 0, kErrTimeout);
             s_abort = 1;
             st_release_cta(&s_ready, iters);
           }
@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
       for (int it = 0; it < iters; ++it) {
         if (!wait_done(it)) {
           if (lane == 0) {
-            atomicExch_system(R->err, kErrTimeout);
+            atomicCAS_system(R->err, 0, kErrTimeout);
             s_abort = 1;
           }
           __syncwarp();
@@ -1008,7 +1008,7 @@ __global__ void __launch_bounds__(kThreads, 1) torus_tma_kernel(const LaunchArgs
     while ((int32_t)(ld_acquire_gpu(ack) - (seq + (uint32_t)T)) < 0) {
       __nanosleep(64);
       if (gtimer() > deadline) {
-        atomicExch_system(R->err, kErrTimeout);
+        atomicCAS_system(R->err, 0, kErrTimeout);
         ok = false;
         break;
       }
@@ -1059,7 +1059,7 @@ __global__ void barrier_kernel(const RankDev* ranks, unsigned long long bar_off,
     unsigned it = 0;
     while ((int32_t)(ld_acquire_sys(f) - e) < 0) {
       if ((++it & 255u) == 0 && gtimer() > deadline) {
-        atomicExch_system(R->err, kErrTimeout);
+        atomicCAS_system(R->err, 0, kErrTimeout);
         break;
       }
     }

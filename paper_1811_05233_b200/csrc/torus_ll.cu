@@ -36,7 +36,7 @@ __device__ __forceinline__ void st_ll(char* p, uint32_t d0, uint32_t d1, uint32_
 
 // Spin until both 8-byte words of the line carry `flag`; returns false on the deadline.
 __device__ __forceinline__ bool ld_ll(const char* p, uint32_t flag, unsigned long long deadline,
-                                      uint32_t* d0, uint32_t* d1) {
+                                      uint32_t* d0, uint32_t* d1, const int* err) {
   unsigned spin = 0;
   for (;;) {
     unsigned long long a, b;
@@ -46,7 +46,11 @@ __device__ __forceinline__ bool ld_ll(const char* p, uint32_t flag, unsigned lon
       *d1 = (uint32_t)b;
       return true;
     }
-    if ((++spin & 255u) == 0 && gtimer() > deadline) return false;
+    if ((++spin & 255u) == 0) {
+      if (gtimer() > deadline) return false;
+      // the error word is host memory: look at it rarely (every 4096 spins)
+      if ((spin & 4095u) == 0 && *(volatile const int*)err) return false;
+    }
   }
 }
 
@@ -110,8 +114,8 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const LaunchArgs a) {
         uint4 w = own;
         if (r != me) {
           const char* src = slot(me, r);
-          ok = ld_ll(src + j * 16, flag, deadline, &w.x, &w.y) &&
-               ld_ll(src + half + j * 16, flag, deadline, &w.z, &w.w);
+          ok = ld_ll(src + j * 16, flag, deadline, &w.x, &w.y, R->err) &&
+               ld_ll(src + half + j * 16, flag, deadline, &w.z, &w.w, R->err);
           if (!ok) break;
         }
         if (kc == 1) unpack<W>(w, P);
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(kLLThreads) ll_kernel(const LaunchArgs a) {
       store_user<DT, W>(buf, a.buf_off + e, nrem, pack<W>(V), a.aligned);
     }
   }
-  if (!ok) atomicExch_system(R->err, kErrTimeout);
+  if (!ok) atomicCAS_system(R->err, 0, kErrTimeout);
 
   // 3. the last CTA of this rank to finish advances the epoch (every CTA read it above)
   __syncthreads();
@@ -230,8 +234,8 @@ __global__ void __launch_bounds__(kLLThreads) ll2_kernel(const LaunchArgs a) {
         uint4 w = own;
         if (r != me) {
           const char* src = rs(me, r);
-          ok = ld_ll(src + v * 16, flag, deadline, &w.x, &w.y) &&
-               ld_ll(src + half + v * 16, flag, deadline, &w.z, &w.w);
+          ok = ld_ll(src + v * 16, flag, deadline, &w.x, &w.y, R->err) &&
+               ld_ll(src + half + v * 16, flag, deadline, &w.z, &w.w, R->err);
           if (!ok) break;
         }
         if (kc == 1) unpack<W>(w, P);
@@ -272,13 +276,13 @@ __global__ void __launch_bounds__(kLLThreads) ll2_kernel(const LaunchArgs a) {
     if (o == me) continue;
     uint4 w;
     const char* src = ag(me, o);
-    ok = ld_ll(src + v * 16, flag, deadline, &w.x, &w.y) &&
-         ld_ll(src + half + v * 16, flag, deadline, &w.z, &w.w);
+    ok = ld_ll(src + v * 16, flag, deadline, &w.x, &w.y, R->err) &&
+         ld_ll(src + half + v * 16, flag, deadline, &w.z, &w.w, R->err);
     if (!ok) break;
     const int nrem = (int)(n - e < (unsigned long long)VE ? n - e : VE);
     store_user<DT, W>(buf, a.buf_off + e, nrem, w, a.aligned);
   }
-  if (!ok) atomicExch_system(R->err, kErrTimeout);
+  if (!ok) atomicCAS_system(R->err, 0, kErrTimeout);
   __syncthreads();
   if (threadIdx.x == 0) {
     if (atomicAdd(ctr + 1, 1u) == (uint32_t)a.G - 1) {

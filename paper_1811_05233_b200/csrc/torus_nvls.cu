@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(512, 1) nvls_kernel(const NvlsArgs a) {
       while ((int32_t)(ld_relaxed_sys32(f) - e) < 0) {
         __nanosleep(64);
         if ((++spin & 63u) == 0 && gtime() > deadline) {
-          atomicExch_system(R->err, 6);
+          atomicCAS_system(R->err, 0, 6);
           s_abort = 1;
           break;
         }
