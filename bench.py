@@ -399,7 +399,10 @@ def run_torus(args):
                                "(MEASURED_PEAKS.json has no NVLink entry)",
                 "traffic": load_traffic(f"torus_{X}x{Y}"), "kernel": kernel_name(comm, D, TD, dtype_s, wire_s),
                 "algorithmic_bytes_per_call": alg_bytes,
-                "nvlink_bytes_per_call": nvl_torus}
+                "nvlink_tx_bytes_ncu": load_traffic(f"torus_{X}x{Y}_nvltx"),
+                "nvlink_tx_user_bytes_ncu": load_traffic(f"torus_{X}x{Y}_nvltx_user"),
+                "traffic_source": "profiles/traffic.json (ncu on rank 0 of a real run, profiles/r02_ncu_push_*.csv)",
+                "nvlink_bytes_per_call_nvml": nvl_torus}
     else:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
             os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -509,12 +512,31 @@ def time_oracle(X, Y, dtype_s, wire_s, op, D):
     return time.perf_counter() - t0
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(args, X, Y, dtype_s, wire_s, world):
     D = min(args.count, oracle_sample_size(X, Y))
     reps, tot = 0, 0.0
-    while tot < 10.0 and reps < 50:
-        tot += time_oracle(X, Y, dtype_s, wire_s, args.op, D)
-        reps += 1
+    # single-threaded oracle pinned to one core (SURVEY 8(d) "oracle timing beside it")
+    old_aff = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    core = min(old_aff) if old_aff else None
+    if core is not None:
+        os.sched_setaffinity(0, {core})
+    try:
+        while tot < 10.0 and reps < 50:
+            tot += time_oracle(X, Y, dtype_s, wire_s, args.op, D)
+            reps += 1
+    finally:
+        if old_aff:
+            os.sched_setaffinity(0, old_aff)
     t = tot / reps
     S = D * DT_BYTES[wire_s]
     bus = 2.0 * (world - 1) / world
@@ -522,8 +544,8 @@ def cpu_baseline(args, X, Y, dtype_s, wire_s, world):
     return {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
             "sample": f"{X}x{Y} grid, {D} of {args.count} elements, {dtype_s} buffer / "
                       f"{wire_s} wire, {args.op}; {reps} reps, {t:.3f} s each, "
-                      "single-threaded C (oracle/torus_oracle.c)",
-            "host_cpus": os.cpu_count()}
+                      f"single-threaded C (oracle/torus_oracle.c), pinned to core {core}",
+            "host_cpus": os.cpu_count(), "cpu_model": cpu_model()}
 
 
 def run_reference(args):
