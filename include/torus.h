@@ -169,16 +169,27 @@ TORUS_API int torus_vallreduce(torus_comm_t comm, void* const* bufs, size_t coun
  * ResNet-50 gradients (161 tensors fused into buckets) fp16 with fused cast/scale").
  * ptrs / counts: HOST arrays [ntensors] of device pointers and element counts.  The
  * result equals torus_allreduce_ex on the concatenation of the tensors (same partition,
- * fold order and rounding): a fused pack kernel casts dtype -> wire into the comm's
- * staging buffer, the torus kernel reduces it (mean applied once), a fused unpack kernel
- * casts back.  The staging buffer grows on the first call with a larger bucket (that
- * call allocates and synchronizes; reserve it up front with torus_comm_reserve to keep
- * every call capturable).  Concurrent buckets need one comm each, with CTA budgets that
- * sum to at most the SM count (spin-waiting kernels of different comms must co-reside). */
+ * fold order and rounding).  When the concatenation takes the multi-phase route the call
+ * is FUSED: the kernel reads the tensors through a device table of (pointer, count,
+ * offset) with the dtype -> wire cast fused into its first read, and writes them back with
+ * the up-cast fused into its last write -- no staging buffer, no pack / unpack kernels.
+ * The first call with a new bucket (pointer list) uploads its table (allocates,
+ * synchronizes); later calls with the same bucket are capturable.  Smaller buckets (the
+ * one-shot / two-shot routes) pack into the comm's staging buffer, all-reduce it and
+ * unpack (that buffer grows on first use; reserve it with torus_comm_reserve).
+ * Concurrent buckets need one comm each, with CTA budgets that sum to at most the SM
+ * count (spin-waiting kernels of different comms must co-reside). */
 TORUS_API int torus_allreduce_multi(torus_comm_t comm, void* const* ptrs, const size_t* counts,
                                     int ntensors, torus_dtype_t dtype, torus_dtype_t wire,
                                     torus_op_t op, torus_stream_t stream);
 TORUS_API int torus_comm_reserve(torus_comm_t comm, size_t staging_bytes);
+
+/* Virtual-rank variant of the fused bucket call: ptrs is a HOST array [N * ntensors] of
+ * device pointers, rank-major (rank r's tensor i at ptrs[r * ntensors + i]); counts
+ * [ntensors] is shared.  Only the multi-phase route (UNSUPPORTED otherwise). */
+TORUS_API int torus_vallreduce_multi(torus_comm_t comm, void* const* ptrs, const size_t* counts,
+                                     int ntensors, torus_dtype_t dtype, torus_dtype_t wire,
+                                     torus_op_t op, torus_stream_t stream);
 
 /* Flat ring all-reduce over the rank ring 0 -> 1 -> ... -> N-1 -> 0 -- the BASELINE the
  * torus replaces ("Ring all-reduce scheme executes 2(N-1) GPU-to-GPU

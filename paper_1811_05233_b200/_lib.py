@@ -45,6 +45,7 @@ PROTOTYPES = {
     "torus_vallreduce": (_i, [_vp, _c.POINTER(_vp), _sz, _i, _i, _i, _vp]),
     "torus_allreduce_multi": (_i, [_vp, _c.POINTER(_vp), _c.POINTER(_sz), _i, _i, _i, _i, _vp]),
     "torus_comm_reserve": (_i, [_vp, _sz]),
+    "torus_vallreduce_multi": (_i, [_vp, _c.POINTER(_vp), _c.POINTER(_sz), _i, _i, _i, _i, _vp]),
     "torus_ring_allreduce": (_i, [_vp, _vp, _sz, _i, _i, _i, _vp]),
     "torus_vring_allreduce": (_i, [_vp, _c.POINTER(_vp), _sz, _i, _i, _i, _vp]),
     "torus_comm_ring_round_elems": (_sz, [_vp, _i]),

@@ -123,6 +123,11 @@ struct torus_comm {
     std::vector<char*> peer;              // every rank's buffer, mapped here
   };
   std::vector<Reg> regs;
+  struct SegTable {                       // NEXT-1: device copy of a bucket's tensor table
+    std::vector<MultiSeg> host;           // [nlocal * ntensors]
+    MultiSeg* dev;
+  };
+  std::vector<SegTable> seg_tables;
   std::vector<std::pair<std::string, void*>> ipc_opened;  // IPC handle -> mapped base
   float pull_w[5] = {0.5f, 1.f, 1.f, 1.f, 1.f};  // pull kernel: CTA weight per kind
   uint32_t* d_pull_ctr = nullptr;         // [nlocal][2] pull call epochs
@@ -347,6 +352,7 @@ void destroy_resources(torus_comm* c) {
   if (c->d_trace) cudaFree(c->d_trace);
   if (c->d_pull_trace) cudaFree(c->d_pull_trace);
   if (c->d_pull_pub) cudaFree(c->d_pull_pub);
+  for (auto& t : c->seg_tables) cudaFree(t.dev);
   if (c->d_done_local) cudaFree(c->d_done_local);
   if (c->d_sig_ack) cudaFree(c->d_sig_ack);
   if (c->d_staging) cudaFree(c->d_staging);
@@ -1029,7 +1035,7 @@ int launch_pull_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype
 }
 
 int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, int wire, int op,
-                   cudaStream_t stream) {
+                   cudaStream_t stream, const MultiSeg* segs = nullptr, int nseg = 0) {
   if (!c) return fail(TORUS_ERR_INVALID_ARG, "comm is NULL");
   if (!valid_pair(dtype, wire))
     return valid_dtype(dtype) && valid_dtype(wire)
@@ -1103,9 +1109,11 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
     return e == cudaSuccess ? TORUS_OK : cuda_fail(e, route == kRouteLL ? "one-shot kernel launch"
                                                                          : "two-shot kernel launch");
   }
-  // the round-1 push kernel (TORUS_KERNEL=push / tma, or grids the pull kernel does not take)
+  // the push kernel (default; TORUS_KERNEL=tma: its TMA-staged variant)
   int rc = switch_data_kernel(c, kDataPush, stream);
   if (rc) return rc;
+  a.segs = segs;  // NEXT-1 fused multi-tensor call: the buffer is a concatenation of tensors
+  a.nseg = nseg;
   a.G = c->G;
   a.fence_early = c->fence_early;
   a.poll_sleep = c->poll_sleep;
@@ -1133,6 +1141,7 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
   a.done_local = c->d_done_local;
   a.sig_ack = c->d_sig_ack;
   a.nsig = c->tma ? (c->nlocal * c->G + kThreads - 1) / kThreads : 0;
+  if (c->tma && nseg) return fail(TORUS_ERR_UNSUPPORTED, "fused multi-tensor call on the TMA variant");
   if (c->tma) {
     // ring buffers of one chunk each (tile pieces stream through in chunks): the largest
     // job holds max(X,Y)+3 buffers at once -- keep room for a few so the producer runs
@@ -1292,7 +1301,68 @@ size_t torus_comm_ring_round_elems(torus_comm_t c, torus_dtype_t wire) {
 
 }  // extern "C"
 
+namespace {
+
+// Device table of a bucket's tensors (all local ranks), cached per bucket: the first call
+// with a new bucket allocates and uploads it (synchronously); later calls reuse it, so
+// they stay CUDA-graph capturable.
+int seg_table(torus_comm* c, void* const* ptrs, const size_t* counts, int ntensors, const MultiSeg** out) {
+  std::vector<MultiSeg> h((size_t)c->nlocal * ntensors);
+  for (int l = 0; l < c->nlocal; ++l) {
+    unsigned long long off = 0;
+    for (int i = 0; i < ntensors; ++i) {
+      MultiSeg& m = h[(size_t)l * ntensors + i];
+      m.ptr = ptrs[(size_t)l * ntensors + i];
+      m.count = counts[i];
+      m.offset = off;
+      off += counts[i];
+    }
+  }
+  for (auto& t : c->seg_tables)
+    if (t.host.size() == h.size() &&
+        std::equal(h.begin(), h.end(), t.host.begin(), [](const MultiSeg& x, const MultiSeg& y) {
+          return x.ptr == y.ptr && x.count == y.count && x.offset == y.offset;
+        })) {
+      *out = t.dev;
+      return TORUS_OK;
+    }
+  torus_comm::SegTable t;
+  t.host = h;
+  CU(cudaSetDevice(c->device));
+  CU(cudaMalloc(&t.dev, h.size() * sizeof(MultiSeg)));
+  cudaError_t e = cudaMemcpy(t.dev, h.data(), h.size() * sizeof(MultiSeg), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(t.dev);
+    return cuda_fail(e, "multi-tensor table upload");
+  }
+  c->seg_tables.push_back(t);
+  *out = t.dev;
+  return TORUS_OK;
+}
+
+}  // namespace
+
 extern "C" {
+
+int torus_vallreduce_multi(torus_comm_t c, void* const* ptrs, const size_t* counts, int ntensors,
+                           torus_dtype_t dtype, torus_dtype_t wire, torus_op_t op, torus_stream_t stream) {
+  if (!c || !c->virt) return fail(TORUS_ERR_INVALID_ARG, "not a virtual comm");
+  if (ntensors <= 0 || !ptrs || !counts) return fail(TORUS_ERR_INVALID_ARG, "multi args");
+  if (!valid_pair(dtype, wire)) return fail(TORUS_ERR_UNSUPPORTED, "dtype %d with wire %d", dtype, wire);
+  size_t total = 0;
+  for (int i = 0; i < ntensors; ++i) total += counts[i];
+  for (size_t i = 0; i < (size_t)c->nlocal * ntensors; ++i)
+    if (counts[i % ntensors] && !ptrs[i]) return fail(TORUS_ERR_INVALID_ARG, "tensor %zu is NULL", i);
+  if (total == 0) return TORUS_OK;
+  if (plan_route(c, total, dtype, wire) != kRoutePush)
+    return fail(TORUS_ERR_UNSUPPORTED, "virtual multi-tensor calls take the multi-phase kernel only");
+  const MultiSeg* d = nullptr;
+  int rc = seg_table(c, ptrs, counts, ntensors, &d);
+  if (rc) return rc;
+  std::vector<void*> bufs(c->nlocal);
+  for (int l = 0; l < c->nlocal; ++l) bufs[l] = ptrs[(size_t)l * ntensors];
+  return allreduce_impl(c, bufs.data(), total, dtype, wire, op, static_cast<cudaStream_t>(stream), d, ntensors);
+}
 
 int torus_comm_reserve(torus_comm_t c, size_t staging_bytes) {
   if (!c) return fail(TORUS_ERR_INVALID_ARG, "comm is NULL");
@@ -1325,6 +1395,16 @@ int torus_allreduce_multi(torus_comm_t c, void* const* ptrs, const size_t* count
     total += counts[i];
   }
   if (total == 0) return TORUS_OK;
+  cudaStream_t s0 = static_cast<cudaStream_t>(stream);
+  if (plan_route(c, total, dtype, wire) == kRoutePush) {
+    // fused: the multi-phase kernel reads the tensors with the cast
+    // fused and writes them back with the up-cast fused -- no staging, no pack / unpack
+    const MultiSeg* d = nullptr;
+    int rc = seg_table(c, ptrs, counts, ntensors, &d);
+    if (rc) return rc;
+    void* bufs[1] = {ptrs[0]};
+    return allreduce_impl(c, bufs, total, dtype, wire, op, s0, d, ntensors);
+  }
   const size_t need = total * wire_size(wire) + 256;
   if (need > c->staging_bytes) {
     int rc = torus_comm_reserve(c, need);  // first use of a larger bucket allocates

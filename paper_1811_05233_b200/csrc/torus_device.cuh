@@ -286,5 +286,56 @@ __device__ __forceinline__ void store_user(void* buf, unsigned long long e, int 
   }
 }
 
+// ------------------------------------------------------------------------------------
+// NEXT-1: the user buffer as a concatenation of tensors (fused multi-tensor call).  A 16-byte
+// wire vector normally lies inside one tensor (ResNet-50's tensor sizes are multiples of 8);
+// one that straddles a boundary is gathered / scattered element by element.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int seg_find(const MultiSeg* seg, int nseg, unsigned long long e) {
+  int lo = 0, hi = nseg - 1;  // last segment with offset <= e
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (seg[mid].offset <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int DT, int W>
+__device__ __forceinline__ uint4 load_user_seg(const MultiSeg* seg, int nseg, unsigned long long e, int nrem) {
+  using T = typename Elem<DT>::T;
+  int i = seg_find(seg, nseg, e);
+  const unsigned long long local = e - seg[i].offset;
+  if (local + nrem <= seg[i].count) {
+    const T* p = reinterpret_cast<const T*>(seg[i].ptr) + local;
+    return load_user<DT, W>(p, 0, nrem, (reinterpret_cast<uintptr_t>(p) & 15) == 0);
+  }
+  T tmp[8];
+  for (int k = 0; k < nrem; ++k) {
+    while (i + 1 < nseg && e + k >= seg[i + 1].offset) ++i;
+    tmp[k] = reinterpret_cast<const T*>(seg[i].ptr)[e + k - seg[i].offset];
+  }
+  return load_user<DT, W>(tmp, 0, nrem, false);
+}
+
+template <int DT, int W>
+__device__ __forceinline__ void store_user_seg(const MultiSeg* seg, int nseg, unsigned long long e, int nrem,
+                                               uint4 v) {
+  using T = typename Elem<DT>::T;
+  int i = seg_find(seg, nseg, e);
+  const unsigned long long local = e - seg[i].offset;
+  if (local + nrem <= seg[i].count) {
+    T* p = reinterpret_cast<T*>(seg[i].ptr) + local;
+    store_user<DT, W>(p, 0, nrem, v, (reinterpret_cast<uintptr_t>(p) & 15) == 0);
+    return;
+  }
+  T tmp[8];
+  store_user<DT, W>(tmp, 0, nrem, v, false);
+  for (int k = 0; k < nrem; ++k) {
+    while (i + 1 < nseg && e + k >= seg[i + 1].offset) ++i;
+    reinterpret_cast<T*>(seg[i].ptr)[e + k - seg[i].offset] = tmp[k];
+  }
+}
+
 }  // namespace
 }  // namespace torus

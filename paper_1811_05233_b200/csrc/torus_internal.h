@@ -96,6 +96,18 @@ struct LaunchArgs {
   int ll_two_shot;               // 1: ll2_kernel (two-shot) instead of ll_kernel
   unsigned poll_sleep;           // default kernel: ns of back-off between flag polls
   int sd1;                       // default kernel: stage distance 1 even with T > 1
+  // NEXT-1 fused multi-tensor call: the "user buffer" of local rank l is the concatenation
+  // of nseg tensors described by segs[l * nseg .. (l + 1) * nseg) (device memory, sorted by
+  // offset); nseg == 0: buf[l] is one flat buffer
+  const struct MultiSeg* segs;
+  int nseg;
+};
+
+// one tensor of a fused multi-tensor call (device memory)
+struct MultiSeg {
+  void* ptr;
+  unsigned long long count;   // elements
+  unsigned long long offset;  // element offset of the tensor in the concatenation
 };
 
 // TMA kernel shared memory: nbufs ring buffers of one piece each (tile_vecs 16-byte wire

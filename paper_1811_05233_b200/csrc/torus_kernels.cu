@@ -121,6 +121,15 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
   char* const hin = myws + a.hin_off;
   char* const vin = myws + a.vin_off;
   char* const chunk = myws + a.chunk_off;
+  const MultiSeg* const segs = a.nseg ? a.segs + (size_t)lr * a.nseg : nullptr;
+  // the user buffer: one flat buffer, or (NEXT-1) the concatenation of a bucket's tensors
+  auto uload = [&](unsigned long long e, int nrem) -> uint4 {
+    return segs ? load_user_seg<DT, W>(segs, a.nseg, e, nrem) : load_user<DT, W>(buf, e, nrem, aligned);
+  };
+  auto ustore = [&](unsigned long long e, int nrem, uint4 v) {
+    if (segs) store_user_seg<DT, W>(segs, a.nseg, e, nrem, v);
+    else store_user<DT, W>(buf, e, nrem, v, aligned);
+  };
 
   __shared__ uint32_t s_seq;
   __shared__ int s_abort;
@@ -276,7 +285,7 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
                   if (v < p.p1) {
                     const unsigned long long el = p.so + v * VE;
                     const int nrem = (int)min((unsigned long long)VE, p.cl - el);
-                    r[u] = load_user<DT, W>(buf, a.buf_off + p.co + el, nrem, aligned);
+                    r[u] = uload(a.buf_off + p.co + el, nrem);
                   }
                 }
 #pragma unroll
@@ -304,7 +313,7 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
                     const unsigned long long el = p.so + v * VE;
                     if (j == c) {
                       const int nrem = (int)min((unsigned long long)VE, p.cl - el);
-                      r[u] = load_user<DT, W>(buf, a.buf_off + p.co + el, nrem, aligned);
+                      r[u] = uload(a.buf_off + p.co + el, nrem);
                     } else {
                       r[u] = ld_ws(hin + (size_t)j * a.hin_stride + el * SW);
                     }
@@ -336,7 +345,7 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
                   const uint4 out = pack<W>(acc[u]);
                   if (X > 1) st_ws(chunk + el * SW, out);
                   const int nrem = (int)min((unsigned long long)VE, p.cl - el);
-                  store_user<DT, W>(buf, a.buf_off + p.co + el, nrem, out, aligned);
+                  ustore(a.buf_off + p.co + el, nrem, out);
                 }
               }
             }
@@ -376,7 +385,7 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
               const unsigned long long el = p.so + v * VE;
               st_ws(chunk + el * SW, out);
               const int nrem = (int)min((unsigned long long)VE, p.cl - el);
-              store_user<DT, W>(buf, a.buf_off + p.co + el, nrem, out, aligned);
+              ustore(a.buf_off + p.co + el, nrem, out);
             }
           }
         } else if (k == kD) {
@@ -399,7 +408,7 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
                 const unsigned long long el = p.so + v * VE;
                 if (X > 1) st_ws(chunk + el * SW, r[u]);
                 const int nrem = (int)min((unsigned long long)VE, p.cl - el);
-                store_user<DT, W>(buf, a.buf_off + p.co + el, nrem, r[u], aligned);
+                ustore(a.buf_off + p.co + el, nrem, r[u]);
               }
             }
           }
@@ -423,7 +432,7 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
                   if (v >= p.p1) continue;
                   const unsigned long long el = p.so + v * VE;
                   const int nrem = (int)min((unsigned long long)VE, p.cl - el);
-                  store_user<DT, W>(buf, a.buf_off + p.co + el, nrem, r[u], aligned);
+                  ustore(a.buf_off + p.co + el, nrem, r[u]);
                 }
               }
             }

@@ -397,6 +397,22 @@ class VirtualTorus(_CommBase):
             OPS[op], _stream_ptr(stream)), "torus_vallreduce")
         return tensors
 
+    def all_reduce_multi(self, buckets: Sequence[Sequence[torch.Tensor]], op: str = "mean",
+                         wire: torch.dtype | None = None,
+                         stream: torch.cuda.Stream | None = None):
+        """Fused bucket call over the virtual ranks (torus_vallreduce_multi): buckets[r] is
+        rank r's list of tensors (same shapes on every rank)."""
+        if len(buckets) != self.N:
+            raise ValueError(f"need {self.N} tensor lists, one per virtual rank")
+        nt = len(buckets[0])
+        dt = buckets[0][0].dtype
+        ptrs = (ctypes.c_void_p * (self.N * nt))(*[t.data_ptr() for b in buckets for t in b])
+        counts = (ctypes.c_size_t * nt)(*[t.numel() for t in buckets[0]])
+        check(_lib.load().torus_vallreduce_multi(self._comm, ptrs, counts, nt, _dtype_code(dt),
+                                                 _dtype_code(wire or dt), OPS[op], _stream_ptr(stream)),
+              "torus_vallreduce_multi")
+        return buckets
+
     def ring_all_reduce(self, tensors: Sequence[torch.Tensor], op: str = "mean",
                         wire: torch.dtype | None = None,
                         stream: torch.cuda.Stream | None = None) -> Sequence[torch.Tensor]:
