@@ -301,15 +301,11 @@ __device__ __forceinline__ int seg_find(const MultiSeg* seg, int nseg, unsigned 
   return lo;
 }
 
+// boundary-straddling vectors: element by element, out of line (keeps the hot path lean)
 template <int DT, int W>
-__device__ __forceinline__ uint4 load_user_seg(const MultiSeg* seg, int nseg, unsigned long long e, int nrem) {
+__device__ __noinline__ uint4 load_user_straddle(const MultiSeg* seg, int nseg, int i, unsigned long long e,
+                                                 int nrem) {
   using T = typename Elem<DT>::T;
-  int i = seg_find(seg, nseg, e);
-  const unsigned long long local = e - seg[i].offset;
-  if (local + nrem <= seg[i].count) {
-    const T* p = reinterpret_cast<const T*>(seg[i].ptr) + local;
-    return load_user<DT, W>(p, 0, nrem, (reinterpret_cast<uintptr_t>(p) & 15) == 0);
-  }
   T tmp[8];
   for (int k = 0; k < nrem; ++k) {
     while (i + 1 < nseg && e + k >= seg[i + 1].offset) ++i;
@@ -317,24 +313,40 @@ __device__ __forceinline__ uint4 load_user_seg(const MultiSeg* seg, int nseg, un
   }
   return load_user<DT, W>(tmp, 0, nrem, false);
 }
-
 template <int DT, int W>
-__device__ __forceinline__ void store_user_seg(const MultiSeg* seg, int nseg, unsigned long long e, int nrem,
-                                               uint4 v) {
+__device__ __noinline__ void store_user_straddle(const MultiSeg* seg, int nseg, int i, unsigned long long e,
+                                                 int nrem, uint4 v) {
   using T = typename Elem<DT>::T;
-  int i = seg_find(seg, nseg, e);
-  const unsigned long long local = e - seg[i].offset;
-  if (local + nrem <= seg[i].count) {
-    T* p = reinterpret_cast<T*>(seg[i].ptr) + local;
-    store_user<DT, W>(p, 0, nrem, v, (reinterpret_cast<uintptr_t>(p) & 15) == 0);
-    return;
-  }
   T tmp[8];
   store_user<DT, W>(tmp, 0, nrem, v, false);
   for (int k = 0; k < nrem; ++k) {
     while (i + 1 < nseg && e + k >= seg[i + 1].offset) ++i;
     reinterpret_cast<T*>(seg[i].ptr)[e + k - seg[i].offset] = tmp[k];
   }
+}
+
+template <int DT, int W>
+__device__ __forceinline__ uint4 load_user_seg(const MultiSeg* seg, int nseg, unsigned long long e, int nrem) {
+  using T = typename Elem<DT>::T;
+  const int i = seg_find(seg, nseg, e);
+  const unsigned long long local = e - seg[i].offset;
+  if (local + nrem > seg[i].count) return load_user_straddle<DT, W>(seg, nseg, i, e, nrem);
+  const T* p = reinterpret_cast<const T*>(seg[i].ptr) + local;
+  return load_user<DT, W>(p, 0, nrem, (reinterpret_cast<uintptr_t>(p) & 15) == 0);
+}
+
+template <int DT, int W>
+__device__ __forceinline__ void store_user_seg(const MultiSeg* seg, int nseg, unsigned long long e, int nrem,
+                                               uint4 v) {
+  using T = typename Elem<DT>::T;
+  const int i = seg_find(seg, nseg, e);
+  const unsigned long long local = e - seg[i].offset;
+  if (local + nrem > seg[i].count) {
+    store_user_straddle<DT, W>(seg, nseg, i, e, nrem, v);
+    return;
+  }
+  T* p = reinterpret_cast<T*>(seg[i].ptr) + local;
+  store_user<DT, W>(p, 0, nrem, v, (reinterpret_cast<uintptr_t>(p) & 15) == 0);
 }
 
 }  // namespace

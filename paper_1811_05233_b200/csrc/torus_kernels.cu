@@ -102,7 +102,7 @@ __device__ __forceinline__ void bar_arrive(int id) {
 // Every wait is on flags peers raise one iteration earlier, so in steady state no stage
 // stalls on a cross-GPU round trip; the control warp polls the next stage's flags and
 // fences/raises the previous stage's flags while the workers move data.
-template <int DT, int W>
+template <int DT, int W, bool MULTI>
 __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const LaunchArgs a) {
   using Acc = typename Wire<W>::Acc;
   constexpr int VE = Wire<W>::VE;
@@ -121,13 +121,15 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
   char* const hin = myws + a.hin_off;
   char* const vin = myws + a.vin_off;
   char* const chunk = myws + a.chunk_off;
-  const MultiSeg* const segs = a.nseg ? a.segs + (size_t)lr * a.nseg : nullptr;
-  // the user buffer: one flat buffer, or (NEXT-1) the concatenation of a bucket's tensors
+  const MultiSeg* const segs = MULTI ? a.segs + (size_t)lr * a.nseg : nullptr;
+  // the user buffer: one flat buffer, or (MULTI, NEXT-1) the concatenation of a bucket's
+  // tensors -- a separate instantiation, so the flat path keeps its register budget
   auto uload = [&](unsigned long long e, int nrem) -> uint4 {
-    return segs ? load_user_seg<DT, W>(segs, a.nseg, e, nrem) : load_user<DT, W>(buf, e, nrem, aligned);
+    if constexpr (MULTI) return load_user_seg<DT, W>(segs, a.nseg, e, nrem);
+    else return load_user<DT, W>(buf, e, nrem, aligned);
   };
   auto ustore = [&](unsigned long long e, int nrem, uint4 v) {
-    if (segs) store_user_seg<DT, W>(segs, a.nseg, e, nrem, v);
+    if constexpr (MULTI) store_user_seg<DT, W>(segs, a.nseg, e, nrem, v);
     else store_user<DT, W>(buf, e, nrem, v, aligned);
   };
 
@@ -1099,19 +1101,23 @@ cudaError_t launch_typed(const LaunchArgs& a, bool cooperative, cudaStream_t str
     return cudaGetLastError();
   }
   const dim3 lblock(kLdgThreads);
+  const void* fn = (const void*)torus_kernel<DT, W, false>;
+  if constexpr (DT != DT_I32) {
+    if (a.nseg) fn = (const void*)torus_kernel<DT, W, true>;
+  }
+  if (a.nseg && DT == DT_I32) return cudaErrorNotSupported;
   if (cooperative) {
     void* args[] = {const_cast<LaunchArgs*>(&a)};
-    return cudaLaunchCooperativeKernel((const void*)torus_kernel<DT, W>, grid, lblock, args, 0,
-                                       stream);
+    return cudaLaunchCooperativeKernel(fn, grid, lblock, args, 0, stream);
   }
-  torus_kernel<DT, W><<<grid, lblock, 0, stream>>>(a);
-  return cudaGetLastError();
+  void* args[] = {const_cast<LaunchArgs*>(&a)};
+  return cudaLaunchKernel(fn, grid, lblock, args, 0, stream);
 }
 
 template <int DT, int W>
 int max_ctas_typed() {
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, torus_kernel<DT, W>, kLdgThreads, 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, torus_kernel<DT, W, false>, kLdgThreads, 0) !=
       cudaSuccess)
     return 0;
   return nb;
