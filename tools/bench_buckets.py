@@ -95,6 +95,27 @@ def main():
     torch.cuda.synchronize()
     tn = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], device="cuda", dtype=torch.float64)
     dist.all_reduce(tn, op=dist.ReduceOp.MAX)
+    # one flat f32 buffer of the same elements through the torus with fp16 wire (the
+    # bound a fused bucket call should approach), and NCCL on pre-flattened buckets: f32
+    # (DDP's bucket views, no compression) and fp16 (collective only, no cast cost)
+    flat32 = torch.randn(sum(sizes), device="cuda") * 2 ** -7
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record()
+        for _ in range(args.steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        x = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], device="cuda", dtype=torch.float64)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        return x.item()
+    t_flat = timed(lambda: comms[0].all_reduce(flat32, op="mean", wire=torch.float16))
+    bk32 = [torch.randn(sum(sizes[i] for i in b), device="cuda") for b in bks]
+    t_nccl32 = timed(lambda: [dist.all_reduce(x, op=dist.ReduceOp.AVG) for x in bk32])
+    t_nccl16 = timed(lambda: [dist.all_reduce(x, op=dist.ReduceOp.AVG) for x in flat16])
     S = sum(sizes) * 2
     bus = 2 * (world - 1) / world
     err = max(c.async_error() for c in comms)
@@ -105,7 +126,12 @@ def main():
                           "n_gpus": world, "grid": f"{X}x{Y}", "buckets": [len(b) for b in bks],
                           "bucket_elems": [sum(sizes[i] for i in b) for b in bks], "streams": K,
                           "us_per_step": t.item() * 1e6, "busbw_fp16": S / t.item() / 1e9 * bus,
+                          "flat_single_call_us": t_flat * 1e6,
+                          "ratio_to_flat": t.item() / t_flat,
+                          "routes": [comms[0].route(sum(sizes[i] for i in b), torch.float32, torch.float16)
+                                     for b in bks],
                           "nccl_fp16_hook_us": tn.item() * 1e6,
+                          "nccl_bucket_f32_us": t_nccl32 * 1e6, "nccl_bucket_fp16_collective_only_us": t_nccl16 * 1e6,
                           "nccl_busbw_fp16": S / tn.item() / 1e9 * bus, "async_error": err}))
     dist.destroy_process_group()
 
