@@ -15,7 +15,7 @@
  * (SURVEY.md Sec. 8(c), C1-C13), single-threaded, scalar, plain C.  Readings of the
  * paper where it is silent are listed in DESIGN.md Sec. 3 (R1..R17).
  *
- * Parity status: every function here is pinned by tests/test_oracle_*.py against
+ * Parity status: every function here is pinned by tests/test_oracle.py against
  * hand-computed values, SPEC worked examples, closed forms and brute force.  No function
  * is "parity unpinned".
  */

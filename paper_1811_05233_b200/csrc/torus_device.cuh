@@ -325,10 +325,26 @@ __device__ __noinline__ void store_user_straddle(const MultiSeg* seg, int nseg, 
   }
 }
 
+// the segment of element e, starting from the caller's last one (a thread walks its tiles in
+// increasing order, so the hint is nearly always right; otherwise binary search)
+__device__ __forceinline__ int seg_find_hint(const MultiSeg* seg, int nseg, unsigned long long e, int& hint) {
+  int i = hint;
+  const unsigned long long o = seg[i].offset;
+  if (e >= o && e < o + seg[i].count) return i;
+  if (e >= o && i + 1 < nseg && e >= seg[i + 1].offset &&
+      (i + 2 >= nseg || e < seg[i + 2].offset)) {
+    hint = i + 1;
+    return hint;
+  }
+  hint = seg_find(seg, nseg, e);
+  return hint;
+}
+
 template <int DT, int W>
-__device__ __forceinline__ uint4 load_user_seg(const MultiSeg* seg, int nseg, unsigned long long e, int nrem) {
+__device__ __forceinline__ uint4 load_user_seg(const MultiSeg* seg, int nseg, unsigned long long e, int nrem,
+                                               int& hint) {
   using T = typename Elem<DT>::T;
-  const int i = seg_find(seg, nseg, e);
+  const int i = seg_find_hint(seg, nseg, e, hint);
   const unsigned long long local = e - seg[i].offset;
   if (local + nrem > seg[i].count) return load_user_straddle<DT, W>(seg, nseg, i, e, nrem);
   const T* p = reinterpret_cast<const T*>(seg[i].ptr) + local;
@@ -337,9 +353,9 @@ __device__ __forceinline__ uint4 load_user_seg(const MultiSeg* seg, int nseg, un
 
 template <int DT, int W>
 __device__ __forceinline__ void store_user_seg(const MultiSeg* seg, int nseg, unsigned long long e, int nrem,
-                                               uint4 v) {
+                                               uint4 v, int& hint) {
   using T = typename Elem<DT>::T;
-  const int i = seg_find(seg, nseg, e);
+  const int i = seg_find_hint(seg, nseg, e, hint);
   const unsigned long long local = e - seg[i].offset;
   if (local + nrem > seg[i].count) {
     store_user_straddle<DT, W>(seg, nseg, i, e, nrem, v);

@@ -124,12 +124,13 @@ __global__ void __launch_bounds__(kLdgThreads, kLdgCtasPerSm) torus_kernel(const
   const MultiSeg* const segs = MULTI ? a.segs + (size_t)lr * a.nseg : nullptr;
   // the user buffer: one flat buffer, or (MULTI, NEXT-1) the concatenation of a bucket's
   // tensors -- a separate instantiation, so the flat path keeps its register budget
+  int seg_hint = 0;  // MULTI: this thread's last segment
   auto uload = [&](unsigned long long e, int nrem) -> uint4 {
-    if constexpr (MULTI) return load_user_seg<DT, W>(segs, a.nseg, e, nrem);
+    if constexpr (MULTI) return load_user_seg<DT, W>(segs, a.nseg, e, nrem, seg_hint);
     else return load_user<DT, W>(buf, e, nrem, aligned);
   };
   auto ustore = [&](unsigned long long e, int nrem, uint4 v) {
-    if constexpr (MULTI) store_user_seg<DT, W>(segs, a.nseg, e, nrem, v);
+    if constexpr (MULTI) store_user_seg<DT, W>(segs, a.nseg, e, nrem, v, seg_hint);
     else store_user<DT, W>(buf, e, nrem, v, aligned);
   };
 

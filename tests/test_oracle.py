@@ -320,6 +320,24 @@ def test_hierarchical_same_ops_x_times_more_vertical_data():
     assert v_h == X * v_t
 
 
+def test_hierarchical_float_chain_order():
+    """DESIGN R14: the hierarchical baseline's chain reduce runs from the highest column to
+    the leader (column 0), so a row's sum is ((w[X-1] + w[X-2]) + ...) + w[0].  Hand-derived
+    f32 pin, X=3, Y=1, one element: inputs [2^24, 1, 1] (columns 0, 1, 2): the chain gives
+    (1 + 1) + 2^24 = 16777218 exactly; the opposite order would give (2^24 + 1) + 1 ->
+    16777216 (2^24 + 1 ties to even).  And with an f16 wire every hop is rounded (HOP,
+    SURVEY C7): inputs [2048, 1, 1] give (1 + 1) + 2048 = 2050, representable in binary16."""
+    ins = [np.array([v], dtype=np.float32) for v in (2.0 ** 24, 1.0, 1.0)]
+    out = oracle.hier_allreduce(ins, 3, 1, "f32", op="sum", policy="hop")
+    assert all(o[0] == np.float32(16777218.0) for o in out)
+    ins16 = [np.array([v], dtype=np.float16) for v in (2048.0, 1.0, 1.0)]
+    out16 = oracle.hier_allreduce(ins16, 3, 1, "f16", op="sum", policy="hop")
+    assert all(o[0] == np.float16(2050.0) for o in out16)
+    # the torus on the same row folds c+1, ..., c: chunk owner 0 sums 1 + 1 + 2^24 as well
+    t = oracle.torus_allreduce(ins, 3, 1, "f32", op="sum")
+    assert all(o[0] == np.float32(16777218.0) for o in t)
+
+
 def test_mixed_precision_phase_not_worse_than_hop():
     """over random trials (U[0,1), N=16, D=256) the mean abs error of
     f16 wire + f32 accumulation is <= that of f16 accumulation."""

@@ -119,6 +119,7 @@ def main():
     S = sum(sizes) * 2
     bus = 2 * (world - 1) / world
     err = max(c.async_error() for c in comms)
+    routes = [comms[0].route(sum(sizes[i] for i in b), torch.float32, torch.float16) for b in bks]
     for c in comms:
         c.destroy()
     if rank == 0:
@@ -128,8 +129,7 @@ def main():
                           "us_per_step": t.item() * 1e6, "busbw_fp16": S / t.item() / 1e9 * bus,
                           "flat_single_call_us": t_flat * 1e6,
                           "ratio_to_flat": t.item() / t_flat,
-                          "routes": [comms[0].route(sum(sizes[i] for i in b), torch.float32, torch.float16)
-                                     for b in bks],
+                          "routes": routes,
                           "nccl_fp16_hook_us": tn.item() * 1e6,
                           "nccl_bucket_f32_us": t_nccl32 * 1e6, "nccl_bucket_fp16_collective_only_us": t_nccl16 * 1e6,
                           "nccl_busbw_fp16": S / tn.item() / 1e9 * bus, "async_error": err}))
