@@ -17,6 +17,7 @@
 // dtype is bit-exact.  No tensor cores: a bandwidth-bound reduction, not a contraction.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "torus_device.cuh"
 
@@ -1187,6 +1188,11 @@ cudaError_t launch_cs_variant(float* buf, unsigned long long n, cudaStream_t str
 cudaError_t launch_castscale(void* buf, unsigned long long n, int dtype, int wire,
                              cudaStream_t stream) {
   if (dtype != DT_F32) return cudaErrorInvalidValue;
+  // TMA-streamed variant (torus_cast.cu) for aligned buffers unless TORUS_CS_KERNEL=ldg
+  const char* kv = getenv("TORUS_CS_KERNEL");
+  const bool tma = !(kv && strcmp(kv, "ldg") == 0);
+  if (tma && (reinterpret_cast<uintptr_t>(buf) & 15) == 0 && n >= 8)
+    return launch_castscale_tma(buf, n, wire, stream);
   if (wire == DT_F16) return launch_cs_variant<DT_F16>(reinterpret_cast<float*>(buf), n, stream);
   if (wire == DT_BF16) return launch_cs_variant<DT_BF16>(reinterpret_cast<float*>(buf), n, stream);
   return cudaErrorInvalidValue;
