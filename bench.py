@@ -412,7 +412,7 @@ def run_torus(args):
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
-                "traffic": load_traffic("castscale"), "kernel": "castscale_kernel",
+                "traffic": load_traffic("castscale_tma"), "kernel": kernel_name(comm, D, TD, dtype_s, wire_s),
                 "algorithmic_bytes_per_call": alg_bytes}
 
     cpu = None

@@ -831,7 +831,7 @@ namespace {
 enum Route { kRouteNone = 0, kRouteCast, kRouteLL, kRouteLL2, kRoutePull, kRoutePush };
 const char* route_name(int r) {
   switch (r) {
-    case kRouteCast: return "castscale_kernel";
+    case kRouteCast: return "castscale_tma_kernel";  // castscale_kernel for unaligned buffers
     case kRouteLL: return "ll_kernel";
     case kRouteLL2: return "ll2_kernel";
     case kRoutePull: return "torus_pull_kernel";
