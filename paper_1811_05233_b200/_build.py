@@ -10,8 +10,8 @@ PKG = pathlib.Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 SOURCES = [CSRC / "torus_abi.cu", CSRC / "torus_kernels.cu", CSRC / "torus_pull.cu", CSRC / "torus_cast.cu",
-           CSRC / "torus_baselines.cu", CSRC / "torus_ll.cu", CSRC / "torus_nvls.cu"]
-HEADERS = [CSRC / "torus_internal.h", CSRC / "torus_device.cuh", CSRC / "torus_pull.h",
+           CSRC / "torus_baselines.cu", CSRC / "torus_ll.cu", CSRC / "torus_ll128.cu", CSRC / "torus_nvls.cu"]
+HEADERS = [CSRC / "torus_internal.h", CSRC / "torus_device.cuh", CSRC / "torus_pull.h", CSRC / "torus_ll128.h",
            ROOT / "include" / "torus.h"]
 
 

@@ -17,6 +17,7 @@
 
 #include "../../include/torus.h"
 #include "torus_internal.h"
+#include "torus_ll128.h"
 #include "torus_pull.h"
 
 using namespace torus;
@@ -140,9 +141,9 @@ struct torus_comm {
 
 namespace {
 
-enum { kModePull = 0, kModePush = 1, kModeTma = 2 };
+enum { kModePull = 0, kModePush = 1, kModeTma = 2, kModeLL128 = 3 };
 // kernels that share the slab's data region (a switch between them needs a barrier)
-enum { kDataNone = 0, kDataPull = 1, kDataPush = 2, kDataRing = 3, kDataHier = 4 };
+enum { kDataNone = 0, kDataPull = 1, kDataPush = 2, kDataRing = 3, kDataHier = 4, kDataLL128 = 5 };
 
 size_t pull_flag_bytes(size_t slab_size) {
   size_t b = std::min<size_t>(kPullFlagBytes, slab_size / 16);
@@ -199,8 +200,16 @@ unsigned long long round_elems(const torus_comm* c, int wire) {
   // push kernel: h_in (X > 1: X slots of R/X) + v_in (Y slots of R/(XY)) + chunk (R/X)
   // pull kernel, per call parity: win (R) + P1 (R/X, if X > 1 and Y > 1) + chunk (R/X)
   unsigned long long per_k;
-  if (c->mode == kModePull) per_k = 2 * q * (X * Y + ((X > 1 && Y > 1) ? 2 : 1) * Y);
-  else per_k = q * Y * ((X > 1 ? X : 0) + 2);
+  if (c->mode == kModePull) {
+    per_k = 2 * q * (X * Y + ((X > 1 && Y > 1) ? 2 : 1) * Y);
+  } else if (c->mode == kModeLL128) {
+    // per parity: H and HAG inboxes (X > 1) R each, V and AG inboxes (Y > 1) R/X each, as
+    // 128-byte lines holding 120 bytes (x 16/15) -- plus a 10% margin for stream padding
+    const unsigned long long slots = (X > 1 ? 2 * X * Y : 0) + (Y > 1 ? 2 * Y : 0);
+    per_k = (2 * q * slots * 16 * 11 + 149) / 150;
+  } else {
+    per_k = q * Y * ((X > 1 ? X : 0) + 2);
+  }
   const unsigned long long k = data_elems / per_k;
   return k * q * X * Y;
 }
@@ -323,6 +332,7 @@ void read_knobs(torus_comm* c) {
   c->mode = kModePush;
   if (k && strcmp(k, "pull") == 0) c->mode = kModePull;
   if (k && strcmp(k, "tma") == 0) c->mode = kModeTma;
+  if (k && strcmp(k, "ll128") == 0) c->mode = kModeLL128;
   c->tma = c->mode == kModeTma;
   c->tile_vecs = (int)env_size("TORUS_TILE", 0);  // push kernel; 0 = auto (T ~ 3 tiles per slice)
   c->one_tile_max = env_size("TORUS_ONE_TILE_MAX", 4096);
@@ -828,7 +838,7 @@ int torus_comm_launches(torus_comm_t c, size_t count, torus_dtype_t dtype, torus
 namespace {
 
 // ---- routing: which kernel serves a call (same decision on every rank) ----
-enum Route { kRouteNone = 0, kRouteCast, kRouteLL, kRouteLL2, kRoutePull, kRoutePush };
+enum Route { kRouteNone = 0, kRouteCast, kRouteLL, kRouteLL2, kRoutePull, kRoutePush, kRouteLL128 };
 const char* route_name(int r) {
   switch (r) {
     case kRouteCast: return "castscale_tma_kernel";  // castscale_kernel for unaligned buffers
@@ -836,6 +846,7 @@ const char* route_name(int r) {
     case kRouteLL2: return "ll2_kernel";
     case kRoutePull: return "torus_pull_kernel";
     case kRoutePush: return "torus_kernel";
+    case kRouteLL128: return "torus_ll128_kernel";
     default: return "none";
   }
 }
@@ -893,6 +904,7 @@ int plan_route(const torus_comm* c, size_t count, int dtype, int wire) {
   if (c->world >= 3 && c->layout.ll_region && count * sw <= c->ll2_max && count <= R && ll2_slot(c, count, sw))
     return kRouteLL2;
   if (pull_fits(c, R, wire, dtype)) return kRoutePull;
+  if (c->mode == kModeLL128 && c->world <= kMaxRanks) return kRouteLL128;
   return kRoutePush;
 }
 
@@ -1034,6 +1046,88 @@ int launch_pull_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype
   return TORUS_OK;
 }
 
+int launch_ll128_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype, int wire, int op,
+                        bool aligned, cudaStream_t stream) {
+  const unsigned long long R = round_elems(c, wire), sw = wire_size(wire);
+  const int X = c->X, Y = c->Y, q = (int)(kVecBytes / sw);
+  const unsigned long long UE = 30ull * q;  // elements per unit
+  L128Args a;
+  memset(&a, 0, sizeof a);
+  a.ranks = c->d_ranks;
+  for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];
+  a.nlocal = c->nlocal;
+  a.op = op;
+  a.inv_n = 1.0f / (float)(X * Y);
+  a.aligned = aligned ? 1 : 0;
+  a.timeout_ns = c->timeout_ns;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  a.ctas = std::max(1, sms / c->nlocal);
+  const int warps = a.ctas * 16;
+  // warps per stage ~ each stage's loads + stores per unit x units
+  double w[5] = {X > 1 ? 2.0 * (X - 1) * Y : 0, (double)Y * (X + 1), Y > 1 ? 2.0 * Y + X - 1 : 0,
+                 Y > 1 ? (double)(Y - 1) * (X + 1) : 0, X > 1 ? 2.0 * (X - 1) * Y : 0};
+  double ws = 0;
+  int present = 0;
+  for (double v : w) {
+    ws += v;
+    present += v > 0;
+  }
+  if (warps < present) return fail(TORUS_ERR_UNSUPPORTED, "ll128 kernel: %d warps for %d stages", warps, present);
+  int tot = 0;
+  for (int k = 0; k < 5; ++k) {
+    a.wk[k] = w[k] > 0 ? std::max(1, (int)(warps * w[k] / ws)) : 0;
+    tot += a.wk[k];
+  }
+  while (tot > warps) {
+    int kb = 0;
+    for (int k = 1; k < 5; ++k)
+      if (a.wk[k] > a.wk[kb]) kb = k;
+    --a.wk[kb];
+    --tot;
+  }
+  a.wsum = tot;
+  int rc = switch_data_kernel(c, kDataLL128, stream);
+  if (rc) return rc;
+  for (unsigned long long r0 = 0; r0 < count; r0 += R) {
+    a.n = std::min<unsigned long long>(R, count - r0);
+    a.buf_off = r0;
+    unsigned long long chunk_units_max = 0, umax = 0;
+    for (int j = 0; j < X; ++j) {
+      unsigned long long cl;
+      qpart(a.n, X, q, j, &a.g_co[j], &cl);
+      unsigned long long cu = 0;
+      for (int s2 = 0; s2 < Y; ++s2) {
+        const int js = j * Y + s2;
+        qpart(cl, Y, q, s2, &a.g_cs[js], &a.g_sl[js]);
+        a.g_U[js] = (int)((a.g_sl[js] + UE - 1) / UE);
+        a.g_uoff[js] = (int)cu;
+        cu += a.g_U[js];
+        umax = std::max<unsigned long long>(umax, a.g_U[js]);
+      }
+      chunk_units_max = std::max(chunk_units_max, cu);
+    }
+    a.Umax = (int)umax;
+    a.h_stride = a.hag_stride = chunk_units_max * kL128Unit;
+    a.v_stride = a.ag_stride = umax * kL128Unit;
+    unsigned long long off = c->layout.data_off;
+    for (int p = 0; p < 2; ++p) {
+      a.h_off[p] = off;
+      off += X > 1 ? X * a.h_stride : 0;
+      a.hag_off[p] = off;
+      off += X > 1 ? X * a.hag_stride : 0;
+      a.v_off[p] = off;
+      off += Y > 1 ? Y * a.v_stride : 0;
+      a.ag_off[p] = off;
+      off += Y > 1 ? Y * a.ag_stride : 0;
+    }
+    if (off > c->slab_size) return fail(TORUS_ERR_INVALID_ARG, "ll128 layout overflow (%llu > %zu)", off, c->slab_size);
+    cudaError_t e = launch_ll128(a, dtype, wire, c->virt, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "ll128 kernel launch");
+  }
+  return TORUS_OK;
+}
+
 int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, int wire, int op,
                    cudaStream_t stream, const MultiSeg* segs = nullptr, int nseg = 0) {
   if (!c) return fail(TORUS_ERR_INVALID_ARG, "comm is NULL");
@@ -1080,6 +1174,7 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
     if (rc) return rc;
     return launch_pull_rounds(c, bufs, count, dtype, wire, op, aligned, stream);
   }
+  if (route == kRouteLL128 && !nseg) return launch_ll128_rounds(c, bufs, count, dtype, wire, op, aligned, stream);
   LaunchArgs a;
   memset(&a, 0, sizeof a);
   a.ranks = c->d_ranks;
