@@ -904,7 +904,7 @@ int plan_route(const torus_comm* c, size_t count, int dtype, int wire) {
   if (c->world >= 3 && c->layout.ll_region && count * sw <= c->ll2_max && count <= R && ll2_slot(c, count, sw))
     return kRouteLL2;
   if (pull_fits(c, R, wire, dtype)) return kRoutePull;
-  if (c->mode == kModeLL128 && c->world <= kMaxRanks) return kRouteLL128;
+  if (c->mode == kModeLL128 && c->X <= 8 && c->Y <= 8) return kRouteLL128;
   return kRoutePush;
 }
 
