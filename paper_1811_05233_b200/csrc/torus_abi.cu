@@ -113,6 +113,8 @@ struct torus_comm {
   int pull_ctas = 0;                      // pull kernel: CTA budget per rank (0 = all resident)
   int pull_fence = 0;                     // pull kernel publish fence (see PullArgs::fence)
   int pull_zc = 1;                        // pull kernel: zero-copy from registered buffers
+  int ll128_ctas = 0;                     // LL128 kernel: CTAs per rank (0 = one per SM)
+  float ll128_w[5] = {1.f, 1.f, 1.f, 1.f, 1.f};  // LL128 kernel: warp weight per stage
   int check = 0;                          // TORUS_CHECK=1: per-call header check (MISMATCH)
   int fault = 0;                          // TORUS_FAULT: negative-control fault injection (tests)
   unsigned delay_ns = 0;                  // TORUS_DELAY_NS: random per-CTA start delay (tests)
@@ -344,6 +346,9 @@ void read_knobs(torus_comm* c) {
   c->pull_ctas = (int)env_size("TORUS_PULL_CTAS", 0);
   c->pull_fence = (int)env_size("TORUS_PULL_FENCE", 3);
   c->pull_zc = (int)env_size("TORUS_PULL_ZC", 1);
+  c->ll128_ctas = (int)env_size("TORUS_LL128_CTAS", 0);
+  if (const char* w = getenv("TORUS_LL128_W"))
+    sscanf(w, "%f,%f,%f,%f,%f", &c->ll128_w[0], &c->ll128_w[1], &c->ll128_w[2], &c->ll128_w[3], &c->ll128_w[4]);
   c->check = (int)env_size("TORUS_CHECK", 0);
   c->fault = (int)env_size("TORUS_FAULT", 0);
   c->delay_ns = (unsigned)env_size("TORUS_DELAY_NS", 0);
@@ -1062,11 +1067,12 @@ int launch_ll128_rounds(torus_comm* c, void* const* bufs, size_t count, int dtyp
   a.timeout_ns = c->timeout_ns;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  a.ctas = std::max(1, sms / c->nlocal);
+  a.ctas = std::max(1, (c->ll128_ctas > 0 ? std::min(c->ll128_ctas, sms) : sms) / c->nlocal);
   const int warps = a.ctas * 16;
-  // warps per stage ~ each stage's loads + stores per unit x units
+  // warps per stage ~ each stage's loads + stores per unit x units (x TORUS_LL128_W)
   double w[5] = {X > 1 ? 2.0 * (X - 1) * Y : 0, (double)Y * (X + 1), Y > 1 ? 2.0 * Y + X - 1 : 0,
                  Y > 1 ? (double)(Y - 1) * (X + 1) : 0, X > 1 ? 2.0 * (X - 1) * Y : 0};
+  for (int k = 0; k < 5; ++k) w[k] *= c->ll128_w[k];
   double ws = 0;
   int present = 0;
   for (double v : w) {

@@ -93,42 +93,6 @@ __device__ __forceinline__ bool get(const char* stream, unsigned long long u, in
   }
 }
 
-// read n (<= M) units at once -- one load round for all of them, retrying only the ones
-// whose lines have not all landed; out[i] gets unit i.  Warp-collective.
-template <int M>
-__device__ __forceinline__ bool get_n(const char* const* p, int n, int lane, uint64_t flag,
-                                      unsigned long long deadline, const int* err, uint4* out) {
-  uint32_t pending = (1u << n) - 1u;
-  unsigned spin = 0;
-  const bool fl = (lane & 7) == 7;
-  for (;;) {
-    uint64_t lo[M], hi[M];
-#pragma unroll
-    for (int i = 0; i < M; ++i)
-      if (i < n && ((pending >> i) & 1u)) ld_line(p[i], lo[i], hi[i]);
-#pragma unroll
-    for (int i = 0; i < M; ++i) {
-      if (i < n && ((pending >> i) & 1u)) {
-        const int mine = !fl || (hi[i] == flag);
-        const int line_ok = __shfl_sync(0xffffffffu, mine, (lane & ~7) | 7);
-        if (__all_sync(0xffffffffu, line_ok)) {
-          out[i] = make_uint4((uint32_t)lo[i], (uint32_t)(lo[i] >> 32), fl ? 0u : (uint32_t)hi[i],
-                              fl ? 0u : (uint32_t)(hi[i] >> 32));
-          pending &= ~(1u << i);
-        }
-      }
-    }
-    if (!pending) return true;
-    if ((++spin & 255u) == 0) {
-      int bad = 0;
-      if (lane == 0) bad = gtimer() > deadline || ((spin & 4095u) == 0 && *(volatile const int*)err);
-      if (__shfl_sync(0xffffffffu, bad, 0)) return false;
-    }
-  }
-}
-
-constexpr int kL128MaxOps = 8;  // the ll128 route takes grids with X, Y <= 8
-
 template <int DT, int W>
 __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128Args a) {
   using Acc = typename Wire<W>::Acc;
@@ -192,27 +156,23 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
       if (u >= a.g_U[cs]) continue;
       const int nr = lane_n(a.g_sl[cs], u);
       const unsigned long long e = a.g_co[c] + a.g_cs[cs] + (unsigned long long)u * UE + eoff;
-      // operands in fold order (columns c+1, ..., c): the X-1 inbox units in one load round
-      const char* ptr[kL128MaxOps];
-      uint4 w[kL128MaxOps];
-#pragma unroll
-      for (int kk = 0; kk < kL128MaxOps - 1; ++kk)
-        if (kk < X - 1)
-          ptr[kk] = lane_ptr(inbox(me, a.h_off[par], a.h_stride, (c + 1 + kk) % X),
-                             (unsigned long long)a.g_uoff[cs] + u, lane);
-      const uint4 own = uload(e, nr);
-      if (X > 1) ok = get_n<kL128MaxOps - 1>(ptr, X - 1, lane, flag, deadline, R->err, w);
-      if (!ok) break;
-      w[X - 1] = own;
       Acc acc[VE];
-      unpack<W>(w[0], acc);
+      for (int kk = 1; kk <= X && ok; ++kk) {
+        const int j = (c + kk) % X;
+        uint4 w;
+        if (j == c) w = uload(e, nr);
+        else ok = get(inbox(me, a.h_off[par], a.h_stride, j), (unsigned long long)a.g_uoff[cs] + u, lane, flag,
+                      deadline, R->err, &w);
+        Acc t[VE];
+        unpack<W>(w, t);
+        if (kk == 1) {
 #pragma unroll
-      for (int kk = 1; kk < kL128MaxOps; ++kk)
-        if (kk < X) {
-          Acc t[VE];
-          unpack<W>(w[kk], t);
+          for (int i = 0; i < VE; ++i) acc[i] = t[i];
+        } else {
           acc_add<W>(acc, t);
         }
+      }
+      if (!ok) break;
       if (Y > 1) {
         put(inbox(s * X + c, a.v_off[par], a.v_stride, rho), u, lane, pack<W>(acc), flag);
       } else {  // the last reduce phase: mean, round once, final
@@ -229,23 +189,21 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
     const int cr = c * Y + rho;
     for (int u = wr; u < a.g_U[cr] && ok; u += WS) {
       const int nr = lane_n(a.g_sl[cr], u);
-      // operands in fold order (rows rho+1, ..., rho), all Y units in one load round
-      const char* ptr[kL128MaxOps];
-      uint4 w[kL128MaxOps];
-#pragma unroll
-      for (int kk = 0; kk < kL128MaxOps; ++kk)
-        if (kk < Y) ptr[kk] = lane_ptr(inbox(me, a.v_off[par], a.v_stride, (rho + 1 + kk) % Y), u, lane);
-      ok = get_n<kL128MaxOps>(ptr, Y, lane, flag, deadline, R->err, w);
-      if (!ok) break;
       Acc acc[VE];
-      unpack<W>(w[0], acc);
+      for (int kk = 1; kk <= Y && ok; ++kk) {
+        const int i = (rho + kk) % Y;
+        uint4 w;
+        ok = get(inbox(me, a.v_off[par], a.v_stride, i), u, lane, flag, deadline, R->err, &w);
+        Acc t[VE];
+        unpack<W>(w, t);
+        if (kk == 1) {
 #pragma unroll
-      for (int kk = 1; kk < kL128MaxOps; ++kk)
-        if (kk < Y) {
-          Acc t[VE];
-          unpack<W>(w[kk], t);
+          for (int q = 0; q < VE; ++q) acc[q] = t[q];
+        } else {
           acc_add<W>(acc, t);
         }
+      }
+      if (!ok) break;
       if (a.op == 1) acc_mean<W>(acc, a.inv_n, N);
       const uint4 out = pack<W>(acc);
       ustore(a.g_co[c] + a.g_cs[cr] + (unsigned long long)u * UE + eoff, nr, out);
@@ -257,55 +215,28 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
     }
   } else if (stage == kSD && Y > 1) {
     // ---- D: a column peer's reduced sub-chunk -> my buffer + the row peers' HAG inboxes ----
-    // two jobs per iteration (one load round for both)
-    const int nj = a.Umax * (Y - 1);
-    for (int J0 = wr; J0 < nj && ok; J0 += 2 * WS) {
-      int uu[2], ii[2], m = 0;
-      const char* ptr[2];
-      for (int h = 0; h < 2; ++h) {
-        const int J = J0 + h * WS;
-        if (J >= nj) continue;
-        const int u = J / (Y - 1), i = (rho + 1 + J % (Y - 1)) % Y;
-        if (u >= a.g_U[c * Y + i]) continue;
-        uu[m] = u;
-        ii[m] = i;
-        ptr[m++] = lane_ptr(inbox(me, a.ag_off[par], a.ag_stride, i), u, lane);
-      }
-      if (!m) continue;
-      uint4 w[2];
-      ok = get_n<2>(ptr, m, lane, flag, deadline, R->err, w);
+    for (int J = wr; J < a.Umax * (Y - 1) && ok; J += WS) {
+      const int u = J / (Y - 1), i = (rho + 1 + J % (Y - 1)) % Y, ci = c * Y + i;
+      if (u >= a.g_U[ci]) continue;
+      uint4 w;
+      ok = get(inbox(me, a.ag_off[par], a.ag_stride, i), u, lane, flag, deadline, R->err, &w);
       if (!ok) break;
-      for (int h = 0; h < m; ++h) {
-        const int ci = c * Y + ii[h], u = uu[h];
-        ustore(a.g_co[c] + a.g_cs[ci] + (unsigned long long)u * UE + eoff, lane_n(a.g_sl[ci], u), w[h]);
-        for (int jj = 1; jj < X; ++jj)
-          put(inbox(rho * X + (c + jj) % X, a.hag_off[par], a.hag_stride, c), (unsigned long long)a.g_uoff[ci] + u,
-              lane, w[h], flag);
-      }
+      ustore(a.g_co[c] + a.g_cs[ci] + (unsigned long long)u * UE + eoff, lane_n(a.g_sl[ci], u), w);
+      for (int jj = 1; jj < X; ++jj)
+        put(inbox(rho * X + (c + jj) % X, a.hag_off[par], a.hag_stride, c), (unsigned long long)a.g_uoff[ci] + u,
+            lane, w, flag);
     }
   } else if (stage == kSE && X > 1) {
     // ---- E: a row peer's completed chunk -> my buffer (wire -> dtype) ----
-    const int per_u = (X - 1) * Y, nj = a.Umax * per_u;
-    for (int J0 = wr; J0 < nj && ok; J0 += 2 * WS) {  // two jobs per iteration
-      int uu[2], jsv[2], jv[2], m = 0;
-      const char* ptr[2];
-      for (int h = 0; h < 2; ++h) {
-        const int J = J0 + h * WS;
-        if (J >= nj) continue;
-        const int u = J / per_u, r = J % per_u, j = (c + 1 + r / Y) % X, s = r % Y, js = j * Y + s;
-        if (u >= a.g_U[js]) continue;
-        uu[m] = u;
-        jsv[m] = js;
-        jv[m] = j;
-        ptr[m++] = lane_ptr(inbox(me, a.hag_off[par], a.hag_stride, j), (unsigned long long)a.g_uoff[js] + u, lane);
-      }
-      if (!m) continue;
-      uint4 w[2];
-      ok = get_n<2>(ptr, m, lane, flag, deadline, R->err, w);
+    const int per_u = (X - 1) * Y;
+    for (int J = wr; J < a.Umax * per_u && ok; J += WS) {
+      const int u = J / per_u, r = J % per_u, j = (c + 1 + r / Y) % X, s = r % Y, js = j * Y + s;
+      if (u >= a.g_U[js]) continue;
+      uint4 w;
+      ok = get(inbox(me, a.hag_off[par], a.hag_stride, j), (unsigned long long)a.g_uoff[js] + u, lane, flag, deadline,
+               R->err, &w);
       if (!ok) break;
-      for (int h = 0; h < m; ++h)
-        ustore(a.g_co[jv[h]] + a.g_cs[jsv[h]] + (unsigned long long)uu[h] * UE + eoff, lane_n(a.g_sl[jsv[h]], uu[h]),
-               w[h]);
+      ustore(a.g_co[j] + a.g_cs[js] + (unsigned long long)u * UE + eoff, lane_n(a.g_sl[js], u), w);
     }
   }
   if (!ok && lane == 0) atomicCAS_system(R->err, 0, kErrTimeout);
