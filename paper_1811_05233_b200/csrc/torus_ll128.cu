@@ -35,7 +35,10 @@
 namespace torus {
 namespace {
 
-constexpr int kL128Threads = 512;
+#ifndef TORUS_LL128_THREADS
+#define TORUS_LL128_THREADS 512
+#endif
+constexpr int kL128Threads = TORUS_LL128_THREADS;
 constexpr int kL128Warps = kL128Threads / 32;
 enum { kSA = 0, kSB = 1, kSC = 2, kSD = 3, kSE = 4, kL128Stages = 5 };
 
@@ -83,6 +86,38 @@ __device__ __forceinline__ bool get(const char* stream, unsigned long long u, in
     if (__all_sync(0xffffffffu, line_ok)) {
       const bool fl = (lane & 7) == 7;
       *v = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), fl ? 0u : (uint32_t)hi, fl ? 0u : (uint32_t)(hi >> 32));
+      return true;
+    }
+    if ((++spin & 255u) == 0) {
+      int bad = 0;
+      if (lane == 0) bad = gtimer() > deadline || ((spin & 4095u) == 0 && *(volatile const int*)err);
+      if (__shfl_sync(0xffffffffu, bad, 0)) return false;
+    }
+  }
+}
+
+// two units in one load round (scalar registers, no arrays): the copy stages and a
+// two-operand fold hide one line latency behind the other
+__device__ __forceinline__ bool get2(const char* p0, const char* p1, int lane, uint64_t flag,
+                                     unsigned long long deadline, const int* err, uint4* v0, uint4* v1) {
+  const bool fl = (lane & 7) == 7;
+  bool need0 = true, need1 = true;
+  uint64_t lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;
+  unsigned spin = 0;
+  for (;;) {
+    if (need0) ld_line(p0, lo0, hi0);
+    if (need1) ld_line(p1, lo1, hi1);
+    if (need0) {
+      const int ok = __shfl_sync(0xffffffffu, (int)(!fl || hi0 == flag), (lane & ~7) | 7);
+      if (__all_sync(0xffffffffu, ok)) need0 = false;
+    }
+    if (need1) {
+      const int ok = __shfl_sync(0xffffffffu, (int)(!fl || hi1 == flag), (lane & ~7) | 7);
+      if (__all_sync(0xffffffffu, ok)) need1 = false;
+    }
+    if (!need0 && !need1) {
+      *v0 = make_uint4((uint32_t)lo0, (uint32_t)(lo0 >> 32), fl ? 0u : (uint32_t)hi0, fl ? 0u : (uint32_t)(hi0 >> 32));
+      *v1 = make_uint4((uint32_t)lo1, (uint32_t)(lo1 >> 32), fl ? 0u : (uint32_t)hi1, fl ? 0u : (uint32_t)(hi1 >> 32));
       return true;
     }
     if ((++spin & 255u) == 0) {
@@ -190,7 +225,17 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
     for (int u = wr; u < a.g_U[cr] && ok; u += WS) {
       const int nr = lane_n(a.g_sl[cr], u);
       Acc acc[VE];
-      for (int kk = 1; kk <= Y && ok; ++kk) {
+      if (Y == 2) {  // both rows in one load round: fold order rho+1, rho
+        uint4 w0, w1;
+        ok = get2(lane_ptr(inbox(me, a.v_off[par], a.v_stride, (rho + 1) % 2), u, lane),
+                  lane_ptr(inbox(me, a.v_off[par], a.v_stride, rho), u, lane), lane, flag, deadline, R->err, &w0,
+                  &w1);
+        Acc t[VE];
+        unpack<W>(w0, acc);
+        unpack<W>(w1, t);
+        acc_add<W>(acc, t);
+      }
+      for (int kk = 1; kk <= Y && ok && Y != 2; ++kk) {
         const int i = (rho + kk) % Y;
         uint4 w;
         ok = get(inbox(me, a.v_off[par], a.v_stride, i), u, lane, flag, deadline, R->err, &w);
@@ -215,28 +260,69 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
     }
   } else if (stage == kSD && Y > 1) {
     // ---- D: a column peer's reduced sub-chunk -> my buffer + the row peers' HAG inboxes ----
-    for (int J = wr; J < a.Umax * (Y - 1) && ok; J += WS) {
-      const int u = J / (Y - 1), i = (rho + 1 + J % (Y - 1)) % Y, ci = c * Y + i;
-      if (u >= a.g_U[ci]) continue;
-      uint4 w;
-      ok = get(inbox(me, a.ag_off[par], a.ag_stride, i), u, lane, flag, deadline, R->err, &w);
-      if (!ok) break;
+    const int nj = a.Umax * (Y - 1);
+    auto job = [&](int J, int* u, int* ci) -> bool {
+      if (J >= nj) return false;
+      *u = J / (Y - 1);
+      *ci = c * Y + (rho + 1 + J % (Y - 1)) % Y;
+      return *u < a.g_U[*ci];
+    };
+    auto emit = [&](int u, int ci, uint4 w) {
       ustore(a.g_co[c] + a.g_cs[ci] + (unsigned long long)u * UE + eoff, lane_n(a.g_sl[ci], u), w);
       for (int jj = 1; jj < X; ++jj)
         put(inbox(rho * X + (c + jj) % X, a.hag_off[par], a.hag_stride, c), (unsigned long long)a.g_uoff[ci] + u,
             lane, w, flag);
+    };
+    for (int J = wr; J < nj && ok; J += 2 * WS) {  // two jobs per load round
+      int u0, c0, u1, c1;
+      const bool h0 = job(J, &u0, &c0), h1 = job(J + WS, &u1, &c1);
+      uint4 w0, w1;
+      if (h0 && h1) {
+        ok = get2(lane_ptr(inbox(me, a.ag_off[par], a.ag_stride, c0 - c * Y), u0, lane),
+                  lane_ptr(inbox(me, a.ag_off[par], a.ag_stride, c1 - c * Y), u1, lane), lane, flag, deadline,
+                  R->err, &w0, &w1);
+        if (!ok) break;
+        emit(u0, c0, w0);
+        emit(u1, c1, w1);
+      } else if (h0 || h1) {
+        const int u = h0 ? u0 : u1, ci = h0 ? c0 : c1;
+        ok = get(inbox(me, a.ag_off[par], a.ag_stride, ci - c * Y), u, lane, flag, deadline, R->err, &w0);
+        if (!ok) break;
+        emit(u, ci, w0);
+      }
     }
   } else if (stage == kSE && X > 1) {
     // ---- E: a row peer's completed chunk -> my buffer (wire -> dtype) ----
-    const int per_u = (X - 1) * Y;
-    for (int J = wr; J < a.Umax * per_u && ok; J += WS) {
-      const int u = J / per_u, r = J % per_u, j = (c + 1 + r / Y) % X, s = r % Y, js = j * Y + s;
-      if (u >= a.g_U[js]) continue;
-      uint4 w;
-      ok = get(inbox(me, a.hag_off[par], a.hag_stride, j), (unsigned long long)a.g_uoff[js] + u, lane, flag, deadline,
-               R->err, &w);
-      if (!ok) break;
-      ustore(a.g_co[j] + a.g_cs[js] + (unsigned long long)u * UE + eoff, lane_n(a.g_sl[js], u), w);
+    const int per_u = (X - 1) * Y, nj = a.Umax * per_u;
+    auto job = [&](int J, int* u, int* js) -> bool {
+      if (J >= nj) return false;
+      *u = J / per_u;
+      const int r = J % per_u;
+      *js = ((c + 1 + r / Y) % X) * Y + r % Y;
+      return *u < a.g_U[*js];
+    };
+    auto src = [&](int u, int js) -> const char* {
+      return lane_ptr(inbox(me, a.hag_off[par], a.hag_stride, js / Y), (unsigned long long)a.g_uoff[js] + u, lane);
+    };
+    auto emit = [&](int u, int js, uint4 w) {
+      ustore(a.g_co[js / Y] + a.g_cs[js] + (unsigned long long)u * UE + eoff, lane_n(a.g_sl[js], u), w);
+    };
+    for (int J = wr; J < nj && ok; J += 2 * WS) {  // two jobs per load round
+      int u0, j0, u1, j1;
+      const bool h0 = job(J, &u0, &j0), h1 = job(J + WS, &u1, &j1);
+      uint4 w0, w1;
+      if (h0 && h1) {
+        ok = get2(src(u0, j0), src(u1, j1), lane, flag, deadline, R->err, &w0, &w1);
+        if (!ok) break;
+        emit(u0, j0, w0);
+        emit(u1, j1, w1);
+      } else if (h0 || h1) {
+        const int u = h0 ? u0 : u1, js = h0 ? j0 : j1;
+        ok = get(inbox(me, a.hag_off[par], a.hag_stride, js / Y), (unsigned long long)a.g_uoff[js] + u, lane, flag,
+                 deadline, R->err, &w0);
+        if (!ok) break;
+        emit(u, js, w0);
+      }
     }
   }
   if (!ok && lane == 0) atomicCAS_system(R->err, 0, kErrTimeout);
