@@ -36,7 +36,7 @@ namespace torus {
 namespace {
 
 #ifndef TORUS_LL128_THREADS
-#define TORUS_LL128_THREADS 512
+#define TORUS_LL128_THREADS 1024
 #endif
 constexpr int kL128Threads = TORUS_LL128_THREADS;
 constexpr int kL128Warps = kL128Threads / 32;
@@ -176,13 +176,26 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
 
   if (stage == kSA && X > 1) {
     // ---- A: my buffer's shares of my row peers' chunks -> their H inboxes ----
-    const int per_u = (X - 1) * Y;
-    for (int J = wr; J < a.Umax * per_u && ok; J += WS) {
-      const int u = J / per_u, r = J % per_u, j = (c + 1 + r / Y) % X, s = r % Y, js = j * Y + s;
-      if (u >= a.g_U[js]) continue;
-      const int nr = lane_n(a.g_sl[js], u);
-      const uint4 v = uload(a.g_co[j] + a.g_cs[js] + (unsigned long long)u * UE + eoff, nr);
-      put(inbox(rho * X + j, a.h_off[par], a.h_stride, c), (unsigned long long)a.g_uoff[js] + u, lane, v, flag);
+    const int per_u = (X - 1) * Y, nj = a.Umax * per_u;
+    for (int J0 = wr; J0 < nj; J0 += 2 * WS) {  // two units per iteration: both loads in flight
+      uint4 v[2];
+      int js2[2], u2[2], j2[2], m = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int J = J0 + h * WS;
+        if (J >= nj) continue;
+        const int u = J / per_u, r = J % per_u, j = (c + 1 + r / Y) % X, s = r % Y, js = j * Y + s;
+        if (u >= a.g_U[js]) continue;
+        v[m] = uload(a.g_co[j] + a.g_cs[js] + (unsigned long long)u * UE + eoff, lane_n(a.g_sl[js], u));
+        js2[m] = js;
+        u2[m] = u;
+        j2[m++] = j;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (h < m)
+          put(inbox(rho * X + j2[h], a.h_off[par], a.h_stride, c), (unsigned long long)a.g_uoff[js2[h]] + u2[h], lane,
+              v[h], flag);
     }
   } else if (stage == kSB) {
     // ---- B: fold my chunk (columns c+1, ..., c), round; push to the column owner ----
@@ -191,11 +204,12 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
       if (u >= a.g_U[cs]) continue;
       const int nr = lane_n(a.g_sl[cs], u);
       const unsigned long long e = a.g_co[c] + a.g_cs[cs] + (unsigned long long)u * UE + eoff;
+      const uint4 own = uload(e, nr);  // issued first: its HBM latency overlaps the inbox polls
       Acc acc[VE];
       for (int kk = 1; kk <= X && ok; ++kk) {
         const int j = (c + kk) % X;
         uint4 w;
-        if (j == c) w = uload(e, nr);
+        if (j == c) w = own;
         else ok = get(inbox(me, a.h_off[par], a.h_stride, j), (unsigned long long)a.g_uoff[cs] + u, lane, flag,
                       deadline, R->err, &w);
         Acc t[VE];

@@ -8,7 +8,7 @@ namespace torus {
 constexpr int kL128Line = 128;      // bytes per line: 120 bytes of data + an 8-byte flag
 constexpr int kL128Unit = 4 * kL128Line;  // one warp moves four lines = 30 wire vectors
 #ifndef TORUS_LL128_THREADS
-#define TORUS_LL128_THREADS 512
+#define TORUS_LL128_THREADS 1024
 #endif
 constexpr int kL128CtaWarps = TORUS_LL128_THREADS / 32;
 
