@@ -88,7 +88,10 @@ __device__ __forceinline__ bool get(const char* stream, unsigned long long u, in
       *v = make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), fl ? 0u : (uint32_t)hi, fl ? 0u : (uint32_t)(hi >> 32));
       return true;
     }
-    if ((++spin & 255u) == 0) {
+    // back off once the lines are clearly not there yet: thousands of warps re-reading
+    // the same L2 lines at full speed slow the NVLink writes that must land in them
+    if (++spin > 4) __nanosleep(spin > 64 ? 256 : 64);
+    if ((spin & 255u) == 0) {
       int bad = 0;
       if (lane == 0) bad = gtimer() > deadline || ((spin & 4095u) == 0 && *(volatile const int*)err);
       if (__shfl_sync(0xffffffffu, bad, 0)) return false;
@@ -120,7 +123,10 @@ __device__ __forceinline__ bool get2(const char* p0, const char* p1, int lane, u
       *v1 = make_uint4((uint32_t)lo1, (uint32_t)(lo1 >> 32), fl ? 0u : (uint32_t)hi1, fl ? 0u : (uint32_t)(hi1 >> 32));
       return true;
     }
-    if ((++spin & 255u) == 0) {
+    // back off once the lines are clearly not there yet: thousands of warps re-reading
+    // the same L2 lines at full speed slow the NVLink writes that must land in them
+    if (++spin > 4) __nanosleep(spin > 64 ? 256 : 64);
+    if ((spin & 255u) == 0) {
       int bad = 0;
       if (lane == 0) bad = gtimer() > deadline || ((spin & 4095u) == 0 && *(volatile const int*)err);
       if (__shfl_sync(0xffffffffu, bad, 0)) return false;
