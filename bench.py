@@ -310,6 +310,10 @@ def run_torus(args):
     t_local = sum(times) / len(times)
     t = gather_max(t_local, world)
     t_min = gather_max(min(times), world)
+    srt = sorted(times)
+    t_p50 = gather_max(srt[len(srt) // 2], world)
+    t_p90 = gather_max(srt[min(len(srt) - 1, (9 * len(srt)) // 10)], world)
+    t_max = gather_max(srt[-1], world)
     algbw = S / t / 1e9
     busbw = algbw * bus
     if comm.async_error():
@@ -440,6 +444,7 @@ def run_torus(args):
                    "message_bytes": S, "l2": "flushed before every timed call (256 MiB write, then 256 MiB read so no dirty flush lines are written back inside the timed call)",
                    "value_is": "busbw" if world > 1 else "algbw (busbw is 0 at N=1)"},
         "algbw": algbw, "busbw": busbw, "us_per_call": t * 1e6, "us_per_call_min": t_min * 1e6,
+        "us_per_call_p50": t_p50 * 1e6, "us_per_call_p90": t_p90 * 1e6, "us_per_call_max": t_max * 1e6,
         "frac_nvlink_900": busbw / NVLINK_NOMINAL if world > 1 else None,
         "gpu_launches": launches * args.steps,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "nccl": nccl, "clocks": clk,

@@ -37,8 +37,10 @@ for spec in rest:
         continue
     d = json.loads(line[-1])
     out = {"n": n, "env": spec, "extra": " ".join(extra), "us": d["us_per_call"], "us_min": d["us_per_call_min"],
+           "us_p50": d.get("us_per_call_p50"), "us_p90": d.get("us_per_call_p90"), "us_max": d.get("us_per_call_max"),
            "busbw": d["busbw"], "kernel": d["roofline"].get("kernel"), "sanity": d["sanity"]}
     print(f"{spec:60s} {d['us_per_call']:8.1f} us  busbw {d['busbw']:6.1f}  min {d['us_per_call_min']:7.1f}  "
+          f"p50 {d.get('us_per_call_p50', 0):7.1f} p90 {d.get('us_per_call_p90', 0):7.1f} max {d.get('us_per_call_max', 0):8.1f}  "
           f"{d['roofline'].get('kernel')} ok={d['sanity'].get('ranks_identical')}", flush=True)
     with open(os.path.join(ROOT, "gpurun_out", "sweep.jsonl"), "a") as f:
         f.write(json.dumps(out) + "\n")
