@@ -90,7 +90,7 @@ __device__ __forceinline__ bool get(const char* stream, unsigned long long u, in
     }
     // back off once the lines are clearly not there yet: thousands of warps re-reading
     // the same L2 lines at full speed slow the NVLink writes that must land in them
-    if (++spin > 4) __nanosleep(spin > 64 ? 256 : 64);
+    if (++spin > 32) __nanosleep(spin > 256 ? 256 : 32);
     if ((spin & 255u) == 0) {
       int bad = 0;
       if (lane == 0) bad = gtimer() > deadline || ((spin & 4095u) == 0 && *(volatile const int*)err);
@@ -125,7 +125,7 @@ __device__ __forceinline__ bool get2(const char* p0, const char* p1, int lane, u
     }
     // back off once the lines are clearly not there yet: thousands of warps re-reading
     // the same L2 lines at full speed slow the NVLink writes that must land in them
-    if (++spin > 4) __nanosleep(spin > 64 ? 256 : 64);
+    if (++spin > 32) __nanosleep(spin > 256 ? 256 : 32);
     if ((spin & 255u) == 0) {
       int bad = 0;
       if (lane == 0) bad = gtimer() > deadline || ((spin & 4095u) == 0 && *(volatile const int*)err);
