@@ -103,7 +103,7 @@ struct torus_comm {
   NvlsState nvls;                         // NVLS (multicast) variant, NEXT-4
   size_t ll2_max = 0;                     // two-shot LL up to this many wire bytes (N >= 3)
   // ---- knobs, read ONCE at init (they must agree across ranks: torus_comm_config) ----
-  int mode = 1;                           // kModePush (default) / kModePull / kModeTma
+  int mode = 3;                           // kModeLL128 (default) / kModePush / kModePull / kModeTma
   unsigned long long one_tile_max = 4096; // push kernel: single-tile threshold (vectors)
   unsigned long long mid_tiles = 1;       // push kernel: tiles per slice below it
   int fence_early = 0;                    // push kernel experiment
@@ -329,9 +329,11 @@ int pick_ctas(int device, int nlocal, int ctas_req) {
 void read_knobs(torus_comm* c) {
   c->timeout_ns = env_size("TORUS_TIMEOUT_MS", 30000) * 1000000ull;
   const char* k = getenv("TORUS_KERNEL");
-  // default: the push kernel -- faster than the pull kernel at every measured size on 2
-  // and 4 B200s (profiles/r02_sizes_n*.jsonl); TORUS_KERNEL=pull selects the pull kernel
-  c->mode = kModePush;
+  // default: the LL128 push kernel (fence-free flag-in-data lines; grids with X, Y <= 8) --
+  // 100 us vs 120 (push kernel) and 124 (NCCL) at 1x2, 161 vs 175 and 161 at 2x2
+  // (profiles/r02_ll128_*); TORUS_KERNEL=push / pull / tma select the others
+  c->mode = kModeLL128;
+  if (k && (strcmp(k, "push") == 0 || strcmp(k, "ldg") == 0)) c->mode = kModePush;
   if (k && strcmp(k, "pull") == 0) c->mode = kModePull;
   if (k && strcmp(k, "tma") == 0) c->mode = kModeTma;
   if (k && strcmp(k, "ll128") == 0) c->mode = kModeLL128;
@@ -1455,7 +1457,8 @@ int torus_vallreduce_multi(torus_comm_t c, void* const* ptrs, const size_t* coun
   for (size_t i = 0; i < (size_t)c->nlocal * ntensors; ++i)
     if (counts[i % ntensors] && !ptrs[i]) return fail(TORUS_ERR_INVALID_ARG, "tensor %zu is NULL", i);
   if (total == 0) return TORUS_OK;
-  if (plan_route(c, total, dtype, wire) != kRoutePush)
+  const int mroute = plan_route(c, total, dtype, wire);
+  if (mroute != kRoutePush && mroute != kRouteLL128)
     return fail(TORUS_ERR_UNSUPPORTED, "virtual multi-tensor calls take the multi-phase kernel only");
   const MultiSeg* d = nullptr;
   int rc = seg_table(c, ptrs, counts, ntensors, &d);
@@ -1497,7 +1500,8 @@ int torus_allreduce_multi(torus_comm_t c, void* const* ptrs, const size_t* count
   }
   if (total == 0) return TORUS_OK;
   cudaStream_t s0 = static_cast<cudaStream_t>(stream);
-  if (plan_route(c, total, dtype, wire) == kRoutePush) {
+  const int mroute = plan_route(c, total, dtype, wire);
+  if (mroute == kRoutePush || mroute == kRouteLL128) {
     // fused: the multi-phase kernel reads the tensors with the cast
     // fused and writes them back with the up-cast fused -- no staging, no pack / unpack
     const MultiSeg* d = nullptr;

@@ -71,16 +71,16 @@ def run_virtual(vt, ins, dtype, wire, op):
 # tma: the push kernel's TMA-staged variant
 # ll / ll2: the one-shot / two-shot small-message kernels (NEXT-2) forced for every size
 # these tests use (ll2: grids with N >= 3; N = 2 falls back to the multi-phase path)
-KERNELS = ["pull", "ldg", "ldgt", "tma", "ll", "ll2"]
+KERNELS = ["ll128", "pull", "ldg", "ldgt", "tma", "ll", "ll2"]
 LL_FORCED = 1 << 20  # 1 MiB of wire per rank: covers D = 200,003 f32
 
 
-def make_vt(X, Y, ws=0, kernel="pull", ll=None):
+def make_vt(X, Y, ws=0, kernel="ll128", ll=None):
     """The kernel is chosen from TORUS_KERNEL / TORUS_LL_MAX_BYTES when the communicator
     is built; the multi-phase variants run with the one-shot path off (ll=0)."""
     import os
     from paper_1811_05233_b200 import VirtualTorus
-    env = {"TORUS_KERNEL": {"tma": "tma", "ldg": "push", "ldgt": "push", "pull": "pull"}.get(kernel, "push"),
+    env = {"TORUS_KERNEL": {"tma": "tma", "ldg": "push", "ldgt": "push", "pull": "pull"}.get(kernel, "ll128"),
            "TORUS_TILE": "256" if kernel == "ldgt" else "0",
            "TORUS_LL_MAX_BYTES": str(ll if ll is not None else (LL_FORCED if kernel == "ll" else 0)),
            "TORUS_LL2_MAX_BYTES": str(LL_FORCED if kernel == "ll2" else 0)}
@@ -107,7 +107,7 @@ def vgrids():
     from collections import OrderedDict
     made = OrderedDict()
 
-    def get(X, Y, ws=0, kernel="pull"):
+    def get(X, Y, ws=0, kernel="ll128"):
         key = (X, Y, ws, kernel)
         if key in made:
             made.move_to_end(key)
@@ -139,7 +139,7 @@ def test_virtual_grid_bit_exact(vgrids, X, Y, dtype, wire, op, kernel):
             assert_same(got[r], ref[r], f"{X}x{Y} {dtype}/{wire} {op} D={D} rank {r}")
 
 
-@pytest.mark.parametrize("kernel", ["pull", "ldg", "ldgt", "tma"])
+@pytest.mark.parametrize("kernel", ["ll128", "pull", "ldg", "ldgt", "tma"])
 @pytest.mark.parametrize("X,Y", [(2, 2), (2, 4), (1, 4)])
 @pytest.mark.parametrize("dtype,wire", [("f16", "f16"), ("f32", "bf16"), ("i32", "i32")])
 def test_multi_round(vgrids, X, Y, dtype, wire, kernel):
@@ -226,7 +226,7 @@ def test_single_rank_cast_scale():
         vt.destroy()
 
 
-@pytest.mark.parametrize("kernel", ["pull", "ldg"])
+@pytest.mark.parametrize("kernel", ["ll128", "pull", "ldg"])
 def test_full_size_resnet50_exhaustive(kernel):
     """BASELINE config 2 at full size, in the bench's launch configuration (2x4 grid,
     fp16, mean, one round): EVERY element of every rank vs the oracle's step-by-step
@@ -237,7 +237,8 @@ def test_full_size_resnet50_exhaustive(kernel):
     try:
         R = vt.round_elems(torch.float16)
         assert R >= D, "north-star message must be a single round"
-        assert vt.route(D, torch.float16) == ("torus_pull_kernel" if kernel == "pull" else "torus_kernel")
+        assert vt.route(D, torch.float16) == {"pull": "torus_pull_kernel", "ldg": "torus_kernel"}.get(
+            kernel, "torus_ll128_kernel")
         ins = synthetic.make_all("grad", D, 8, "f16")
         ts = [_np_to_dev(a, "f16") for a in ins]
         vt.all_reduce(ts, op="mean")
@@ -531,7 +532,7 @@ def test_fused_multi_tensor_bucket(X, Y, dtype, wire):
             ins = synthetic.make_all("grad" if dtype == "f16" else "normal", D, N, dtype, salt=80 + k)
             buckets = [list(torch.split(_np_to_dev(a, dtype), sz)) for a in ins]
             buckets = [[t.contiguous() for t in b] for b in buckets]
-            assert vt.route(D, TD[dtype], TD[wire]) == "torus_kernel"
+            assert vt.route(D, TD[dtype], TD[wire]) in ("torus_kernel", "torus_ll128_kernel")
             vt.all_reduce_multi(buckets, op="mean", wire=TD[wire])
             torch.cuda.synchronize()
             assert vt.async_error() == 0
