@@ -204,7 +204,7 @@ unsigned long long round_elems(const torus_comm* c, int wire) {
   unsigned long long per_k;
   if (c->mode == kModePull) {
     per_k = 2 * q * (X * Y + ((X > 1 && Y > 1) ? 2 : 1) * Y);
-  } else if (c->mode == kModeLL128) {
+  } else if (c->mode == kModeLL128 && X * Y > 1) {
     // per parity: H and HAG inboxes (X > 1) R each, V and AG inboxes (Y > 1) R/X each, as
     // 128-byte lines holding 120 bytes (x 16/15) -- plus a 10% margin for stream padding
     const unsigned long long slots = (X > 1 ? 2 * X * Y : 0) + (Y > 1 ? 2 * Y : 0);
