@@ -1072,7 +1072,8 @@ int launch_ll128_rounds(torus_comm* c, void* const* bufs, size_t count, int dtyp
   a.ctas = std::max(1, (c->ll128_ctas > 0 ? std::min(c->ll128_ctas, sms) : sms) / c->nlocal);
   const int warps = a.ctas * kL128CtaWarps;
   // warps per stage ~ each stage's loads + stores per unit x units (x TORUS_LL128_W)
-  double w[5] = {X > 1 ? 2.0 * (X - 1) * Y : 0, (double)Y * (X + 1), Y > 1 ? 2.0 * Y + X - 1 : 0,
+  // (B with Y == 1 also pushes its final values to the X-1 row peers)
+  double w[5] = {X > 1 ? 2.0 * (X - 1) * Y : 0, (double)Y * (X + (Y > 1 ? 1 : X)), Y > 1 ? 2.0 * Y + X - 1 : 0,
                  Y > 1 ? (double)(Y - 1) * (X + 1) : 0, X > 1 ? 2.0 * (X - 1) * Y : 0};
   for (int k = 0; k < 5; ++k) w[k] *= c->ll128_w[k];
   double ws = 0;
