@@ -112,7 +112,7 @@ class Clocks:
             try:
                 self.fh = open(self.path, "w")
                 self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}",
-                                              "--format=csv,noheader,nounits", "-lms", "50"],
+                                              "--format=csv,noheader,nounits", "-lms", "200"],
                                              stdout=self.fh, stderr=subprocess.DEVNULL)
             except OSError:
                 self.proc = None
@@ -394,6 +394,8 @@ def run_torus(args):
     launches = comm.launches(D, TD[dtype_s], TD[wire_s])
     # ---- roofline of the dominant (only) kernel ----
     if world > 1:
+        kname = kernel_name(comm, D, TD, dtype_s, wire_s)
+        tkey = "ll128" if kname == "torus_ll128_kernel" else "torus"
         alg_bytes = bus * S                        # NVLink bytes per rank per call
         achieved = alg_bytes / t / 1e9             # t is per call (all rounds)
         roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_MEASURED,
@@ -401,11 +403,11 @@ def run_torus(args):
                 "frac_of_nominal_900": achieved / NVLINK_NOMINAL,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction "
                                "(MEASURED_PEAKS.json has no NVLink entry)",
-                "traffic": load_traffic(f"torus_{X}x{Y}"), "kernel": kernel_name(comm, D, TD, dtype_s, wire_s),
+                "traffic": load_traffic(f"{tkey}_{X}x{Y}"), "kernel": kname,
                 "algorithmic_bytes_per_call": alg_bytes,
-                "nvlink_tx_bytes_ncu": load_traffic(f"torus_{X}x{Y}_nvltx"),
-                "nvlink_tx_user_bytes_ncu": load_traffic(f"torus_{X}x{Y}_nvltx_user"),
-                "traffic_source": "profiles/traffic.json (ncu on rank 0 of a real run, profiles/r02_ncu_push_*.csv)",
+                "nvlink_tx_bytes_ncu": load_traffic(f"{tkey}_{X}x{Y}_nvltx"),
+                "nvlink_tx_user_bytes_ncu": load_traffic(f"{tkey}_{X}x{Y}_nvltx_user"),
+                "traffic_source": "profiles/traffic.json (ncu on rank 0 of a real run, profiles/r02_ncu_*.csv)",
                 "nvlink_bytes_per_call_nvml": nvl_torus}
     else:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(

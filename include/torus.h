@@ -260,7 +260,7 @@ TORUS_API size_t torus_comm_ll_max_bytes(torus_comm_t comm);
 /* Mid-size threshold (N >= 3): calls above the one-shot threshold and up to this many
  * wire bytes run the two-shot kernel -- each rank sends every sub-chunk C_{c,s} to its
  * torus owner (s, c), the owner folds it in the torus order and broadcasts it back;
- * bit-identical to the multi-phase path.  Env TORUS_LL2_MAX_BYTES (default 8 MiB at
+ * bit-identical to the multi-phase path.  Env TORUS_LL2_MAX_BYTES (default 4 MiB at
  * N >= 3; 0 disables; same on every rank); needs ~8x that many bytes of slab region.
  * 0 if disabled, N < 3 or comm is NULL. */
 TORUS_API size_t torus_comm_ll2_max_bytes(torus_comm_t comm);

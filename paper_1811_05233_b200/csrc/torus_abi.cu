@@ -189,7 +189,9 @@ size_t ll_max_env(int N) {
   else if (N >= 3) dflt = ((3ull << 19) / (N - 1)) & ~(size_t)15;
   return env_size("TORUS_LL_MAX_BYTES", dflt);
 }
-size_t ll2_max_env(int N) { return env_size("TORUS_LL2_MAX_BYTES", N >= 3 ? (8ull << 20) : 0); }
+// two-shot up to 4 MiB at N >= 3: above it the LL128 multi-phase kernel is faster (8 MB at
+// 2x2: 45 us vs 58, profiles/r02_thresholds.txt)
+size_t ll2_max_env(int N) { return env_size("TORUS_LL2_MAX_BYTES", N >= 3 ? (4ull << 20) : 0); }
 
 // Round capacity for a wire type (elements): R = k * q * X * Y with
 // h_in (X>1: X slots of R/X) + v_in (Y slots of R/(XY)) + chunk (R/X) in the data region.

@@ -281,7 +281,7 @@ def test_small_and_large_calls_interleaved(X, Y):
 @pytest.mark.parametrize("X,Y", [(2, 1), (2, 2), (2, 4)])
 def test_default_ll_threshold(X, Y):
     """Default thresholds: one-shot 6 MiB at N = 2, 1.5 MiB / (N-1) (16-byte multiple) at
-    N >= 3; two-shot 8 MiB at N >= 3, off at N = 2."""
+    N >= 3; two-shot 4 MiB at N >= 3, off at N = 2."""
     import os
     if "TORUS_LL_MAX_BYTES" in os.environ or "TORUS_LL2_MAX_BYTES" in os.environ:
         pytest.skip("threshold overridden in the environment")
@@ -290,7 +290,7 @@ def test_default_ll_threshold(X, Y):
     try:
         N = X * Y
         assert vt.ll_max_bytes() == (6 << 20 if N == 2 else ((3 << 19) // (N - 1)) & ~15)
-        assert vt.ll2_max_bytes() == (0 if N == 2 else 8 << 20)
+        assert vt.ll2_max_bytes() == (0 if N == 2 else 4 << 20)
     finally:
         vt.destroy()
 
