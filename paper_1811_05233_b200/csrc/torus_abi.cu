@@ -800,7 +800,7 @@ int torus_comm_trace(torus_comm_t c, unsigned long long* host, size_t bytes) {
 
 int torus_probe(torus_comm_t c, int mode, size_t bytes, int iters, int ctas, unsigned long long* ns_out,
                 torus_stream_t stream) {
-  if (!c || c->virt || mode < 0 || mode > 9) return fail(TORUS_ERR_INVALID_ARG, "probe args");
+  if (!c || c->virt || mode < 0 || mode > 11) return fail(TORUS_ERR_INVALID_ARG, "probe args");
   const size_t room = c->slab_size - c->layout.data_off;
   if (mode != 2 && (bytes == 0 || (bytes / 16) * 16 * (size_t)(c->world + 1) > room))
     return fail(TORUS_ERR_INVALID_ARG, "probe bytes %zu exceed the slab", bytes);

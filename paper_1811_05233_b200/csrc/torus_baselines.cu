@@ -52,6 +52,26 @@ __global__ void __launch_bounds__(512) probe_kernel(const RankDev* ranks, unsign
     return;
   }
   const unsigned long long per = nvec / (N - 1);
+  if (mode == 10 || mode == 11) {
+    // store-injection probe: every thread pushes a register pattern to its peers with
+    // 16-byte (10) or 32-byte (11) volatile stores -- no loads in the loop
+    const unsigned long long a = 0x0123456789abcdefull ^ tid, bb = a * 3;
+    for (int pp = 1; pp < N; ++pp) {
+      const int p = (me + pp) % N;
+      char* dst = R->ws[p] + data_off + (unsigned long long)me * per * 16;
+      if (mode == 10) {
+        for (unsigned long long v = (unsigned long long)b * blockDim.x + tid; v < per;
+             v += (unsigned long long)G * blockDim.x)
+          asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(dst + v * 16), "l"(a), "l"(bb) : "memory");
+      } else {
+        for (unsigned long long v = (unsigned long long)b * blockDim.x + tid; v < per / 2;
+             v += (unsigned long long)G * blockDim.x)
+          asm volatile("st.volatile.global.v4.u64 [%0], {%1, %2, %1, %2};" ::"l"(dst + v * 32), "l"(a), "l"(bb)
+                       : "memory");
+      }
+    }
+    return;
+  }
   for (int pp = 1; pp < N; ++pp) {
     const int p = (me + pp) % N;
     if (mode == 0) {

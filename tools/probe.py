@@ -24,10 +24,11 @@ def main():
     nbytes = 51_114_064 * 2 * (world - 1) // world // 16 * 16  # 2(N-1)/N * S
     out = []
     only = os.environ.get("PROBE_ONLY")
-    for mode, name in ((0, "push"), (1, "pull"), (4, "tma_push"), (5, "tma_pull"), (3, "local_copy")):
+    for mode, name in ((0, "push"), (1, "pull"), (4, "tma_push"), (5, "tma_pull"), (3, "local_copy"),
+                       (10, "store16"), (11, "store32")):
         if only and name not in only.split(","):
             continue
-        for ctas in ((16, 32, 64, 148, 296) if mode < 4 else (16, 32, 64, 148)):
+        for ctas in ((16, 32, 64, 148, 296) if mode < 4 or mode >= 10 else (16, 32, 64, 148)):
             for _ in range(3):
                 comm.probe(mode, nbytes, ctas=ctas)
             torch.cuda.synchronize()
