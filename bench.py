@@ -86,6 +86,17 @@ def barrier(world):
         dist.barrier()
 
 
+def device_align(world):
+    """Line the GPUs up right before a timed loop.  The host barrier returns at different
+    times on different ranks (100-300 us apart), and a collective's first timed call would
+    absorb that skew waiting for its slowest peer.  A one-element NCCL all-reduce enqueued
+    on the stream releases every GPU together; the timed calls are enqueued behind it."""
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.all_reduce(torch.zeros(1, device="cuda"))
+
+
 def gather_max(x, world):
     if world == 1:
         return x
@@ -298,6 +309,9 @@ def run_torus(args):
           for _ in range(args.steps)]
     torch.cuda.synchronize()
     barrier(world)
+    device_align(world)
+    evict(0)
+    call()  # untimed: the first call after the idle barrier pays a wake-up (profiles/r02_ab*.txt: call 0)
     for s in range(args.steps):
         evict(s)                                # L2 evicted and clean, untimed
         ev[s][0].record(stream)
@@ -343,6 +357,9 @@ def run_torus(args):
         evn = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(args.steps)]
         ns = torch.cuda.current_stream()
+        device_align(world)
+        evict(0)
+        dist.all_reduce(buf, op=op)  # untimed, as for the torus arm
         for s in range(args.steps):
             evict(s)
             evn[s][0].record(ns)
@@ -378,6 +395,7 @@ def run_torus(args):
         torch.cuda.synchronize()
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        device_align(world)
         e0.record(stream)
         for s in range(args.steps):
             view.copy_(hin, non_blocking=True)

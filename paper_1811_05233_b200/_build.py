@@ -38,11 +38,21 @@ FLAGS = [
 ]
 
 
+def _dep_time(src: pathlib.Path) -> float:
+    return max([src.stat().st_mtime] + [h.stat().st_mtime for h in _deps(src)])
+
+
 def stale() -> bool:
+    """The library is missing, older than a source or header, or linked from an object
+    compiled before its source last changed (an edit made while nvcc was running)."""
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    return any(p.stat().st_mtime > t for p in SOURCES + HEADERS)
+    if any(p.stat().st_mtime > t for p in SOURCES + HEADERS):
+        return True
+    odir = PKG / "build" / "default"
+    return any(not (odir / f"{s.stem}.o").exists() or (odir / f"{s.stem}.o").stat().st_mtime < _dep_time(s)
+               for s in SOURCES)
 
 
 def build(force: bool = False, verbose: bool = False, out: pathlib.Path | None = None,
@@ -59,15 +69,15 @@ def build(force: bool = False, verbose: bool = False, out: pathlib.Path | None =
     for src in SOURCES:
         o = odir / f"{src.stem}.o"
         objs.append(o)
-        dep_t = max([src.stat().st_mtime] + [h.stat().st_mtime for h in _deps(src)])
-        if not force and o.exists() and o.stat().st_mtime > dep_t:
+        dep_t = _dep_time(src)
+        if not force and o.exists() and o.stat().st_mtime >= dep_t:
             continue
         tmp_o = o.with_name(f"{o.name}.tmp{os.getpid()}")
-        procs.append((src, tmp_o, o, subprocess.Popen(
+        procs.append((src, tmp_o, o, dep_t, subprocess.Popen(
             [NVCC, *compile_flags, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(tmp_o)],
             stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
     failed = None
-    for src, tmp_o, o, p in procs:
+    for src, tmp_o, o, dep_t, p in procs:
         _, err_s = p.communicate()
         (odir / f"{src.stem}.ptxas.log").write_text(err_s)
         if p.returncode != 0:
@@ -76,6 +86,9 @@ def build(force: bool = False, verbose: bool = False, out: pathlib.Path | None =
                 tmp_o.unlink()
         else:
             os.replace(tmp_o, o)
+            # stamp the object with the source time it was compiled from, so an edit
+            # made while nvcc ran leaves it stale
+            os.utime(o, (dep_t, dep_t))
     if failed is not None:
         raise RuntimeError(f"nvcc failed ({failed[0]}):\n{failed[1][-4000:]}")
     tmp = lib.with_name(f"{lib.name}.tmp{os.getpid()}")

@@ -178,30 +178,39 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
   auto inbox = [&](int rank, unsigned long long off, unsigned long long stride, int slot) -> char* {
     return R->ws[rank] + off + (unsigned long long)slot * stride;
   };
+  // this call's inbox offsets, selected (not indexed: a parameter array indexed by a
+  // runtime value is copied to local memory)
+  const unsigned long long h_off = par ? a.h_off[1] : a.h_off[0], v_off = par ? a.v_off[1] : a.v_off[0],
+                           ag_off = par ? a.ag_off[1] : a.ag_off[0], hag_off = par ? a.hag_off[1] : a.hag_off[0];
   bool ok = true;
 
   if (stage == kSA && X > 1) {
     // ---- A: my buffer's shares of my row peers' chunks -> their H inboxes ----
     const int per_u = (X - 1) * Y, nj = a.Umax * per_u;
+    // job J -> (unit u, destination column j, sub-chunk js); both loads issued before
+    // either store (named registers, not an array indexed by a running count: that
+    // array would live in local memory)
+    auto job = [&](int J, int& u, int& j, int& js) -> bool {
+      if (J >= nj) return false;
+      u = J / per_u;
+      const int r = J % per_u;
+      j = (c + 1 + r / Y) % X;
+      js = j * Y + r % Y;
+      return u < a.g_U[js];
+    };
+    auto load = [&](int u, int j, int js) -> uint4 {
+      return uload(a.g_co[j] + a.g_cs[js] + (unsigned long long)u * UE + eoff, lane_n(a.g_sl[js], u));
+    };
+    auto push = [&](int u, int j, int js, uint4 v) {
+      put(inbox(rho * X + j, h_off, a.h_stride, c), (unsigned long long)a.g_uoff[js] + u, lane, v, flag);
+    };
     for (int J0 = wr; J0 < nj; J0 += 2 * WS) {  // two units per iteration: both loads in flight
-      uint4 v[2];
-      int js2[2], u2[2], j2[2], m = 0;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int J = J0 + h * WS;
-        if (J >= nj) continue;
-        const int u = J / per_u, r = J % per_u, j = (c + 1 + r / Y) % X, s = r % Y, js = j * Y + s;
-        if (u >= a.g_U[js]) continue;
-        v[m] = uload(a.g_co[j] + a.g_cs[js] + (unsigned long long)u * UE + eoff, lane_n(a.g_sl[js], u));
-        js2[m] = js;
-        u2[m] = u;
-        j2[m++] = j;
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        if (h < m)
-          put(inbox(rho * X + j2[h], a.h_off[par], a.h_stride, c), (unsigned long long)a.g_uoff[js2[h]] + u2[h], lane,
-              v[h], flag);
+      int u0 = 0, j0 = 0, js0 = 0, u1 = 0, j1 = 0, js1 = 0;
+      const bool h0 = job(J0, u0, j0, js0), h1 = job(J0 + WS, u1, j1, js1);
+      const uint4 v0 = h0 ? load(u0, j0, js0) : zero;
+      const uint4 v1 = h1 ? load(u1, j1, js1) : zero;
+      if (h0) push(u0, j0, js0, v0);
+      if (h1) push(u1, j1, js1, v1);
     }
   } else if (stage == kSB) {
     // ---- B: fold my chunk (columns c+1, ..., c), round; push to the column owner ----
@@ -216,7 +225,7 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
         const int j = (c + kk) % X;
         uint4 w;
         if (j == c) w = own;
-        else ok = get(inbox(me, a.h_off[par], a.h_stride, j), (unsigned long long)a.g_uoff[cs] + u, lane, flag,
+        else ok = get(inbox(me, h_off, a.h_stride, j), (unsigned long long)a.g_uoff[cs] + u, lane, flag,
                       deadline, R->err, &w);
         Acc t[VE];
         unpack<W>(w, t);
@@ -229,13 +238,13 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
       }
       if (!ok) break;
       if (Y > 1) {
-        put(inbox(s * X + c, a.v_off[par], a.v_stride, rho), u, lane, pack<W>(acc), flag);
+        put(inbox(s * X + c, v_off, a.v_stride, rho), u, lane, pack<W>(acc), flag);
       } else {  // the last reduce phase: mean, round once, final
         if (a.op == 1) acc_mean<W>(acc, a.inv_n, N);
         const uint4 out = pack<W>(acc);
         ustore(e, nr, out);
         for (int jj = 1; jj < X; ++jj)
-          put(inbox(rho * X + (c + jj) % X, a.hag_off[par], a.hag_stride, c), (unsigned long long)a.g_uoff[cs] + u,
+          put(inbox(rho * X + (c + jj) % X, hag_off, a.hag_stride, c), (unsigned long long)a.g_uoff[cs] + u,
               lane, out, flag);
       }
     }
@@ -247,8 +256,8 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
       Acc acc[VE];
       if (Y == 2) {  // both rows in one load round: fold order rho+1, rho
         uint4 w0, w1;
-        ok = get2(lane_ptr(inbox(me, a.v_off[par], a.v_stride, (rho + 1) % 2), u, lane),
-                  lane_ptr(inbox(me, a.v_off[par], a.v_stride, rho), u, lane), lane, flag, deadline, R->err, &w0,
+        ok = get2(lane_ptr(inbox(me, v_off, a.v_stride, (rho + 1) % 2), u, lane),
+                  lane_ptr(inbox(me, v_off, a.v_stride, rho), u, lane), lane, flag, deadline, R->err, &w0,
                   &w1);
         Acc t[VE];
         unpack<W>(w0, acc);
@@ -258,7 +267,7 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
       for (int kk = 1; kk <= Y && ok && Y != 2; ++kk) {
         const int i = (rho + kk) % Y;
         uint4 w;
-        ok = get(inbox(me, a.v_off[par], a.v_stride, i), u, lane, flag, deadline, R->err, &w);
+        ok = get(inbox(me, v_off, a.v_stride, i), u, lane, flag, deadline, R->err, &w);
         Acc t[VE];
         unpack<W>(w, t);
         if (kk == 1) {
@@ -273,9 +282,9 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
       const uint4 out = pack<W>(acc);
       ustore(a.g_co[c] + a.g_cs[cr] + (unsigned long long)u * UE + eoff, nr, out);
       for (int ii = 1; ii < Y; ++ii)
-        put(inbox(((rho + ii) % Y) * X + c, a.ag_off[par], a.ag_stride, rho), u, lane, out, flag);
+        put(inbox(((rho + ii) % Y) * X + c, ag_off, a.ag_stride, rho), u, lane, out, flag);
       for (int jj = 1; jj < X; ++jj)
-        put(inbox(rho * X + (c + jj) % X, a.hag_off[par], a.hag_stride, c), (unsigned long long)a.g_uoff[cr] + u,
+        put(inbox(rho * X + (c + jj) % X, hag_off, a.hag_stride, c), (unsigned long long)a.g_uoff[cr] + u,
             lane, out, flag);
     }
   } else if (stage == kSD && Y > 1) {
@@ -290,7 +299,7 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
     auto emit = [&](int u, int ci, uint4 w) {
       ustore(a.g_co[c] + a.g_cs[ci] + (unsigned long long)u * UE + eoff, lane_n(a.g_sl[ci], u), w);
       for (int jj = 1; jj < X; ++jj)
-        put(inbox(rho * X + (c + jj) % X, a.hag_off[par], a.hag_stride, c), (unsigned long long)a.g_uoff[ci] + u,
+        put(inbox(rho * X + (c + jj) % X, hag_off, a.hag_stride, c), (unsigned long long)a.g_uoff[ci] + u,
             lane, w, flag);
     };
     for (int J = wr; J < nj && ok; J += 2 * WS) {  // two jobs per load round
@@ -298,15 +307,15 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
       const bool h0 = job(J, &u0, &c0), h1 = job(J + WS, &u1, &c1);
       uint4 w0, w1;
       if (h0 && h1) {
-        ok = get2(lane_ptr(inbox(me, a.ag_off[par], a.ag_stride, c0 - c * Y), u0, lane),
-                  lane_ptr(inbox(me, a.ag_off[par], a.ag_stride, c1 - c * Y), u1, lane), lane, flag, deadline,
+        ok = get2(lane_ptr(inbox(me, ag_off, a.ag_stride, c0 - c * Y), u0, lane),
+                  lane_ptr(inbox(me, ag_off, a.ag_stride, c1 - c * Y), u1, lane), lane, flag, deadline,
                   R->err, &w0, &w1);
         if (!ok) break;
         emit(u0, c0, w0);
         emit(u1, c1, w1);
       } else if (h0 || h1) {
         const int u = h0 ? u0 : u1, ci = h0 ? c0 : c1;
-        ok = get(inbox(me, a.ag_off[par], a.ag_stride, ci - c * Y), u, lane, flag, deadline, R->err, &w0);
+        ok = get(inbox(me, ag_off, a.ag_stride, ci - c * Y), u, lane, flag, deadline, R->err, &w0);
         if (!ok) break;
         emit(u, ci, w0);
       }
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
       return *u < a.g_U[*js];
     };
     auto src = [&](int u, int js) -> const char* {
-      return lane_ptr(inbox(me, a.hag_off[par], a.hag_stride, js / Y), (unsigned long long)a.g_uoff[js] + u, lane);
+      return lane_ptr(inbox(me, hag_off, a.hag_stride, js / Y), (unsigned long long)a.g_uoff[js] + u, lane);
     };
     auto emit = [&](int u, int js, uint4 w) {
       ustore(a.g_co[js / Y] + a.g_cs[js] + (unsigned long long)u * UE + eoff, lane_n(a.g_sl[js], u), w);
@@ -338,7 +347,7 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
         emit(u1, j1, w1);
       } else if (h0 || h1) {
         const int u = h0 ? u0 : u1, js = h0 ? j0 : j1;
-        ok = get(inbox(me, a.hag_off[par], a.hag_stride, js / Y), (unsigned long long)a.g_uoff[js] + u, lane, flag,
+        ok = get(inbox(me, hag_off, a.hag_stride, js / Y), (unsigned long long)a.g_uoff[js] + u, lane, flag,
                  deadline, R->err, &w0);
         if (!ok) break;
         emit(u, js, w0);
