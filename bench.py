@@ -35,6 +35,7 @@ import synthetic  # noqa: E402  (seeded inputs only; no method arithmetic)
 METRIC = ("2D-torus allreduce busbw GB/s (fp16 25.6M elems, 8×B200, max over ranks) "
           "vs NVLink peak")
 NVLINK_NOMINAL = 900.0      # GB/s per direction per GPU (18 x 50)
+L2_BYTES = 126 * 1000 * 1000  # B200 L2 (B200_PROFILING.md)
 NVLINK_MEASURED = 770.0     # GB/s per direction, B200_PROFILING.md "peer copy" measurement
 DEFAULT_GRID = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
 DT_BYTES = {"f32": 4, "f16": 2, "bf16": 2, "i32": 4}
@@ -59,6 +60,8 @@ def parse():
     p.add_argument("--no-register", action="store_true",
                    help="do not register the buffer (the pull kernel then copies inputs into the slab)")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
+    p.add_argument("--l2", default=None, choices=["flush", "rotate"],
+                   help="L2 protocol between timed calls (default: rotate at N=1, flush at N>1)")
     p.add_argument("--out", default=None, help="also append the JSON line to this file")
     return p.parse_args()
 
@@ -95,6 +98,7 @@ def device_align(world):
         import torch
         import torch.distributed as dist
         dist.all_reduce(torch.zeros(1, device="cuda"))
+        torch.cuda._sleep(2_000_000)  # ~1 ms on every GPU while the hosts enqueue ahead
 
 
 def gather_max(x, world):
@@ -125,6 +129,11 @@ class Clocks:
                 self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}",
                                               "--format=csv,noheader,nounits", "-lms", "200"],
                                              stdout=self.fh, stderr=subprocess.DEVNULL)
+                # nvidia-smi takes ~0.5-1 s to start on a multi-GPU box: wait for its first
+                # sample so the warm-up and the (short) timed region are both covered
+                t0 = time.perf_counter()
+                while os.path.getsize(self.path) == 0 and time.perf_counter() - t0 < 5.0:
+                    time.sleep(0.05)
             except OSError:
                 self.proc = None
 
@@ -265,8 +274,20 @@ def run_torus(args):
     reduce_fn = {"ring": comm.ring_all_reduce, "hier": comm.hier_all_reduce,
                  "nvls": comm.nvls_all_reduce}.get(args.algo, comm.all_reduce)
 
-    def call():
-        reduce_fn(buf, op=args.op, wire=TD[wire_s], stream=stream)
+    def call(b=None):
+        reduce_fn(buf if b is None else b, op=args.op, wire=TD[wire_s], stream=stream)
+
+    # L2 protocol between timed calls.  N > 1 (NVLink-bound): evict before every call.  N = 1
+    # (HBM-bound): rotate over buffers whose total exceeds 3x L2 with no eviction, so each
+    # call reads a cold buffer AND writes back the dirty lines the previous call left in L2
+    # -- the steady state of back-to-back kernels.  (An eviction that leaves L2 clean lets
+    # ~58 MB of this call's writes be written back after its end event, which puts the
+    # algorithmic-byte rate above the HBM peak.)
+    l2_mode = args.l2 or ("rotate" if world == 1 else "flush")
+    ring = [buf]
+    if l2_mode == "rotate":
+        nbytes = buf.numel() * buf.element_size()
+        ring += [x0.clone() for _ in range(max(2, -(-3 * L2_BYTES // nbytes)) - 1)]
 
     # sanity (not the parity gate -- that is tests/): all ranks agree, and the result is
     # within the north-star tolerance of an f64 all-reduce done with NCCL in f64.
@@ -298,11 +319,11 @@ def run_torus(args):
     # ---- device-timed region (the clock sampler starts before the warm-up) ----
     clocks = Clocks(rank == 0)
     t_w = time.perf_counter()
-    while True:  # warm-up: >= W calls and >= 0.3 s so the sampler has seen load
-        for _ in range(max(args.warmup, 3)):
-            call()
+    while True:  # warm-up: >= W calls and >= 0.5 s so the sampler has seen load
+        for i in range(max(args.warmup, 3)):
+            call(ring[i % len(ring)])
         torch.cuda.synchronize()
-        if gather_max(time.perf_counter() - t_w, world) > 0.3:
+        if gather_max(time.perf_counter() - t_w, world) > 0.5:
             break
     barrier(world)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -310,12 +331,14 @@ def run_torus(args):
     torch.cuda.synchronize()
     barrier(world)
     device_align(world)
-    evict(0)
-    call()  # untimed: the first call after the idle barrier pays a wake-up (profiles/r02_ab*.txt: call 0)
+    if l2_mode == "flush":
+        evict(0)
+    call(ring[-1])  # untimed: the first call after the idle barrier pays a wake-up (profiles/r02_ab*.txt: call 0)
     for s in range(args.steps):
-        evict(s)                                # L2 evicted and clean, untimed
+        if l2_mode == "flush":
+            evict(s)                            # L2 evicted and clean, untimed
         ev[s][0].record(stream)
-        call()
+        call(ring[s % len(ring)])
         ev[s][1].record(stream)
     torch.cuda.synchronize()
     barrier(world)
@@ -409,6 +432,13 @@ def run_torus(args):
                "unit": "GB/s", "us_per_step": te * 1e6,
                "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb}
 
+    if l2_mode == "flush":
+        l2_desc = ("flushed before every timed call (256 MiB write, then 256 MiB read so no dirty "
+                   "flush lines are written back inside the timed call)")
+    else:
+        l2_desc = (f"no flush: {len(ring)} buffers of {buf.numel() * buf.element_size()} B in rotation "
+                   f"(> 3x the 126 MB L2), so every call reads a cold buffer and pays the write-back "
+                   f"of the dirty lines the previous call left in L2")
     launches = comm.launches(D, TD[dtype_s], TD[wire_s])
     # ---- roofline of the dominant (only) kernel ----
     if world > 1:
@@ -436,7 +466,8 @@ def run_torus(args):
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
-                "traffic": load_traffic("castscale_tma"), "kernel": kernel_name(comm, D, TD, dtype_s, wire_s),
+                "traffic": load_traffic(kernel_name(comm, D, TD, dtype_s, wire_s).replace("_kernel", "")),
+                "kernel": kernel_name(comm, D, TD, dtype_s, wire_s),
                 "algorithmic_bytes_per_call": alg_bytes}
 
     cpu = None
@@ -461,7 +492,7 @@ def run_torus(args):
                    "ctas_per_rank": comm_ctas(),
                    "buffer": ("registered (zero-copy)" if world > 1 and not args.no_register
                               else "unregistered"),
-                   "message_bytes": S, "l2": "flushed before every timed call (256 MiB write, then 256 MiB read so no dirty flush lines are written back inside the timed call)",
+                   "message_bytes": S, "l2": l2_desc,
                    "value_is": "busbw" if world > 1 else "algbw (busbw is 0 at N=1)"},
         "algbw": algbw, "busbw": busbw, "us_per_call": t * 1e6, "us_per_call_min": t_min * 1e6,
         "us_per_call_p50": t_p50 * 1e6, "us_per_call_p90": t_p90 * 1e6, "us_per_call_max": t_max * 1e6,

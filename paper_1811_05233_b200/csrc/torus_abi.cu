@@ -850,7 +850,7 @@ namespace {
 enum Route { kRouteNone = 0, kRouteCast, kRouteLL, kRouteLL2, kRoutePull, kRoutePush, kRouteLL128 };
 const char* route_name(int r) {
   switch (r) {
-    case kRouteCast: return "castscale_tma_kernel";  // castscale_kernel for unaligned buffers
+    case kRouteCast: return castscale_use_tma() ? "castscale_tma_kernel" : "castscale_kernel";
     case kRouteLL: return "ll_kernel";
     case kRouteLL2: return "ll2_kernel";
     case kRoutePull: return "torus_pull_kernel";

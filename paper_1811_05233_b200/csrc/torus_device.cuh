@@ -223,9 +223,7 @@ template <> struct Elem<DT_F16> { using T = __half; };
 template <> struct Elem<DT_BF16> { using T = __nv_bfloat16; };
 
 // Load `nrem` (<= VE) elements at element index e of the user buffer, converted to the
-// wire type (C1: w = to_wire(in)); missing lanes are zero.  The ragged / unaligned case
-// uses fully unrolled predicated accesses: a loop bound by nrem would index the element
-// arrays dynamically and put them in local memory, on the hot path too.
+// wire type (C1: w = to_wire(in)); missing lanes are zero.
 template <int DT, int W>
 __device__ __forceinline__ uint4 load_user(const void* buf, unsigned long long e, int nrem,
                                            bool aligned) {
@@ -234,17 +232,16 @@ __device__ __forceinline__ uint4 load_user(const void* buf, unsigned long long e
   const T* p = reinterpret_cast<const T*>(buf) + e;
   if constexpr (DT == W) {
     if (aligned && nrem == VE) return __ldcs(reinterpret_cast<const uint4*>(p));
+    uint16_t h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t u[4] = {0, 0, 0, 0};
     if constexpr (sizeof(T) == 2) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (i < nrem) u[i >> 1] |= uint32_t(reinterpret_cast<const uint16_t*>(p)[i]) << (16 * (i & 1));
+      for (int i = 0; i < nrem; ++i) h[i] = reinterpret_cast<const uint16_t*>(p)[i];
+      return make_uint4(h[0] | (uint32_t(h[1]) << 16), h[2] | (uint32_t(h[3]) << 16),
+                        h[4] | (uint32_t(h[5]) << 16), h[6] | (uint32_t(h[7]) << 16));
     } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i < nrem) u[i] = reinterpret_cast<const uint32_t*>(p)[i];
+      for (int i = 0; i < nrem; ++i) u[i] = reinterpret_cast<const uint32_t*>(p)[i];
+      return make_uint4(u[0], u[1], u[2], u[3]);
     }
-    return make_uint4(u[0], u[1], u[2], u[3]);
   } else {
     static_assert(DT == DT_F32 && VE == 8, "only f32 buffers take a narrower wire");
     float f[8];
@@ -272,13 +269,10 @@ __device__ __forceinline__ void store_user(void* buf, unsigned long long e, int 
     if (aligned && nrem == VE) { __stcs(reinterpret_cast<uint4*>(p), v); return; }
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
     if constexpr (sizeof(T) == 2) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (i < nrem) reinterpret_cast<uint16_t*>(p)[i] = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
+      for (int i = 0; i < nrem; ++i)
+        reinterpret_cast<uint16_t*>(p)[i] = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
     } else {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i < nrem) reinterpret_cast<uint32_t*>(p)[i] = w[i];
+      for (int i = 0; i < nrem; ++i) reinterpret_cast<uint32_t*>(p)[i] = w[i];
     }
   } else {
     float f[8];
@@ -287,9 +281,7 @@ __device__ __forceinline__ void store_user(void* buf, unsigned long long e, int 
       __stcs(reinterpret_cast<float4*>(p), make_float4(f[0], f[1], f[2], f[3]));
       __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(f[4], f[5], f[6], f[7]));
     } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (i < nrem) p[i] = f[i];
+      for (int i = 0; i < nrem; ++i) p[i] = f[i];
     }
   }
 }

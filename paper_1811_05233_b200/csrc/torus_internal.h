@@ -189,6 +189,7 @@ cudaError_t launch_torus(const LaunchArgs& a, int dtype, int wire, bool cooperat
                          cudaStream_t stream);
 cudaError_t launch_castscale(void* buf, unsigned long long n, int dtype, int wire,
                              cudaStream_t stream);
+bool castscale_use_tma();  // env TORUS_CS_KERNEL=tma: the TMA ring instead of the one-shot LDG/STG kernel
 cudaError_t launch_castscale_tma(void* buf, unsigned long long n, int wire, cudaStream_t stream);
 cudaError_t launch_barrier(const RankDev* ranks, int nlocal, unsigned long long bar_off,
                            unsigned long long timeout_ns, cudaStream_t stream);

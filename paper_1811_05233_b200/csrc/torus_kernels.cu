@@ -1160,14 +1160,18 @@ int torus_kernel_max_ctas_per_sm(int dtype, int wire) {
   return 0;
 }
 
-// castscale variant (env TORUS_CS = "<unroll>x<block>x<ctas per SM>", default 4x256x4)
+// castscale variant (env TORUS_CS = "<unroll>x<block>x<ctas per SM>", default 1x512x0: one
+// 32-byte vector per thread, a one-shot grid covering the buffer, no CTA cap (0)).  Measured
+// in the steady state of back-to-back calls on cold buffers (profiles/r02_cast_probe*.jsonl:
+// 36.0 us for the 102 MB buffer, vs 38.5 for the best TMA ring and 36.5 for torch's own
+// in-place elementwise kernel on the same bytes).
 template <int W, int U, int BLK>
 cudaError_t launch_cs(float* buf, unsigned long long n, int cps, cudaStream_t stream) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const unsigned long long nv = (n + 7) / 8;
   const unsigned long long want = (nv + (unsigned long long)BLK * U - 1) / ((unsigned long long)BLK * U);
-  const unsigned long long cap = (unsigned long long)sms * cps;
+  const unsigned long long cap = cps > 0 ? (unsigned long long)sms * cps : want;
   const int blocks = (int)(want < 1 ? 1 : (want < cap ? want : cap));
   castscale_kernel<W, U, BLK><<<blocks, BLK, 0, stream>>>(buf, n);
   return cudaGetLastError();
@@ -1175,23 +1179,31 @@ cudaError_t launch_cs(float* buf, unsigned long long n, int cps, cudaStream_t st
 
 template <int W>
 cudaError_t launch_cs_variant(float* buf, unsigned long long n, cudaStream_t stream) {
-  int u = 4, blk = 256, cps = 4;
+  int u = 1, blk = 512, cps = 0;
   if (const char* v = getenv("TORUS_CS")) sscanf(v, "%dx%dx%d", &u, &blk, &cps);
   if (u == 8 && blk == 256) return launch_cs<W, 8, 256>(buf, n, cps, stream);
   if (u == 2 && blk == 256) return launch_cs<W, 2, 256>(buf, n, cps, stream);
   if (u == 4 && blk == 512) return launch_cs<W, 4, 512>(buf, n, cps, stream);
   if (u == 8 && blk == 512) return launch_cs<W, 8, 512>(buf, n, cps, stream);
   if (u == 4 && blk == 128) return launch_cs<W, 4, 128>(buf, n, cps, stream);
-  return launch_cs<W, 4, 256>(buf, n, cps, stream);
+  if (u == 2 && blk == 128) return launch_cs<W, 2, 128>(buf, n, cps, stream);
+  if (u == 1 && blk == 128) return launch_cs<W, 1, 128>(buf, n, cps, stream);
+  if (u == 1 && blk == 256) return launch_cs<W, 1, 256>(buf, n, cps, stream);
+  if (u == 1 && blk == 512) return launch_cs<W, 1, 512>(buf, n, cps, stream);
+  if (u == 4 && blk == 256) return launch_cs<W, 4, 256>(buf, n, cps, stream);
+  return launch_cs<W, 1, 512>(buf, n, cps, stream);
+}
+
+bool castscale_use_tma() {
+  const char* kv = getenv("TORUS_CS_KERNEL");
+  return kv && strcmp(kv, "tma") == 0;
 }
 
 cudaError_t launch_castscale(void* buf, unsigned long long n, int dtype, int wire,
                              cudaStream_t stream) {
   if (dtype != DT_F32) return cudaErrorInvalidValue;
-  // TMA-streamed variant (torus_cast.cu) for aligned buffers unless TORUS_CS_KERNEL=ldg
-  const char* kv = getenv("TORUS_CS_KERNEL");
-  const bool tma = !(kv && strcmp(kv, "ldg") == 0);
-  if (tma && (reinterpret_cast<uintptr_t>(buf) & 15) == 0 && n >= 8)
+  // the TMA-streamed ring (torus_cast.cu) for aligned buffers with TORUS_CS_KERNEL=tma
+  if (castscale_use_tma() && (reinterpret_cast<uintptr_t>(buf) & 15) == 0 && n >= 8)
     return launch_castscale_tma(buf, n, wire, stream);
   if (wire == DT_F16) return launch_cs_variant<DT_F16>(reinterpret_cast<float*>(buf), n, stream);
   if (wire == DT_BF16) return launch_cs_variant<DT_BF16>(reinterpret_cast<float*>(buf), n, stream);

@@ -209,13 +209,20 @@ def test_special_values(vgrids, kernel):
             assert_same(got[r], ref[r], f"specials {wire} rank {r}")
 
 
-def test_single_rank_cast_scale():
-    """N = 1 (a7): f32 buffer with f16/bf16 wire -> fused cast round trip; same-type no-op."""
+@pytest.mark.parametrize("cs_kernel", ["default", "tma"])
+def test_single_rank_cast_scale(cs_kernel, monkeypatch):
+    """N = 1 (a7): f32 buffer with f16/bf16 wire -> fused cast round trip; same-type no-op.
+    Both kernels: the one-shot castscale_kernel (default) and the TMA ring (TORUS_CS_KERNEL=tma),
+    at sizes spanning one partial tile, several tiles and a ragged tail."""
     from paper_1811_05233_b200 import VirtualTorus
+    if cs_kernel == "tma":
+        monkeypatch.setenv("TORUS_CS_KERNEL", "tma")
     vt = VirtualTorus(1, 1, device=0)
     try:
+        want = "castscale_tma_kernel" if cs_kernel == "tma" else "castscale_kernel"
+        assert vt.route(1 << 20, torch.float32, torch.float16) == want
         for wire in ("f16", "bf16", "f32"):
-            for D in (1, 13, 1 << 20):
+            for D in (1, 13, 8195, 1 << 20, 3_000_017):
                 x = synthetic.make("wide", D, 0, "f32")
                 got = run_virtual(vt, [x], "f32", wire, "mean")[0]
                 ref = oracle.torus_allreduce([x], 1, 1, "f32", wire=wire, op="mean")[0]
