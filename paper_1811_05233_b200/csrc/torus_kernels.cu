@@ -1054,6 +1054,69 @@ __global__ void __launch_bounds__(BLK) castscale_kernel(float* buf, unsigned lon
   }
 }
 
+// Cache-operator variants of the one-shot cast (env TORUS_CS_CACHE = "<load>,<store>"):
+// load 0 ld.global.cs, 1 ld.global.nc.L1::no_allocate, 2 ld.global with an L2 evict_first
+// policy; store 0 st.global.cs, 1 st.global (write-back), 2 / 3 st.global with an L2
+// evict_first / evict_last policy.  One 32-byte vector per thread, 512 threads per CTA.
+template <int W, int LC, int SC>
+__global__ void __launch_bounds__(512) castscale_cache_kernel(float* buf, unsigned long long n) {
+  const unsigned long long nv = n / 8;  // whole vectors (the caller handles n % 8 == 0 only)
+  const unsigned long long v = blockIdx.x * 512ull + threadIdx.x;
+  if (v >= nv) return;
+  float* p = buf + v * 8;
+  uint64_t pol_first = 0, pol_last = 0;
+  if constexpr (LC == 2 || SC == 2)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+  if constexpr (SC == 3)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+  float f[8];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float* q = p + 4 * h;
+    if constexpr (LC == 0)
+      asm volatile("ld.global.cs.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(f[4 * h]), "=f"(f[4 * h + 1]), "=f"(f[4 * h + 2]), "=f"(f[4 * h + 3]) : "l"(q));
+    else if constexpr (LC == 1)
+      asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(f[4 * h]), "=f"(f[4 * h + 1]), "=f"(f[4 * h + 2]), "=f"(f[4 * h + 3]) : "l"(q));
+    else
+      asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                   : "=f"(f[4 * h]), "=f"(f[4 * h + 1]), "=f"(f[4 * h + 2]), "=f"(f[4 * h + 3])
+                   : "l"(q), "l"(pol_first));
+  }
+  float y[8];
+  unpack<W>(pack<W>(f), y);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float* q = p + 4 * h;
+    if constexpr (SC == 0)
+      asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(q), "f"(y[4 * h]), "f"(y[4 * h + 1]),
+                   "f"(y[4 * h + 2]), "f"(y[4 * h + 3]) : "memory");
+    else if constexpr (SC == 1)
+      asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(q), "f"(y[4 * h]), "f"(y[4 * h + 1]),
+                   "f"(y[4 * h + 2]), "f"(y[4 * h + 3]) : "memory");
+    else
+      asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(q), "f"(y[4 * h]),
+                   "f"(y[4 * h + 1]), "f"(y[4 * h + 2]), "f"(y[4 * h + 3]), "l"(SC == 2 ? pol_first : pol_last)
+                   : "memory");
+  }
+}
+
+template <int W>
+cudaError_t launch_cs_cache(float* buf, unsigned long long n, int lc, int sc, cudaStream_t stream) {
+  const unsigned long long blocks = (n / 8 + 511) / 512;
+  const int k = lc * 4 + sc;
+#define CSC(L, S) \
+  case L * 4 + S: castscale_cache_kernel<W, L, S><<<(unsigned)blocks, 512, 0, stream>>>(buf, n); break;
+  switch (k) {
+    CSC(0, 0) CSC(0, 1) CSC(0, 2) CSC(0, 3) CSC(1, 0) CSC(1, 1) CSC(1, 2) CSC(1, 3)
+    CSC(2, 0) CSC(2, 1) CSC(2, 2) CSC(2, 3)
+    default: return cudaErrorInvalidValue;
+  }
+#undef CSC
+  return cudaGetLastError();
+}
+
 // Device barrier among all ranks (init/destroy): every rank stores its epoch into every
 // peer's barrier slot, then waits for all peers' slots.
 __global__ void barrier_kernel(const RankDev* ranks, unsigned long long bar_off,
@@ -1203,6 +1266,14 @@ cudaError_t launch_castscale(void* buf, unsigned long long n, int dtype, int wir
                              cudaStream_t stream) {
   if (dtype != DT_F32) return cudaErrorInvalidValue;
   // the TMA-streamed ring (torus_cast.cu) for aligned buffers with TORUS_CS_KERNEL=tma
+  if (const char* cc = getenv("TORUS_CS_CACHE")) {  // cache-operator experiment (aligned, n % 8 == 0)
+    int lc = 0, sc = 0;
+    sscanf(cc, "%d,%d", &lc, &sc);
+    if ((reinterpret_cast<uintptr_t>(buf) & 15) == 0 && n % 8 == 0) {
+      if (wire == DT_F16) return launch_cs_cache<DT_F16>(reinterpret_cast<float*>(buf), n, lc, sc, stream);
+      if (wire == DT_BF16) return launch_cs_cache<DT_BF16>(reinterpret_cast<float*>(buf), n, lc, sc, stream);
+    }
+  }
   if (castscale_use_tma() && (reinterpret_cast<uintptr_t>(buf) & 15) == 0 && n >= 8)
     return launch_castscale_tma(buf, n, wire, stream);
   if (wire == DT_F16) return launch_cs_variant<DT_F16>(reinterpret_cast<float*>(buf), n, stream);

@@ -2,7 +2,7 @@
 the full workload in rotation, so every call reads a cold buffer and inherits the dirty
 lines the previous call left): the castscale kernel variants against torch's own copy of
 the same bytes (read 102 MB + write 102 MB).  One JSON line per variant.
-Usage (GPU box): python tools/cast_probe.py [calls [TORUS_CS ldg variants...]]"""
+Usage (GPU box): python tools/cast_probe.py [calls [variant ...]]"""
 import json
 import os
 import sys
@@ -41,14 +41,16 @@ def report(name, r):
     print(json.dumps(r), flush=True)
 
 
-variants = [("tma 6x1", {"TORUS_CS_TMA": "6x1"}), ("tma 4x1", {"TORUS_CS_TMA": "4x1"}),
-            ("tma 3x1", {"TORUS_CS_TMA": "3x1"}), ("tma 2x2", {"TORUS_CS_TMA": "2x2"}),
-            ("tma 3x2", {"TORUS_CS_TMA": "3x2"}), ("tma 5x1", {"TORUS_CS_TMA": "5x1"})]
-for cs in sys.argv[2:] or ["4x256x4", "4x256x1000", "2x256x1000", "8x256x1000", "4x512x1000", "4x128x1000",
-                           "8x512x2", "2x512x1000"]:
-    variants.append((f"ldg {cs}", {"TORUS_CS_KERNEL": "ldg", "TORUS_CS": cs}))
+# variants: "tma:<NB>x<cps>", "ldg:<U>x<BLK>x<cps>", "cache:<load>,<store>" (see torus_kernels.cu)
+specs = sys.argv[2:] or ["tma:6x1", "tma:4x1", "ldg:1x512x0", "ldg:2x256x0", "ldg:4x256x4"]
+variants = []
+for sp in specs:
+    kind, arg = sp.split(":")
+    env = {"tma": {"TORUS_CS_KERNEL": "tma", "TORUS_CS_TMA": arg}, "ldg": {"TORUS_CS": arg},
+           "cache": {"TORUS_CS_CACHE": arg}}[kind]
+    variants.append((sp, env))
 for name, env in variants:
-    saved = {k: os.environ.get(k) for k in ("TORUS_CS_TMA", "TORUS_CS_KERNEL", "TORUS_CS")}
+    saved = {k: os.environ.get(k) for k in ("TORUS_CS_TMA", "TORUS_CS_KERNEL", "TORUS_CS", "TORUS_CS_CACHE")}
     for k in saved:
         os.environ.pop(k, None)
     os.environ.update(env)
