@@ -1077,6 +1077,14 @@ int launch_ll128_rounds(torus_comm* c, void* const* bufs, size_t count, int dtyp
   // (B with Y == 1 also pushes its final values to the X-1 row peers)
   double w[5] = {X > 1 ? 2.0 * (X - 1) * Y : 0, (double)Y * (X + (Y > 1 ? 1 : X)), Y > 1 ? 2.0 * Y + X - 1 : 0,
                  Y > 1 ? (double)(Y - 1) * (X + 1) : 0, X > 1 ? 2.0 * (X - 1) * Y : 0};
+  // measured at 2x2 (profiles/r02_wsweep2_n4.txt, 3 interleaved repeats): 0.8 x the fold
+  // stages B, C and 1.2 x the row all-gather E is 2% faster than the formula alone
+  // (150.0 vs 152.9 us); at 1x2 the formula is best (profiles/r02_wsweep_n2.txt)
+  if (X > 1 && Y > 1) {
+    w[1] *= 0.8;
+    w[2] *= 0.8;
+    w[4] *= 1.2;
+  }
   for (int k = 0; k < 5; ++k) w[k] *= c->ll128_w[k];
   double ws = 0;
   int present = 0;
