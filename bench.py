@@ -57,6 +57,8 @@ def parse():
                    help="ring / hier = baseline kernels; nvls = in-switch-reduction variant")
     p.add_argument("--no-nccl", action="store_true", help="skip the NCCL comparison")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--e2e-piece", type=int, default=4 << 20,
+                   help="elements per pipelined piece of the e2e host-buffer call (0 = one piece)")
     p.add_argument("--no-register", action="store_true",
                    help="do not register the buffer (the pull kernel then copies inputs into the slab)")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
@@ -408,29 +410,38 @@ def run_torus(args):
     # ---- e2e through the public API with HOST buffers: H2D, all-reduce, D2H ----
     e2e = None
     if not args.no_e2e:
-        hin = torch.from_numpy(host.view(np.int16) if dtype_s == "bf16" else host).pin_memory()
-        hout = torch.empty_like(hin).pin_memory()
-        view = buf.view(torch.int16) if dtype_s == "bf16" else buf
+        hbuf = (torch.from_numpy(host.view(np.int16).copy()).view(torch.bfloat16) if dtype_s == "bf16"
+                else torch.from_numpy(host.copy())).pin_memory()
+        piece = args.e2e_piece
+        if args.algo == "torus":
+            def e2e_step():
+                comm.all_reduce_host(hbuf, buf, op=args.op, wire=TD[wire_s], piece=piece, stream=stream)
+            how = (f"torus_allreduce_host (C-ABI): pinned host buffer, H2D + all-reduce + D2H "
+                   f"pipelined over pieces of {piece} elements on two copy streams")
+        else:
+            hout = torch.empty_like(hbuf).pin_memory()
+
+            def e2e_step():
+                buf.copy_(hbuf, non_blocking=True)
+                call()
+                hout.copy_(buf, non_blocking=True)
+            how = "H2D copy, all-reduce, D2H copy on one stream"
         for _ in range(2):
-            view.copy_(hin, non_blocking=True)
-            call()
-            hout.copy_(view, non_blocking=True)
+            e2e_step()
         torch.cuda.synchronize()
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         device_align(world)
         e0.record(stream)
         for s in range(args.steps):
-            view.copy_(hin, non_blocking=True)
-            call()
-            hout.copy_(view, non_blocking=True)
+            e2e_step()
         e1.record(stream)
         torch.cuda.synchronize()
         te = gather_max(e0.elapsed_time(e1) * 1e-3 / args.steps, world)
         nb = host.nbytes
         e2e = {"value": (S / te / 1e9) * (bus if world > 1 else 1.0),
                "unit": "GB/s", "us_per_step": te * 1e6,
-               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb}
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "how": how}
 
     if l2_mode == "flush":
         l2_desc = ("flushed before every timed call (256 MiB write, then 256 MiB read so no dirty "

@@ -160,6 +160,25 @@ TORUS_API int torus_allreduce(torus_comm_t comm, void* buf, size_t count, torus_
 TORUS_API int torus_allreduce_ex(torus_comm_t comm, void* buf, size_t count, torus_dtype_t dtype,
                        torus_dtype_t wire, torus_op_t op, torus_stream_t stream);
 
+/* End-to-end all-reduce of a HOST buffer (PAPER.md:54's all-reduce of the gradients,
+ * starting and ending in host memory): the `count` elements of `dtype` at host pointer
+ * `host` are copied to the device buffer `dev` (>= count elements on the comm's device,
+ * owned by the caller), all-reduced in place as torus_allreduce_ex(dev + k*piece, piece,
+ * dtype, wire, op) for each piece k in order, and copied back to `host`.  The three steps
+ * are pipelined over the pieces on two internal copy streams (piece k+1 travels host ->
+ * device and piece k-1 device -> host while piece k is reduced); `stream` is forked at the
+ * call and joined after the last copy, so work queued on `stream` afterwards sees the
+ * result in `host` once the stream reaches it.  piece == 0 or >= count: one piece.
+ * `host` should be pinned (cudaHostAlloc / cudaHostRegister): pageable memory works but
+ * its copies do not overlap.  The result equals torus_allreduce_ex on each piece, bit for
+ * bit (each piece is its own message: its own partition and fold order).
+ * Every rank must call it with the same count, piece, dtype, wire and op.
+ * Not for virtual comms (INVALID_ARG); not capturable in a CUDA graph.  Errors as
+ * torus_allreduce_ex, plus CUDA for a failed copy or event. */
+TORUS_API int torus_allreduce_host(torus_comm_t comm, void* host, void* dev, size_t count, size_t piece,
+                                   torus_dtype_t dtype, torus_dtype_t wire, torus_op_t op,
+                                   torus_stream_t stream);
+
 /* Virtual-rank variant (comm from torus_vcomm_init): bufs is a HOST array [N] of device
  * pointers, one buffer per virtual rank, all on the comm's device. */
 TORUS_API int torus_vallreduce(torus_comm_t comm, void* const* bufs, size_t count, torus_dtype_t dtype,

@@ -42,6 +42,7 @@ PROTOTYPES = {
     "torus_comm_route": (_c.c_char_p, [_vp, _sz, _i, _i]),
     "torus_allreduce": (_i, [_vp, _vp, _sz, _i, _i, _vp]),
     "torus_allreduce_ex": (_i, [_vp, _vp, _sz, _i, _i, _i, _vp]),
+    "torus_allreduce_host": (_i, [_vp, _vp, _vp, _sz, _sz, _i, _i, _i, _vp]),
     "torus_vallreduce": (_i, [_vp, _c.POINTER(_vp), _sz, _i, _i, _i, _vp]),
     "torus_allreduce_multi": (_i, [_vp, _c.POINTER(_vp), _c.POINTER(_sz), _i, _i, _i, _i, _vp]),
     "torus_comm_reserve": (_i, [_vp, _sz]),

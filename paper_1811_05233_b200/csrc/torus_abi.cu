@@ -101,6 +101,8 @@ struct torus_comm {
   void* d_staging = nullptr;              // multi-tensor staging buffer (wire type)
   size_t staging_bytes = 0;
   NvlsState nvls;                         // NVLS (multicast) variant, NEXT-4
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;  // torus_allreduce_host copy streams (lazy)
+  cudaEvent_t ev_fork = nullptr, ev_h2d = nullptr, ev_red = nullptr, ev_d2h = nullptr;
   size_t ll2_max = 0;                     // two-shot LL up to this many wire bytes (N >= 3)
   // ---- knobs, read ONCE at init (they must agree across ranks: torus_comm_config) ----
   int mode = 3;                           // kModeLL128 (default) / kModePush / kModePull / kModeTma
@@ -363,6 +365,10 @@ void read_knobs(torus_comm* c) {
 
 void destroy_resources(torus_comm* c) {
   nvls_release(&c->nvls);
+  for (cudaEvent_t e : {c->ev_fork, c->ev_h2d, c->ev_red, c->ev_d2h})
+    if (e) cudaEventDestroy(e);
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   for (void* p : c->opened) cudaIpcCloseMemHandle(p);
   for (auto& h : c->ipc_opened) cudaIpcCloseMemHandle(h.second);
   for (void* p : c->own_slabs) cudaFree(p);
@@ -1299,6 +1305,51 @@ int torus_allreduce_ex(torus_comm_t c, void* buf, size_t count, torus_dtype_t dt
 int torus_allreduce(torus_comm_t c, void* buf, size_t count, torus_dtype_t dtype, torus_op_t op,
                     torus_stream_t stream) {
   return torus_allreduce_ex(c, buf, count, dtype, dtype, op, stream);
+}
+
+int torus_allreduce_host(torus_comm_t c, void* host, void* dev, size_t count, size_t piece,
+                         torus_dtype_t dtype, torus_dtype_t wire, torus_op_t op, torus_stream_t stream_) {
+  if (!c || !host || !dev) return fail(TORUS_ERR_INVALID_ARG, "null argument");
+  if (c->virt) return fail(TORUS_ERR_INVALID_ARG, "virtual comm: not supported by torus_allreduce_host");
+  if (!valid_dtype(dtype)) return fail(TORUS_ERR_INVALID_ARG, "bad dtype code");
+  if (count == 0) return TORUS_OK;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+  if (!c->s_h2d) {  // lazily: two copy streams and the fork / join events
+    cudaError_t e = cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking);
+    for (cudaEvent_t* ev : {&c->ev_fork, &c->ev_h2d, &c->ev_red, &c->ev_d2h})
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_fail(e, "torus_allreduce_host setup");
+  }
+  const size_t esz = wire_size(dtype);
+  const size_t P = piece == 0 || piece > count ? count : piece;
+  char* h = static_cast<char*>(host);
+  char* d = static_cast<char*>(dev);
+  // fork: both copy streams start after the work already queued on `stream`
+  cudaError_t e = cudaEventRecord(c->ev_fork, stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->s_h2d, c->ev_fork, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->s_d2h, c->ev_fork, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "torus_allreduce_host fork");
+  // piece k: H2D on s_h2d -> all-reduce on `stream` -> D2H on s_d2h.  An event is re-recorded
+  // every piece: a wait binds to the record that precedes it, so two events suffice.
+  for (size_t off = 0; off < count; off += P) {
+    const size_t n = std::min(P, count - off);
+    e = cudaMemcpyAsync(d + off * esz, h + off * esz, n * esz, cudaMemcpyHostToDevice, c->s_h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(c->ev_h2d, c->s_h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, c->ev_h2d, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "torus_allreduce_host H2D");
+    void* bufs[1] = {d + off * esz};
+    const int rc = allreduce_impl(c, bufs, n, dtype, wire, op, stream);
+    if (rc) return rc;
+    e = cudaEventRecord(c->ev_red, stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c->s_d2h, c->ev_red, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h + off * esz, d + off * esz, n * esz, cudaMemcpyDeviceToHost, c->s_d2h);
+    if (e != cudaSuccess) return cuda_fail(e, "torus_allreduce_host D2H");
+  }
+  // join: `stream` continues after the last D2H (and the H2D stream has nothing left)
+  e = cudaEventRecord(c->ev_d2h, c->s_d2h);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, c->ev_d2h, 0);
+  return e == cudaSuccess ? TORUS_OK : cuda_fail(e, "torus_allreduce_host join");
 }
 
 int torus_vallreduce(torus_comm_t c, void* const* bufs, size_t count, torus_dtype_t dtype,

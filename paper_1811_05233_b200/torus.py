@@ -275,6 +275,23 @@ class TorusComm(_CommBase):
         return t
 
 
+    def all_reduce_host(self, host: torch.Tensor, dev: torch.Tensor, op: str = "mean",
+                        wire: torch.dtype | None = None, piece: int = 0,
+                        stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+        """All-reduce of a (pinned) CPU tensor through the device buffer `dev` (same dtype,
+        >= as many elements): H2D, all-reduce and D2H pipelined over pieces of `piece`
+        elements (torus_allreduce_host).  Asynchronous on `stream`; `host` holds the result
+        once the stream reaches it."""
+        if host.is_cuda or not host.is_contiguous() or not dev.is_cuda or not dev.is_contiguous():
+            raise ValueError("all_reduce_host needs a contiguous CPU tensor and a contiguous CUDA tensor")
+        if host.dtype != dev.dtype or dev.numel() < host.numel():
+            raise ValueError("dev must have host's dtype and at least as many elements")
+        check(_lib.load().torus_allreduce_host(
+            self._comm, ctypes.c_void_p(host.data_ptr()), ctypes.c_void_p(dev.data_ptr()), host.numel(),
+            piece, _dtype_code(host.dtype), _dtype_code(wire or host.dtype), OPS[op], _stream_ptr(stream)),
+            "torus_allreduce_host")
+        return host
+
     def register(self, t: torch.Tensor, group=None) -> torch.Tensor:
         """Collective: register `t` (a contiguous CUDA tensor every rank will pass to
         all_reduce) for zero-copy -- peers then read its inputs straight over NVLink

@@ -384,3 +384,62 @@ def test_back_to_back_calls_across_routes(tmp_path, world, X, Y):
         mp.spawn(_stream_worker, args=(world, _free_port(), errfile, X, Y), nprocs=world, join=True)
     except Exception as e:
         raise AssertionError(open(errfile).read() if os.path.exists(errfile) else str(e)) from None
+
+
+def _host_worker(rank, world, port, errfile):
+    """torus_allreduce_host: pinned host buffer -> device -> all-reduce -> host, pipelined
+    over pieces; each piece must equal the oracle on that piece (its own message)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    try:
+        import torch.distributed as dist
+
+        import oracle
+        import synthetic
+        from paper_1811_05233_b200 import TorusComm
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        X, Y = (1, 2) if world == 2 else (2, 2)
+        comm = TorusComm.init(X=X, Y=Y)
+        for dtype, wire, D, piece in [("f16", "f16", 1_000_003, 262_144), ("f32", "f16", 600_001, 0),
+                                      ("f32", "bf16", 300_007, 100_000), ("bf16", "bf16", 5_000, 1_024)]:
+            ins = synthetic.make_all("normal", D, world, dtype, salt=D % 97)
+            host = _to_dev(ins[rank], dtype, "cpu").pin_memory()
+            dev = torch.empty(D + 13, dtype=TD[dtype], device=f"cuda:{rank}")
+            torch.cuda.synchronize()
+            dist.barrier()
+            comm.all_reduce_host(host, dev, op="mean", wire=TD[wire], piece=piece)
+            torch.cuda.synchronize()
+            assert comm.async_error() == 0, "watchdog"
+            got = host.view(torch.int16).numpy().view(np.uint16) if dtype == "bf16" else host.numpy()
+            q = 16 // (2 if wire in ("f16", "bf16") else 4)
+            P = D if piece == 0 else piece
+            for off in range(0, D, P):
+                n = min(P, D - off)
+                R = comm.round_elems(TD[wire])
+                ref = oracle.torus_allreduce([a[off:off + n].copy() for a in ins], X, Y, dtype, wire=wire,
+                                             op="mean", q=q, round_elems=R)[rank]
+                ok, nbad = _same(got[off:off + n], ref)
+                assert ok, f"rank {rank} host {dtype}/{wire} D={D} piece@{off}: {nbad} mismatches"
+            dist.barrier()
+        dist.barrier()
+        comm.destroy()
+        dist.destroy_process_group()
+    except Exception:
+        with open(errfile, "a") as f:
+            f.write(f"rank {rank}:\n{traceback.format_exc()}\n")
+        raise
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_allreduce_host_pipelined(tmp_path, world):
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    errfile = str(tmp_path / "errors.txt")
+    try:
+        mp.spawn(_host_worker, args=(world, _free_port(), errfile), nprocs=world, join=True)
+    except Exception as e:
+        msg = open(errfile).read() if os.path.exists(errfile) else str(e)
+        raise AssertionError(msg) from None

@@ -233,6 +233,24 @@ def test_single_rank_cast_scale(cs_kernel, monkeypatch):
         vt.destroy()
 
 
+def test_allreduce_host_single_rank():
+    """torus_allreduce_host at N = 1 (the e2e path of the bench's 1-GPU line): pinned host
+    f32 buffer, fp16 / bf16 wire, pieces with a ragged last one -> the cast round trip."""
+    from paper_1811_05233_b200 import TorusComm
+    comm = TorusComm.init()
+    try:
+        for wire, D, piece in [("f16", 3_000_017, 1 << 20), ("bf16", 777_777, 0), ("f16", 13, 4)]:
+            x = synthetic.make("wide", D, 0, "f32")
+            host = torch.from_numpy(x.copy()).pin_memory()
+            dev = torch.empty(D, dtype=torch.float32, device="cuda")
+            comm.all_reduce_host(host, dev, op="mean", wire=TD[wire], piece=piece)
+            torch.cuda.synchronize()
+            ref = oracle.torus_allreduce([x], 1, 1, "f32", wire=wire, op="mean")[0]
+            assert_same(host.numpy(), ref, f"host N=1 {wire} D={D} piece={piece}")
+    finally:
+        comm.destroy()
+
+
 @pytest.mark.parametrize("kernel", ["ll128", "pull", "ldg"])
 def test_full_size_resnet50_exhaustive(kernel):
     """BASELINE config 2 at full size, in the bench's launch configuration (2x4 grid,
