@@ -352,7 +352,10 @@ void read_knobs(torus_comm* c) {
   c->pull_ctas = (int)env_size("TORUS_PULL_CTAS", 0);
   c->pull_fence = (int)env_size("TORUS_PULL_FENCE", 3);
   c->pull_zc = (int)env_size("TORUS_PULL_ZC", 1);
-  c->ll128_ctas = (int)env_size("TORUS_LL128_CTAS", 0);
+  // LL128 CTAs (per device): TORUS_LL128_CTAS, else (one rank per process) the comm's CTA
+  // budget TORUS_CTAS, set by TorusComm.init(ctas=...) so that concurrent comms' spinning
+  // kernels co-reside, else all SMs
+  c->ll128_ctas = (int)env_size("TORUS_LL128_CTAS", c->virt ? 0 : env_size("TORUS_CTAS", 0));
   if (const char* w = getenv("TORUS_LL128_W"))
     sscanf(w, "%f,%f,%f,%f,%f", &c->ll128_w[0], &c->ll128_w[1], &c->ll128_w[2], &c->ll128_w[3], &c->ll128_w[4]);
   c->check = (int)env_size("TORUS_CHECK", 0);
@@ -1062,7 +1065,7 @@ int launch_pull_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype
 }
 
 int launch_ll128_rounds(torus_comm* c, void* const* bufs, size_t count, int dtype, int wire, int op,
-                        bool aligned, cudaStream_t stream) {
+                        bool aligned, cudaStream_t stream, const MultiSeg* segs = nullptr, int nseg = 0) {
   const unsigned long long R = round_elems(c, wire), sw = wire_size(wire);
   const int X = c->X, Y = c->Y, q = (int)(kVecBytes / sw);
   const unsigned long long UE = 30ull * q;  // elements per unit
@@ -1070,6 +1073,8 @@ int launch_ll128_rounds(torus_comm* c, void* const* bufs, size_t count, int dtyp
   memset(&a, 0, sizeof a);
   a.ranks = c->d_ranks;
   for (int l = 0; l < c->nlocal; ++l) a.buf[l] = bufs[l];
+  a.segs = segs;  // NEXT-1 fused multi-tensor call: the buffer is a concatenation of tensors
+  a.nseg = nseg;
   a.nlocal = c->nlocal;
   a.op = op;
   a.inv_n = 1.0f / (float)(X * Y);
@@ -1199,7 +1204,7 @@ int allreduce_impl(torus_comm* c, void* const* bufs, size_t count, int dtype, in
     if (rc) return rc;
     return launch_pull_rounds(c, bufs, count, dtype, wire, op, aligned, stream);
   }
-  if (route == kRouteLL128 && !nseg) return launch_ll128_rounds(c, bufs, count, dtype, wire, op, aligned, stream);
+  if (route == kRouteLL128) return launch_ll128_rounds(c, bufs, count, dtype, wire, op, aligned, stream, segs, nseg);
   LaunchArgs a;
   memset(&a, 0, sizeof a);
   a.ranks = c->d_ranks;

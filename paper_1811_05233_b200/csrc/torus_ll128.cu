@@ -134,7 +134,7 @@ __device__ __forceinline__ bool get2(const char* p0, const char* p1, int lane, u
   }
 }
 
-template <int DT, int W>
+template <int DT, int W, bool MULTI>
 __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128Args a) {
   using Acc = typename Wire<W>::Acc;
   constexpr int VE = Wire<W>::VE;
@@ -168,12 +168,20 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
     const long long r = (long long)sl - (long long)(u * UE + eoff);
     return r <= 0 ? 0 : (r < cnt ? (int)r : cnt);
   };
-  // my buffer at element e of the round
+  // my buffer at element e of the round: one flat buffer, or (MULTI, NEXT-1) the
+  // concatenation of a bucket's tensors -- a separate instantiation, so the flat path
+  // keeps its register budget
+  const MultiSeg* const segs = MULTI ? a.segs + (size_t)lr * a.nseg : nullptr;
+  int seg_hint = 0;
   auto uload = [&](unsigned long long e, int nrem) -> uint4 {
-    return nrem > 0 ? load_user<DT, W>(buf, a.buf_off + e, nrem, aligned && nrem == VE) : zero;
+    if (nrem <= 0) return zero;
+    if constexpr (MULTI) return load_user_seg<DT, W>(segs, a.nseg, a.buf_off + e, nrem, seg_hint);
+    else return load_user<DT, W>(buf, a.buf_off + e, nrem, aligned && nrem == VE);
   };
   auto ustore = [&](unsigned long long e, int nrem, uint4 v) {
-    if (nrem > 0) store_user<DT, W>(buf, a.buf_off + e, nrem, v, aligned && nrem == VE);
+    if (nrem <= 0) return;
+    if constexpr (MULTI) store_user_seg<DT, W>(segs, a.nseg, a.buf_off + e, nrem, v, seg_hint);
+    else store_user<DT, W>(buf, a.buf_off + e, nrem, v, aligned && nrem == VE);
   };
   auto inbox = [&](int rank, unsigned long long off, unsigned long long stride, int slot) -> char* {
     return R->ws[rank] + off + (unsigned long long)slot * stride;
@@ -371,11 +379,14 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
 template <int DT, int W>
 cudaError_t launch_ll128_typed(const L128Args& a, bool cooperative, cudaStream_t stream) {
   const dim3 grid(a.nlocal * a.ctas), block(kL128Threads);
+  const void* fn = a.nseg > 0 ? (const void*)torus_ll128_kernel<DT, W, true>
+                              : (const void*)torus_ll128_kernel<DT, W, false>;
   if (cooperative) {
     void* args[] = {const_cast<L128Args*>(&a)};
-    return cudaLaunchCooperativeKernel((const void*)torus_ll128_kernel<DT, W>, grid, block, args, 0, stream);
+    return cudaLaunchCooperativeKernel(fn, grid, block, args, 0, stream);
   }
-  torus_ll128_kernel<DT, W><<<grid, block, 0, stream>>>(a);
+  if (a.nseg > 0) torus_ll128_kernel<DT, W, true><<<grid, block, 0, stream>>>(a);
+  else torus_ll128_kernel<DT, W, false><<<grid, block, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

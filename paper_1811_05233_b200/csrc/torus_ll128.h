@@ -22,6 +22,8 @@ struct L128Args {
   int op;                        // 0 sum, 1 mean
   float inv_n;                   // f32(1/N)
   int aligned;                   // all user buffers 16-byte aligned
+  const MultiSeg* segs;          // NEXT-1: device table [nlocal][nseg] of the bucket's tensors
+  int nseg;                      //   (nullptr / 0: one flat buffer per rank)
   // round geometry, host-computed: chunk j offset, sub-chunk (j, s) at [j*Y+s]:
   // offset inside the chunk, length, units (30 wire vectors each), unit offset of the
   // sub-chunk inside its chunk's stream

@@ -443,3 +443,63 @@ def test_allreduce_host_pipelined(tmp_path, world):
     except Exception as e:
         msg = open(errfile).read() if os.path.exists(errfile) else str(e)
         raise AssertionError(msg) from None
+
+
+def _concurrent_worker(rank, world, port, errfile):
+    """Two communicators with split CTA budgets (TorusComm.init(ctas=SMs/2)) running the
+    LL128 kernel concurrently on two streams: both kernels must co-reside (their CTAs spin
+    on peers) and both results must equal the oracle."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    try:
+        import torch.distributed as dist
+
+        import oracle
+        import synthetic
+        from paper_1811_05233_b200 import TorusComm
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        X, Y = (1, 2) if world == 2 else (2, 2)
+        sms = torch.cuda.get_device_properties(rank).multi_processor_count
+        comms = [TorusComm.init(X=X, Y=Y, ctas=sms // 2) for _ in range(2)]
+        streams = [torch.cuda.Stream() for _ in range(2)]
+        D = 4_000_037  # 8 MB of f16: above the one-shot / two-shot thresholds at N = 2 and 4
+        ins = [synthetic.make_all("normal", D, world, "f16", salt=s) for s in (5, 6)]
+        assert comms[0].route(D, torch.float16) == "torus_ll128_kernel"
+        for rep in range(3):
+            ts = [_to_dev(ins[k][rank], "f16", f"cuda:{rank}") for k in range(2)]
+            torch.cuda.synchronize()
+            dist.barrier()
+            for k in range(2):
+                with torch.cuda.stream(streams[k]):
+                    comms[k].all_reduce(ts[k], op="mean", stream=streams[k])
+            torch.cuda.synchronize()
+            for k in range(2):
+                assert comms[k].async_error() == 0, "watchdog"
+                ref = oracle.torus_allreduce(ins[k], X, Y, "f16", wire="f16", op="mean", q=8,
+                                             round_elems=comms[k].round_elems(torch.float16))[rank]
+                ok, nbad = _same(_from_dev(ts[k], "f16"), ref)
+                assert ok, f"rank {rank} comm {k} rep {rep}: {nbad} mismatches"
+            dist.barrier()
+        for c in comms:
+            dist.barrier()
+            c.destroy()
+        dist.destroy_process_group()
+    except Exception:
+        with open(errfile, "a") as f:
+            f.write(f"rank {rank}:\n{traceback.format_exc()}\n")
+        raise
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_concurrent_comms_split_ctas(tmp_path, world):
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    errfile = str(tmp_path / "errors.txt")
+    try:
+        mp.spawn(_concurrent_worker, args=(world, _free_port(), errfile), nprocs=world, join=True)
+    except Exception as e:
+        msg = open(errfile).read() if os.path.exists(errfile) else str(e)
+        raise AssertionError(msg) from None
