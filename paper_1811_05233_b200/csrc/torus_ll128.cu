@@ -173,15 +173,49 @@ __global__ void __launch_bounds__(kL128Threads, 1) torus_ll128_kernel(const L128
   // keeps its register budget
   const MultiSeg* const segs = MULTI ? a.segs + (size_t)lr * a.nseg : nullptr;
   int seg_hint = 0;
+  // (flat: the whole-vector case is decided first and written out here, so the ragged
+  // path's per-element arrays stay in its own cold branch instead of local memory on
+  // every call)
   auto uload = [&](unsigned long long e, int nrem) -> uint4 {
     if (nrem <= 0) return zero;
-    if constexpr (MULTI) return load_user_seg<DT, W>(segs, a.nseg, a.buf_off + e, nrem, seg_hint);
-    else return load_user<DT, W>(buf, a.buf_off + e, nrem, aligned && nrem == VE);
+    if constexpr (MULTI) {
+      return load_user_seg<DT, W>(segs, a.nseg, a.buf_off + e, nrem, seg_hint);
+    } else {
+      if (aligned && nrem == VE) {
+        using T = typename Elem<DT>::T;
+        const T* p = reinterpret_cast<const T*>(buf) + a.buf_off + e;
+        if constexpr (DT == W) {
+          return __ldcs(reinterpret_cast<const uint4*>(p));
+        } else {
+          const float4 x0 = __ldcs(reinterpret_cast<const float4*>(p));
+          const float4 x1 = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+          const float f[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          return pack<W>(f);
+        }
+      }
+      return load_user<DT, W>(buf, a.buf_off + e, nrem, false);
+    }
   };
   auto ustore = [&](unsigned long long e, int nrem, uint4 v) {
     if (nrem <= 0) return;
-    if constexpr (MULTI) store_user_seg<DT, W>(segs, a.nseg, a.buf_off + e, nrem, v, seg_hint);
-    else store_user<DT, W>(buf, a.buf_off + e, nrem, v, aligned && nrem == VE);
+    if constexpr (MULTI) {
+      store_user_seg<DT, W>(segs, a.nseg, a.buf_off + e, nrem, v, seg_hint);
+    } else {
+      if (aligned && nrem == VE) {
+        using T = typename Elem<DT>::T;
+        T* p = reinterpret_cast<T*>(buf) + a.buf_off + e;
+        if constexpr (DT == W) {
+          __stcs(reinterpret_cast<uint4*>(p), v);
+        } else {
+          float f[8];
+          unpack<W>(v, f);
+          __stcs(reinterpret_cast<float4*>(p), make_float4(f[0], f[1], f[2], f[3]));
+          __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(f[4], f[5], f[6], f[7]));
+        }
+        return;
+      }
+      store_user<DT, W>(buf, a.buf_off + e, nrem, v, false);
+    }
   };
   auto inbox = [&](int rank, unsigned long long off, unsigned long long stride, int slot) -> char* {
     return R->ws[rank] + off + (unsigned long long)slot * stride;
