@@ -503,3 +503,68 @@ def test_concurrent_comms_split_ctas(tmp_path, world):
     except Exception as e:
         msg = open(errfile).read() if os.path.exists(errfile) else str(e)
         raise AssertionError(msg) from None
+
+
+def _oversub_worker(rank, world, port, ngpu, errfile):
+    """The 8-rank 2x4 headline grid as 8 real processes on `ngpu` GPUs (8 / ngpu ranks per
+    GPU, each comm capped to its share of the SMs so the spinning kernels co-reside): CUDA
+    IPC between every pair of processes, NVLink between GPUs, the LL128 kernel at 2x4."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    try:
+        import torch.distributed as dist
+
+        import oracle
+        import synthetic
+        from paper_1811_05233_b200 import TorusComm
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+                          TORUS_LL_MAX_BYTES="0", TORUS_LL2_MAX_BYTES="0")
+        dev = rank % ngpu
+        torch.cuda.set_device(dev)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        comm = TorusComm.init(X=2, Y=4, ctas=sms // (world // ngpu))
+        assert comm.route(1_000_003, torch.float16) == "torus_ll128_kernel"
+        for dtype, wire, D in [("f16", "f16", 1_000_003), ("f32", "f16", 300_007), ("bf16", "bf16", 200_003),
+                               ("f16", "f16", synthetic.RESNET50_NUMEL)]:
+            ins = synthetic.make_all("grad" if dtype == "f16" else "normal", D, world, dtype, salt=D % 83)
+            t = _to_dev(ins[rank], dtype, f"cuda:{dev}")
+            torch.cuda.synchronize()
+            dist.barrier()
+            comm.all_reduce(t, op="mean", wire=TD[wire])
+            torch.cuda.synchronize()
+            assert comm.async_error() == 0, "watchdog"
+            got = _from_dev(t, dtype)
+            q = 16 // (2 if wire in ("f16", "bf16") else 4)
+            R = comm.round_elems(TD[wire])
+            if D <= 1_000_003:
+                ref = oracle.torus_allreduce(ins, 2, 4, dtype, wire=wire, op="mean", q=q, round_elems=R)[rank]
+                ok, nbad = _same(got, ref)
+            else:
+                g = np.random.Generator(np.random.PCG64(rank))
+                idx = np.unique(np.concatenate([g.integers(0, D, 4000), [0, D - 1]]))
+                ref = oracle.torus_elements(ins, 2, 4, idx, dtype, wire=wire, op="mean", q=q, round_elems=R)
+                ok, nbad = _same(got[idx], ref)
+            assert ok, f"rank {rank} 2x4 {dtype}/{wire} D={D}: {nbad} mismatches"
+            dist.barrier()
+        dist.barrier()
+        comm.destroy()
+        dist.destroy_process_group()
+    except Exception:
+        with open(errfile, "a") as f:
+            f.write(f"rank {rank}:\n{traceback.format_exc()}\n")
+        raise
+
+
+def test_eight_ranks_2x4_oversubscribed(tmp_path):
+    """N = 8, 2x4 (BASELINE.json's headline grid) on the GPUs this box has (4 or 2)."""
+    import torch.multiprocessing as mp
+    ngpu = torch.cuda.device_count()
+    if ngpu < 2 or 8 % ngpu:
+        pytest.skip("needs 2, 4 or 8 GPUs")
+    errfile = str(tmp_path / "errors.txt")
+    try:
+        mp.spawn(_oversub_worker, args=(8, _free_port(), ngpu, errfile), nprocs=8, join=True)
+    except Exception as e:
+        msg = open(errfile).read() if os.path.exists(errfile) else str(e)
+        raise AssertionError(msg) from None
