@@ -117,6 +117,7 @@ struct torus_comm {
   int pull_zc = 1;                        // pull kernel: zero-copy from registered buffers
   int ll128_ctas = 0;                     // LL128 kernel: CTAs per rank (0 = one per SM)
   float ll128_w[5] = {1.f, 1.f, 1.f, 1.f, 1.f};  // LL128 kernel: warp weight per stage
+  int ll128_lane = 16;                    // LL128 kernel: bytes per lane per line store (16 / 32)
   int check = 0;                          // TORUS_CHECK=1: per-call header check (MISMATCH)
   int fault = 0;                          // TORUS_FAULT: negative-control fault injection (tests)
   unsigned delay_ns = 0;                  // TORUS_DELAY_NS: random per-CTA start delay (tests)
@@ -356,6 +357,7 @@ void read_knobs(torus_comm* c) {
   // budget TORUS_CTAS, set by TorusComm.init(ctas=...) so that concurrent comms' spinning
   // kernels co-reside, else all SMs
   c->ll128_ctas = (int)env_size("TORUS_LL128_CTAS", c->virt ? 0 : env_size("TORUS_CTAS", 0));
+  c->ll128_lane = (int)env_size("TORUS_LL128_LANE", 16) == 32 ? 32 : 16;
   if (const char* w = getenv("TORUS_LL128_W"))
     sscanf(w, "%f,%f,%f,%f,%f", &c->ll128_w[0], &c->ll128_w[1], &c->ll128_w[2], &c->ll128_w[3], &c->ll128_w[4]);
   c->check = (int)env_size("TORUS_CHECK", 0);
@@ -1068,7 +1070,11 @@ int launch_ll128_rounds(torus_comm* c, void* const* bufs, size_t count, int dtyp
                         bool aligned, cudaStream_t stream, const MultiSeg* segs = nullptr, int nseg = 0) {
   const unsigned long long R = round_elems(c, wire), sw = wire_size(wire);
   const int X = c->X, Y = c->Y, q = (int)(kVecBytes / sw);
-  const unsigned long long UE = 30ull * q;  // elements per unit
+  // 32-byte lanes (TORUS_LL128_LANE=32) for flat calls: 60 vectors per 1 KiB unit, 512-thread
+  // CTAs; multi-tensor buckets keep 16-byte lanes (30 vectors per 512-byte unit, 1024 threads)
+  const int lane_bytes = (nseg == 0 && c->ll128_lane == 32) ? 32 : 16;
+  const unsigned long long UE = (lane_bytes == 32 ? 60ull : 30ull) * q;  // elements per unit
+  const unsigned long long unit_bytes = lane_bytes == 32 ? 2ull * kL128Unit : (unsigned long long)kL128Unit;
   L128Args a;
   memset(&a, 0, sizeof a);
   a.ranks = c->d_ranks;
@@ -1083,7 +1089,8 @@ int launch_ll128_rounds(torus_comm* c, void* const* bufs, size_t count, int dtyp
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   a.ctas = std::max(1, (c->ll128_ctas > 0 ? std::min(c->ll128_ctas, sms) : sms) / c->nlocal);
-  const int warps = a.ctas * kL128CtaWarps;
+  a.lane_bytes = lane_bytes;
+  const int warps = a.ctas * (lane_bytes == 32 ? 16 : kL128CtaWarps);
   // warps per stage ~ each stage's loads + stores per unit x units (x TORUS_LL128_W)
   // (B with Y == 1 also pushes its final values to the X-1 row peers)
   double w[5] = {X > 1 ? 2.0 * (X - 1) * Y : 0, (double)Y * (X + (Y > 1 ? 1 : X)), Y > 1 ? 2.0 * Y + X - 1 : 0,
@@ -1138,8 +1145,8 @@ int launch_ll128_rounds(torus_comm* c, void* const* bufs, size_t count, int dtyp
       chunk_units_max = std::max(chunk_units_max, cu);
     }
     a.Umax = (int)umax;
-    a.h_stride = a.hag_stride = chunk_units_max * kL128Unit;
-    a.v_stride = a.ag_stride = umax * kL128Unit;
+    a.h_stride = a.hag_stride = chunk_units_max * unit_bytes;
+    a.v_stride = a.ag_stride = umax * unit_bytes;
     unsigned long long off = c->layout.data_off;
     for (int p = 0; p < 2; ++p) {
       a.h_off[p] = off;
@@ -1689,7 +1696,7 @@ int torus_comm_config(torus_comm_t c, unsigned long long* words, int n) {
       (unsigned long long)c->G, c->slab_size, c->layout.data_off, c->layout.ll_off,
       c->layout.ll_slot, c->layout.ll_region, c->layout.pull_flag_off, c->ll2_max,
       (unsigned long long)c->mode, (unsigned long long)c->tile_vecs, c->one_tile_max, c->mid_tiles,
-      (unsigned long long)tv16, (unsigned long long)tv32, c->timeout_ns};
+      (unsigned long long)tv16, (unsigned long long)tv32, c->timeout_ns, (unsigned long long)c->ll128_lane};
   const int m = (int)(sizeof v / sizeof v[0]);
   for (int i = 0; i < n; ++i) words[i] = i < m ? v[i] : 0;
   return m;

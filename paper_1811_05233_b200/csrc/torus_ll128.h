@@ -6,7 +6,7 @@
 namespace torus {
 
 constexpr int kL128Line = 128;      // bytes per line: 120 bytes of data + an 8-byte flag
-constexpr int kL128Unit = 4 * kL128Line;  // one warp moves four lines = 30 wire vectors
+constexpr int kL128Unit = 4 * kL128Line;  // 16-byte lanes: one warp moves four lines = 30 wire vectors
 #ifndef TORUS_LL128_THREADS
 #define TORUS_LL128_THREADS 1024
 #endif
@@ -36,6 +36,7 @@ struct L128Args {
   int wk[5];                     // warps per rank of each stage: A, B, C, D, E
   int wsum;                      // warps per rank
   int ctas;                      // CTAs per rank
+  int lane_bytes;                // 16 (1024-thread CTAs) or 32 (512-thread CTAs, flat calls only)
 };
 
 cudaError_t launch_ll128(const L128Args& a, int dtype, int wire, bool cooperative, cudaStream_t stream);
