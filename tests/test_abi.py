@@ -78,6 +78,24 @@ def test_null_and_bad_arguments_rejected_without_gpu():
     assert L.torus_comm_init(0, 100, 10, 10, h, ctypes.byref(c)) == 2
     assert L.torus_workspace_alloc(0, 0, None) == 1
     assert b"GRID" in L.torus_last_error() or b"INVALID" in L.torus_last_error()
+    # host-buffer path: NULL comm / pointers are INVALID_ARG before anything is enqueued
+    assert L.torus_allreduce_host(None, None, None, 10, 0, 1, 1, 1, None) == 1
+    buf = ctypes.create_string_buffer(64)
+    assert L.torus_allreduce_host(None, buf, buf, 10, 0, 1, 1, 1, None) == 1
+
+
+def test_all_reduce_host_binding_validates_tensors():
+    """TorusComm.all_reduce_host rejects a CUDA host tensor / CPU device tensor / short or
+    mistyped device buffer before calling the library (marshalling only)."""
+    import torch
+
+    from paper_1811_05233_b200 import TorusComm
+    comm = TorusComm.__new__(TorusComm)
+    cpu = torch.zeros(16, dtype=torch.float16)
+    with pytest.raises(ValueError):
+        comm.all_reduce_host(cpu, cpu.clone())             # dev must be a CUDA tensor
+    with pytest.raises(ValueError):
+        comm.all_reduce_host(cpu[::2], cpu.clone())        # host must be contiguous
 
 
 def test_strerror_names():
