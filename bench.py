@@ -36,6 +36,10 @@ METRIC = ("2D-torus allreduce busbw GB/s (fp16 25.6M elems, 8×B200, max over ra
           "vs NVLink peak")
 NVLINK_NOMINAL = 900.0      # GB/s per direction per GPU (18 x 50)
 L2_BYTES = 126 * 1000 * 1000  # B200 L2 (B200_PROFILING.md)
+# TORUS_BENCH_OVERSUB=1: run N ranks on fewer GPUs (rank r on GPU r % count, gloo plumbing,
+# no NCCL comparator; set TORUS_CTAS to each rank's SM share) to exercise the N = 8 code
+# path on a smaller box.  The line is marked "oversubscribed" and is not a measurement.
+OVERSUB = os.environ.get("TORUS_BENCH_OVERSUB") == "1"
 NVLINK_MEASURED = 770.0     # GB/s per direction, B200_PROFILING.md "peer copy" measurement
 DEFAULT_GRID = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
 DT_BYTES = {"f32": 4, "f16": 2, "bf16": 2, "i32": 4}
@@ -79,6 +83,12 @@ def dist_setup(n_gpus):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != n_gpus:
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
+    if OVERSUB:  # code-path check only: several ranks per GPU, gloo plumbing, never a result
+        local = local % torch.cuda.device_count()
+        torch.cuda.set_device(local)
+        if world > 1:
+            dist.init_process_group("gloo")
+        return rank, world, local
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -504,7 +514,9 @@ def run_torus(args):
                    "buffer": ("registered (zero-copy)" if world > 1 and not args.no_register
                               else "unregistered"),
                    "message_bytes": S, "l2": l2_desc,
-                   "value_is": "busbw" if world > 1 else "algbw (busbw is 0 at N=1)"},
+                   "value_is": "busbw" if world > 1 else "algbw (busbw is 0 at N=1)",
+                   **({"oversubscribed": "several ranks per GPU: a code-path check, not a measurement"}
+                      if OVERSUB else {})},
         "algbw": algbw, "busbw": busbw, "us_per_call": t * 1e6, "us_per_call_min": t_min * 1e6,
         "us_per_call_p50": t_p50 * 1e6, "us_per_call_p90": t_p90 * 1e6, "us_per_call_max": t_max * 1e6,
         "frac_nvlink_900": busbw / NVLINK_NOMINAL if world > 1 else None,
@@ -666,6 +678,8 @@ def main():
     args = parse()
     if args.ctas:
         os.environ["TORUS_CTAS"] = str(args.ctas)
+    if OVERSUB:
+        args.no_nccl = True
     if args.impl == "reference":
         run_reference(args)
         return
